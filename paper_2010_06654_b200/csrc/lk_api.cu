@@ -1,0 +1,510 @@
+// lk_api.cu -- the extern "C" boundary declared in include/lloydkit_b200.h.
+//
+// A context owns no device memory of its own: every buffer is carved out of
+// the caller's workspace at fixed, 256-byte aligned offsets, so the Python
+// host (torch) accounts for all of HBM and can view any buffer as a tensor.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "lk_common.cuh"
+#include "lk_internal.h"
+
+namespace lkh {
+
+static thread_local char g_err[1024] = {0};
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+}  // namespace lkh
+
+using lkh::set_error;
+
+namespace {
+
+enum InternalBuf {
+    B_X32 = 0, B_X64, B_C64, B_LABELS, B_UB, B_LB, B_DELTA, B_STATS, B_SSE, B_GROUP_OF, B_COUNTS,
+    B_QEXP,
+    // internal
+    B_C64_PREV, B_C32, B_CNORM, B_DRIFT, B_SHALF, B_GDRIFT, B_SCAL, B_MOVED, B_FLAGGED, B_WORK,
+    B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
+    B_COUNT_
+};
+
+struct Layout {
+    uint64_t off[B_COUNT_];
+    uint64_t size[B_COUNT_];
+    uint64_t total;
+    int64_t ldx, ldc, delta_len;
+    int32_t nlb, groups;
+};
+
+static uint64_t align256(uint64_t v) { return (v + 255) & ~uint64_t(255); }
+
+static int32_t nlb_for(const lk_config& c, int32_t* groups) {
+    int32_t g = 1;
+    switch (c.strategy) {
+        case LK_STRAT_LLOYD: g = 0; break;
+        case LK_STRAT_HAMERLY: g = 1; break;
+        case LK_STRAT_ELKAN: g = c.k; break;
+        default: g = c.groups > 0 ? c.groups : (c.k + 9) / 10; break;
+    }
+    if (g > c.k) g = c.k;
+    *groups = g;
+    return g < 1 ? 1 : g;
+}
+
+static bool make_layout(const lk_config& c, Layout* L) {
+    if (c.n_local < 0 || c.d < 1 || c.k < 1 || c.t_max < 0 || c.n_total < c.n_local) return false;
+    if (c.n_local > 0x7fffffffLL) return false;  // row ids are int32 on device
+    memset(L, 0, sizeof(*L));
+    L->ldx = (c.d <= 2) ? c.d : ((c.d + 3) / 4) * 4;
+    L->ldc = ((c.d + 3) / 4) * 4;
+    L->nlb = nlb_for(c, &L->groups);
+    L->delta_len = (int64_t)c.k * c.d + 2 * (int64_t)c.k + 8;
+    const int64_t n = c.n_local, k = c.k, d = c.d;
+    const int64_t tm = c.t_max > 0 ? c.t_max : 1;
+    L->size[B_X32] = (uint64_t)n * L->ldx * 4;
+    L->size[B_X64] = c.has_x64 ? (uint64_t)n * d * 8 : 0;
+    L->size[B_C64] = (uint64_t)k * d * 8;
+    L->size[B_LABELS] = (uint64_t)n * 4;
+    L->size[B_UB] = c.strategy == LK_STRAT_LLOYD ? 0 : (uint64_t)n * 4;
+    L->size[B_LB] = c.strategy == LK_STRAT_LLOYD ? 0 : (uint64_t)n * L->nlb * 4;
+    L->size[B_DELTA] = (uint64_t)L->delta_len * 8;
+    L->size[B_STATS] = (uint64_t)tm * LK_NSTAT * 8;
+    L->size[B_SSE] = (uint64_t)tm * 8;
+    L->size[B_GROUP_OF] = (uint64_t)k * 4;
+    L->size[B_COUNTS] = (uint64_t)k * 8;
+    L->size[B_QEXP] = (uint64_t)(d + 1) * 4;
+    L->size[B_C64_PREV] = (uint64_t)k * d * 8;
+    L->size[B_C32] = (uint64_t)k * L->ldc * 4;
+    L->size[B_CNORM] = (uint64_t)k * 4;
+    L->size[B_DRIFT] = (uint64_t)k * 4;
+    L->size[B_SHALF] = (uint64_t)k * 4;
+    L->size[B_GDRIFT] = (uint64_t)(L->groups > 0 ? L->groups : 1) * 4;
+    L->size[B_SCAL] = 8 * 4;
+    L->size[B_MOVED] = (uint64_t)n * 8;
+    L->size[B_FLAGGED] = (uint64_t)n * 4;
+    L->size[B_WORK] = c.strategy == LK_STRAT_LLOYD ? 0 : (uint64_t)n * 4;
+    L->size[B_SUMS] = (uint64_t)k * d * 8;
+    L->size[B_QSUM] = (uint64_t)k * 8;
+    L->size[B_QSCALE] = (uint64_t)(d + 1) * 8;
+    L->size[B_QINV] = (uint64_t)(d + 1) * 8;
+    L->size[B_DONE] = 16;
+    L->size[B_SSE_PART] = (uint64_t)k * 8;
+    L->size[B_PW_PROG] = 4096 * 4;
+    uint64_t off = 0;
+    for (int b = 0; b < B_COUNT_; b++) {
+        L->off[b] = off;
+        off = align256(off + L->size[b]);
+    }
+    L->total = off;
+    return true;
+}
+
+// numpy pairwise_sum association tree for a length-d reduction, as a postfix
+// program: (0, start, len) = leaf, (1, 0, 0) = add the two top values.
+static void build_pw(int start, int n, std::vector<int32_t>& prog) {
+    if (n <= 128) {
+        prog.push_back(0);
+        prog.push_back(start);
+        prog.push_back(n);
+        return;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    build_pw(start, n2, prog);
+    build_pw(start + n2, n - n2, prog);
+    prog.push_back(1);
+    prog.push_back(0);
+    prog.push_back(0);
+}
+
+}  // namespace
+
+struct lk_ctx {
+    lk_config cfg;
+    Layout L;
+    uint8_t* ws;
+    lk::DevState S;
+    int sms;
+    bool quant_set;
+    bool centroids_set;
+    int64_t launches;
+    // profiling
+    bool profile;
+    struct Rec { int cls; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+};
+
+namespace {
+
+template <typename T>
+T* buf(lk_ctx* c, int b) {
+    return c->L.size[b] ? reinterpret_cast<T*>(c->ws + c->L.off[b]) : nullptr;
+}
+
+cudaEvent_t take_event(lk_ctx* c) {
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    lk_ctx* c;
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    ProfScope(lk_ctx* c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
+        if (c->profile) {
+            a = take_event(c);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (c->profile) {
+            cudaEvent_t b = take_event(c);
+            cudaEventRecord(b, st);
+            c->recs.push_back({cls, a, b});
+        }
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+int32_t lk_version(void) { return 1; }
+
+const char* lk_last_error(void) { return lkh::g_err; }
+
+lk_status lk_workspace_bytes(const lk_config* cfg, uint64_t* bytes) {
+    if (!cfg || !bytes) return LK_ERR_ARG;
+    Layout L;
+    if (!make_layout(*cfg, &L)) {
+        set_error("invalid configuration");
+        return LK_ERR_ARG;
+    }
+    *bytes = L.total;
+    return LK_OK;
+}
+
+lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uint64_t bytes) {
+    if (!out || !cfg || !workspace) {
+        set_error("null argument");
+        return LK_ERR_ARG;
+    }
+    if (cfg->strategy < LK_STRAT_LLOYD || cfg->strategy > LK_STRAT_REGROUP) {
+        set_error("unknown strategy id %d", cfg->strategy);
+        return LK_ERR_ARG;
+    }
+    if (cfg->strategy != LK_STRAT_LLOYD && cfg->strategy != LK_STRAT_HAMERLY) {
+        set_error("strategy %d not available in this build", cfg->strategy);
+        return LK_ERR_UNSUPPORTED;
+    }
+    Layout L;
+    if (!make_layout(*cfg, &L)) {
+        set_error("invalid configuration (n=%lld d=%d k=%d)", (long long)cfg->n_local, cfg->d,
+                  cfg->k);
+        return LK_ERR_ARG;
+    }
+    if (bytes < L.total) {
+        set_error("workspace too small: %llu < %llu", (unsigned long long)bytes,
+                  (unsigned long long)L.total);
+        return LK_ERR_ARG;
+    }
+    LK_CUDA_CHECK(cudaSetDevice(cfg->device));
+    lk_ctx* c = new lk_ctx();
+    c->cfg = *cfg;
+    c->L = L;
+    c->ws = reinterpret_cast<uint8_t*>(workspace);
+    c->quant_set = false;
+    c->centroids_set = false;
+    c->launches = 0;
+    c->profile = false;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    c->sms = sms;
+
+    lk::DevState& S = c->S;
+    memset(&S, 0, sizeof(S));
+    S.n = cfg->n_local;
+    S.d = cfg->d;
+    S.k = cfg->k;
+    S.ldx = (int32_t)L.ldx;
+    S.ldc = (int32_t)L.ldc;
+    S.nlb = L.nlb;
+    S.strategy = cfg->strategy;
+    S.t_groups = L.groups;
+    S.X32 = buf<float>(c, B_X32);
+    S.X64 = buf<double>(c, B_X64);
+    S.C64 = buf<double>(c, B_C64);
+    S.C64_prev = buf<double>(c, B_C64_PREV);
+    S.C32 = buf<float>(c, B_C32);
+    S.cnorm = buf<float>(c, B_CNORM);
+    S.drift = buf<float>(c, B_DRIFT);
+    S.s_half = buf<float>(c, B_SHALF);
+    S.gdrift = (cfg->strategy == LK_STRAT_YINYANG || cfg->strategy == LK_STRAT_ELKAN ||
+                cfg->strategy == LK_STRAT_REGROUP)
+                   ? buf<float>(c, B_GDRIFT)
+                   : nullptr;
+    S.scal = buf<float>(c, B_SCAL);
+    S.group_of = buf<int32_t>(c, B_GROUP_OF);
+    S.labels = buf<int32_t>(c, B_LABELS);
+    S.ub = buf<float>(c, B_UB);
+    S.lb = buf<float>(c, B_LB);
+    S.moved = buf<int2>(c, B_MOVED);
+    S.flagged = buf<int32_t>(c, B_FLAGGED);
+    S.work = buf<int32_t>(c, B_WORK);
+    S.delta = buf<int64_t>(c, B_DELTA);
+    S.sums = buf<int64_t>(c, B_SUMS);
+    S.counts = buf<int64_t>(c, B_COUNTS);
+    S.qsum = buf<int64_t>(c, B_QSUM);
+    S.qexp = buf<int32_t>(c, B_QEXP);
+    S.done = buf<int32_t>(c, B_DONE);
+    S.stats = buf<int64_t>(c, B_STATS);
+    S.sse = buf<double>(c, B_SSE);
+    S.pw_prog = buf<int32_t>(c, B_PW_PROG);
+
+    std::vector<int32_t> prog;
+    build_pw(0, cfg->d, prog);
+    if (prog.size() > 4096) {
+        delete c;
+        set_error("pairwise program too long for d=%d", cfg->d);
+        return LK_ERR_UNSUPPORTED;
+    }
+    S.pw_len = (int32_t)prog.size();
+    LK_CUDA_CHECK(cudaMemcpy(S.pw_prog, prog.data(), prog.size() * 4, cudaMemcpyHostToDevice));
+    LK_CUDA_CHECK(cudaMemset(S.done, 0, 16));
+    *out = c;
+    return LK_OK;
+}
+
+lk_status lk_ctx_destroy(lk_ctx* c) {
+    if (!c) return LK_OK;
+    for (auto& r : c->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : c->pool) cudaEventDestroy(e);
+    delete c;
+    return LK_OK;
+}
+
+lk_status lk_buffer(const lk_ctx* c, int32_t id, uint64_t* offset, uint64_t* bytes) {
+    if (!c || id < 0 || id >= LK_NBUF) {
+        set_error("bad buffer id %d", id);
+        return LK_ERR_ARG;
+    }
+    if (offset) *offset = c->L.off[id];
+    if (bytes) *bytes = c->L.size[id];
+    return LK_OK;
+}
+
+lk_status lk_layout(const lk_ctx* c, int64_t* ldx, int64_t* delta_len, int32_t* nlb) {
+    if (!c) return LK_ERR_ARG;
+    if (ldx) *ldx = c->L.ldx;
+    if (delta_len) *delta_len = c->L.delta_len;
+    if (nlb) *nlb = c->L.nlb;
+    return LK_OK;
+}
+
+static __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+lk_status lk_scan_points(lk_ctx* c, void* stream) {
+    if (!c) return LK_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_fill_i32<<<1, 256, 0, st>>>(c->S.qexp, c->cfg.d + 1, -1100);
+    LK_LAUNCH_CHECK();
+    c->launches += 2;
+    return lkh::launch_scan_exp(c->S, c->sms, st);
+}
+
+lk_status lk_set_quant(lk_ctx* c, void* stream) {
+    if (!c) return LK_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int d = c->cfg.d;
+    std::vector<int32_t> e(d + 1);
+    LK_CUDA_CHECK(cudaMemcpyAsync(e.data(), c->S.qexp, (d + 1) * 4, cudaMemcpyDeviceToHost, st));
+    LK_CUDA_CHECK(cudaStreamSynchronize(st));
+    // Sum of n_total values each < 2^B in magnitude must stay below 2^62.
+    int lg = 0;
+    while ((1LL << lg) <= c->cfg.n_total) lg++;
+    const int B = 62 - lg;
+    std::vector<double> sc(d + 1), inv(d + 1);
+    for (int z = 0; z <= d; z++) {
+        int ez = e[z] < -1000 ? 0 : e[z];
+        int sh = B - ez;
+        sc[z] = ldexp(1.0, sh);
+        inv[z] = ldexp(1.0, -sh);
+    }
+    LK_CUDA_CHECK(cudaMemcpyAsync(buf<double>(c, B_QSCALE), sc.data(), (d + 1) * 8,
+                                  cudaMemcpyHostToDevice, st));
+    LK_CUDA_CHECK(cudaMemcpyAsync(buf<double>(c, B_QINV), inv.data(), (d + 1) * 8,
+                                  cudaMemcpyHostToDevice, st));
+    LK_CUDA_CHECK(cudaStreamSynchronize(st));
+    c->quant_set = true;
+    return LK_OK;
+}
+
+static __global__ void k_init_centroids(lk::DevState S) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (blockDim.x / 32) + warp;
+    if (j >= S.k) return;
+    double cn2 = 0.0;
+    for (int z = lane; z < S.ldc; z += 32) {
+        float v = z < S.d ? (float)S.C64[(int64_t)j * S.d + z] : 0.f;
+        S.C32[(int64_t)j * S.ldc + z] = v;
+        if (z < S.d) S.C64_prev[(int64_t)j * S.d + z] = S.C64[(int64_t)j * S.d + z];
+        cn2 = fma((double)v, (double)v, cn2);
+    }
+    for (int o = 16; o > 0; o >>= 1) cn2 += __shfl_xor_sync(LK_FULL_MASK, cn2, o);
+    if (lane == 0) {
+        float cn = __double2float_ru(sqrt(cn2) * (1.0 + 1e-12));
+        S.cnorm[j] = cn;
+        S.drift[j] = 0.f;
+        S.s_half[j] = 0.f;
+        lk::atomic_max_pos(S.scal, cn);
+    }
+}
+
+lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
+    if (!c || !c64) return LK_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    lk::DevState& S = c->S;
+    const int64_t k = c->cfg.k, d = c->cfg.d;
+    if ((const void*)c64 != (const void*)S.C64)
+        LK_CUDA_CHECK(cudaMemcpyAsync(S.C64, c64, k * d * 8, cudaMemcpyDeviceToDevice, st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.scal, 0, 8 * 4, st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.labels, 0xff, (size_t)c->cfg.n_local * 4, st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.sums, 0, k * d * 8, st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.counts, 0, k * 8, st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.qsum, 0, k * 8, st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.done, 0, 16, st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.stats, 0, c->L.size[B_STATS], st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.sse, 0, c->L.size[B_SSE], st));
+    k_init_centroids<<<(int)((k + 7) / 8), 256, 0, st>>>(S);
+    LK_LAUNCH_CHECK();
+    c->launches += 1;
+    c->centroids_set = true;
+    return LK_OK;
+}
+
+lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
+    if (!c) return LK_ERR_ARG;
+    if (!c->quant_set || !c->centroids_set) {
+        set_error("lk_step_assign before lk_set_quant / lk_set_centroids");
+        return LK_ERR_STATE;
+    }
+    if (t < 1 || t > c->cfg.t_max) {
+        set_error("iteration %d outside [1, %d]", t, c->cfg.t_max);
+        return LK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    lk::DevState& S = c->S;
+    int64_t* stat = S.stats + (int64_t)(t - 1) * LK_NSTAT;
+    LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
+    const int64_t n = c->cfg.n_local;
+    const bool use_tc = (c->cfg.kernel == LK_KERNEL_TC ||
+                         (c->cfg.kernel == LK_KERNEL_AUTO && c->cfg.d >= 32)) &&
+                        lkh::tc_supported(S);
+    lk_status s;
+    if (n > 0) {
+        if (c->cfg.strategy == LK_STRAT_LLOYD || t == 1) {
+            ProfScope p(c, 0, st);
+            s = use_tc ? lkh::launch_assign_tc(S, nullptr, nullptr, stat, n, c->sms, st)
+                       : lkh::launch_assign_simt(S, nullptr, nullptr, stat, n, c->sms, st);
+            if (s != LK_OK) return s;
+            c->launches += 1;
+        } else {
+            {
+                ProfScope p(c, 1, st);
+                s = lkh::launch_filter_hamerly(S, stat, c->sms, st);
+                if (s != LK_OK) return s;
+            }
+            ProfScope p(c, 0, st);
+            s = lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
+            if (s != LK_OK) return s;
+            c->launches += 2;
+        }
+        {
+            ProfScope p(c, 2, st);
+            s = lkh::launch_recheck(S, stat, n, c->sms, st);
+            if (s != LK_OK) return s;
+        }
+        {
+            ProfScope p(c, 3, st);
+            s = lkh::launch_refine(S, stat, buf<double>(c, B_QSCALE), n, c->sms, st);
+            if (s != LK_OK) return s;
+        }
+        c->launches += 2;
+    }
+    return LK_OK;
+}
+
+lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
+    if (!c) return LK_ERR_ARG;
+    if (t < 1 || t > c->cfg.t_max) {
+        set_error("iteration %d outside [1, %d]", t, c->cfg.t_max);
+        return LK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    ProfScope p(c, 4, st);
+    bool need_half = c->cfg.strategy == LK_STRAT_HAMERLY;
+    lk_status s = lkh::launch_update(c->S, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV),
+                                     buf<double>(c, B_SSE_PART), t, need_half, st);
+    c->launches += need_half ? 3 : 2;
+    return s;
+}
+
+int64_t lk_launch_count(const lk_ctx* c) { return c ? c->launches : 0; }
+
+lk_status lk_profile(lk_ctx* c, int32_t enable) {
+    if (!c) return LK_ERR_ARG;
+    c->profile = enable != 0;
+    LK_CUDA_CHECK(cudaDeviceSynchronize());
+    for (auto& r : c->recs) {
+        c->pool.push_back(r.a);
+        c->pool.push_back(r.b);
+    }
+    c->recs.clear();
+    return LK_OK;
+}
+
+lk_status lk_profile_read(lk_ctx* c, int32_t cls, double* total_ms, int64_t* launches) {
+    if (!c) return LK_ERR_ARG;
+    double tot = 0.0;
+    int64_t nl = 0;
+    for (auto& r : c->recs) {
+        if (r.cls != cls) continue;
+        LK_CUDA_CHECK(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        LK_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+        tot += ms;
+        nl++;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = nl;
+    return LK_OK;
+}
+
+}  // extern "C"

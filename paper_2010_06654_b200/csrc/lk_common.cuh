@@ -1,0 +1,127 @@
+// lk_common.cuh -- shared device helpers and the parameter block every kernel
+// of the exact-Lloyd path receives.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lloydkit_b200.h"
+
+#define LK_FULL_MASK 0xffffffffu
+
+namespace lk {
+
+constexpr int kWarp = 32;
+constexpr float kU32 = 5.9604644775390625e-08f;  // 2^-24, fp32 unit roundoff
+
+// Everything the hot kernels need, passed by value (fits the 4 KB param space).
+struct DevState {
+    int64_t n;        // local rows
+    int32_t d, k;
+    int32_t ldx;      // X32 row stride (floats)
+    int32_t ldc;      // C32 row stride (floats)
+    int32_t nlb;      // lower bounds per row (1 Hamerly, t Yinyang, k Elkan)
+    int32_t strategy;
+    int32_t t_groups; // group count
+    const float* X32;
+    const double* X64;      // nullable
+    double* C64;            // [k, d] master centroids
+    double* C64_prev;       // [k, d] previous centroids (for drift)
+    float* C32;             // [k, ldc] fp32 copy
+    float* cnorm;           // [k] ||c32|| rounded up
+    float* drift;           // [k] centroid drift rounded up
+    float* s_half;          // [k] 1/2 min distance to another centroid, rounded down
+    float* gdrift;          // [t] max drift inside each group
+    float* scal;            // [8] scalars: 0 cmax, 1 drift max1, 2 drift max2, 3 (int) argmax
+    int32_t* group_of;      // [k]
+    int32_t* labels;        // [n]
+    float* ub;              // [n]
+    float* lb;              // [n, nlb]
+    int2* moved;            // [n] (row, old label)
+    int32_t* flagged;       // [n]
+    int32_t* work;          // [n]
+    int64_t* delta;         // [k*d | k | k | 1]
+    int64_t* sums;          // [k, d] fixed-point member sums
+    int64_t* counts;        // [k]
+    int64_t* qsum;          // [k] fixed-point sum of ||x||^2 per cluster
+    int32_t* qexp;          // [d+1] exponents (max|x_z| < 2^qexp[z]; qexp[d] for ||x||^2)
+    int32_t* qshift;        // [d+1] fixed-point shifts
+    int32_t* done;          // [1] set once an iteration had changed == 0
+    int64_t* stats;         // [t_max, LK_NSTAT]
+    double* sse;            // [t_max]
+    int32_t* pw_prog;       // numpy pairwise-sum program for the fp64 recheck
+    int32_t pw_len;
+};
+
+__device__ __forceinline__ unsigned lane_id() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// Warp-aggregated append to a device worklist: one atomic per warp.  Every
+// lane of the (converged) warp must call it.
+__device__ __forceinline__ int64_t warp_append(bool pred, unsigned long long* counter) {
+    unsigned m = __ballot_sync(LK_FULL_MASK, pred);
+    if (m == 0) return -1;
+    int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if ((int)lane_id() == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+    base = __shfl_sync(LK_FULL_MASK, base, leader);
+    return pred ? (int64_t)(base + __popc(m & lanemask_lt())) : -1;
+}
+
+__device__ __forceinline__ void warp_count(bool pred, int64_t* counter) {
+    unsigned m = __ballot_sync(LK_FULL_MASK, pred);
+    if (m && lane_id() == (unsigned)(__ffs(m) - 1))
+        atomicAdd((unsigned long long*)counter, (unsigned long long)__popc(m));
+}
+
+__device__ __forceinline__ void warp_add(int64_t v, int64_t* counter) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(LK_FULL_MASK, v, o);
+    if (lane_id() == 0 && v) atomicAdd((unsigned long long*)counter, (unsigned long long)v);
+}
+
+// Nonnegative-float atomic max via integer ordering.
+__device__ __forceinline__ void atomic_max_pos(float* addr, float v) {
+    atomicMax((int*)addr, __float_as_int(v));
+}
+
+// Relative error (in units of the computed distance) of the fp32
+// difference-form distance sqrt(sum_z fl(x_z - c_z)^2) against the exact
+// distance of the fp32 operands, plus the fp64 oracle's own error.  Generous
+// (d + 8) u; see DESIGN.md "certifying labels".
+__device__ __forceinline__ float simt_rel_err(int d) { return (float)(d + 8) * kU32; }
+
+}  // namespace lk
+
+// Host-side error plumbing shared by the launchers.
+namespace lkh {
+void set_error(const char* fmt, ...);
+}
+
+#define LK_CUDA_CHECK(expr)                                                          \
+    do {                                                                             \
+        cudaError_t _e = (expr);                                                     \
+        if (_e != cudaSuccess) {                                                     \
+            lkh::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,                \
+                           cudaGetErrorString(_e));                                  \
+            return LK_ERR_CUDA;                                                      \
+        }                                                                            \
+    } while (0)
+
+#define LK_LAUNCH_CHECK()                                                            \
+    do {                                                                             \
+        cudaError_t _e = cudaGetLastError();                                         \
+        if (_e != cudaSuccess) {                                                     \
+            lkh::set_error("%s:%d launch: %s", __FILE__, __LINE__,                   \
+                           cudaGetErrorString(_e));                                  \
+            return LK_ERR_CUDA;                                                      \
+        }                                                                            \
+    } while (0)

@@ -1,0 +1,743 @@
+// lk_kernels.cu -- the SIMT kernels of the exact-Lloyd iteration on sm_100a.
+//
+//   K1  k_assign_reg / k_assign_gen   fused fp32 difference-form distance +
+//       per-row top-2 (replaces assign_full, lloyd.py:69-75 and
+//       SequentialStrategy.seed, pruners.py:83-87 + _two_smallest :44-50).
+//       Rows whose top-2 gap is inside the certified error bound are not
+//       decided here; they go to K1x.
+//   K1x k_recheck_fp64  exact re-decision of ambiguous rows in fp64 with
+//       numpy's pairwise association order (core.py:98-108), so the label is
+//       the oracle's label bit for bit, ties to the lowest index.
+//   K2  k_filter_hamerly  drift decay of ub/lb + gate + tighten + compaction
+//       (Hamerly.update_bounds pruners.py:234-239, assign_pass :244-254).
+//   K4  k_refine_moved  fixed-point member-sum deltas of moved points
+//       (refine_full lloyd.py:78-97, incrementally as in engine.py:134-172).
+//   K5  k_update_centroids / k_update_global / k_half_sep  centroid divide with
+//       the empty-cluster rule (lloyd.py:94-96), drifts (bounds.py:31-35),
+//       s = half nearest-other distance (bounds.py:38-47), SSE (core.py:172).
+#include <float.h>
+#include <math.h>
+
+#include "lk_common.cuh"
+#include "lk_internal.h"
+
+namespace lk {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// shared epilogue: certify or flag one row, write label / bounds / worklists
+
+// U1: certified upper bound on the true distance to candidate j1.
+// L2: certified lower bound on the true distance to every other centroid.
+// Must be called by all 32 lanes of a warp (valid=false lanes just vote).
+__device__ __forceinline__ void row_finish(const DevState& S, bool valid, int64_t row, int j1,
+                                           float U1, float L2, int64_t* stat) {
+    bool certain = valid && (L2 > U1);
+    bool flag = valid && !certain;
+    int old = 0;
+    bool moved = false;
+    if (certain) {
+        old = S.labels[row];
+        moved = (old != j1);
+        S.labels[row] = j1;
+        if (S.strategy != LK_STRAT_LLOYD) {
+            S.ub[row] = U1;
+            S.lb[row * S.nlb] = fmaxf(L2, 0.0f);
+        }
+    }
+    int64_t pos = warp_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED));
+    if (moved) S.moved[pos] = make_int2((int)row, old);
+    int64_t fpos = warp_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED));
+    if (flag) S.flagged[fpos] = (int)row;
+}
+
+__device__ __forceinline__ void top2_push(float D, int j, float& b1, int& j1, float& b2) {
+    if (D < b1) {
+        b2 = b1;
+        b1 = D;
+        j1 = j;
+    } else {
+        b2 = fminf(b2, D);
+    }
+}
+
+// Certified bounds from fp32 difference-form squared distances b1 (label j1)
+// and b2 (best other): see DESIGN.md "certifying labels".
+__device__ __forceinline__ void simt_bounds(const DevState& S, float b1, int j1, float b2,
+                                            float xnorm, float& U1, float& L2) {
+    const float rho = simt_rel_err(S.d);
+    const float cmax = S.scal[0];
+    float a1 = kU32 * (xnorm + S.cnorm[j1]);
+    float a2 = kU32 * (xnorm + cmax);
+    U1 = (sqrtf(b1) + a1) * (1.0f + rho);
+    L2 = isinf(b2) ? INFINITY : (sqrtf(b2) - a2) * (1.0f - rho);
+}
+
+// ---------------------------------------------------------------------------
+// K1 (d <= 32): point rows in registers, centroid tiles in shared memory
+
+template <int DP, int RPT>
+__global__ void __launch_bounds__(kThreads) k_assign_reg(DevState S, const int32_t* rowlist,
+                                                         const int64_t* rowcount, int64_t* stat,
+                                                         int tile_k) {
+    if (*S.done) return;
+    extern __shared__ __align__(16) float csm[];  // [tile_k][DP]
+    const int64_t m = rowlist ? *rowcount : S.n;
+    const int ntiles = (S.k + tile_k - 1) / tile_k;
+    const int64_t rpb = (int64_t)kThreads * RPT;
+    int loaded = -1;
+    for (int64_t base = (int64_t)blockIdx.x * rpb; base < m; base += (int64_t)gridDim.x * rpb) {
+        float x[RPT][DP];
+        float xn2[RPT];
+        int64_t row[RPT];
+        bool valid[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; q++) {
+            int64_t r = base + threadIdx.x + (int64_t)q * kThreads;
+            valid[q] = r < m;
+            row[q] = valid[q] ? (rowlist ? (int64_t)rowlist[r] : r) : 0;
+            const float* xp = S.X32 + row[q] * S.ldx;
+            xn2[q] = 0.f;
+#pragma unroll
+            for (int z = 0; z < DP; z++) {
+                float v = (valid[q] && z < S.d) ? __ldg(xp + z) : 0.f;
+                x[q][z] = v;
+                xn2[q] = fmaf(v, v, xn2[q]);
+            }
+        }
+        float b1[RPT], b2[RPT];
+        int j1[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; q++) { b1[q] = INFINITY; b2[q] = INFINITY; j1[q] = 0; }
+
+        for (int tile = 0; tile < ntiles; tile++) {
+            const int j0 = tile * tile_k;
+            const int nj = min(tile_k, S.k - j0);
+            if (loaded != tile) {
+                __syncthreads();
+                for (int e = threadIdx.x; e < nj * DP; e += kThreads) {
+                    int jj = e / DP, z = e - jj * DP;
+                    csm[e] = z < S.d ? S.C32[(int64_t)(j0 + jj) * S.ldc + z] : 0.f;
+                }
+                __syncthreads();
+                loaded = tile;
+            }
+            for (int jj = 0; jj < nj; jj++) {
+                float c[DP];
+                if constexpr (DP % 4 == 0) {
+#pragma unroll
+                    for (int z = 0; z < DP; z += 4) {
+                        float4 v = *reinterpret_cast<const float4*>(csm + jj * DP + z);
+                        c[z] = v.x; c[z + 1] = v.y; c[z + 2] = v.z; c[z + 3] = v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int z = 0; z < DP; z++) c[z] = csm[jj * DP + z];
+                }
+#pragma unroll
+                for (int q = 0; q < RPT; q++) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int z = 0; z < DP; z++) {
+                        float t = x[q][z] - c[z];
+                        acc = fmaf(t, t, acc);
+                    }
+                    top2_push(acc, j0 + jj, b1[q], j1[q], b2[q]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RPT; q++) {
+            float U1 = 0.f, L2 = 0.f;
+            if (valid[q]) simt_bounds(S, b1[q], j1[q], b2[q], sqrtf(xn2[q]), U1, L2);
+            row_finish(S, valid[q], row[q], j1[q], U1, L2, stat);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1 (d > 32): 256 rows x 32 centroids per pass, d streamed in chunks of 32
+
+constexpr int kGenTJ = 32;
+constexpr int kGenDC = 32;
+
+__global__ void __launch_bounds__(kThreads) k_assign_gen(DevState S, const int32_t* rowlist,
+                                                         const int64_t* rowcount, int64_t* stat) {
+    if (*S.done) return;
+    __shared__ float xs[kGenDC][kThreads + 1];
+    __shared__ __align__(16) float cs[kGenDC][kGenTJ];
+    __shared__ int64_t rows_s[kThreads];
+    const int64_t m = rowlist ? *rowcount : S.n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < m;
+         base += (int64_t)gridDim.x * kThreads) {
+        __syncthreads();
+        {
+            int64_t r = base + threadIdx.x;
+            rows_s[threadIdx.x] = r < m ? (rowlist ? (int64_t)rowlist[r] : r) : -1;
+        }
+        __syncthreads();
+        const bool valid = rows_s[threadIdx.x] >= 0;
+        float b1 = INFINITY, b2 = INFINITY, xn2 = 0.f;
+        int j1 = 0;
+        for (int j0 = 0; j0 < S.k; j0 += kGenTJ) {
+            float acc[kGenTJ];
+#pragma unroll
+            for (int c = 0; c < kGenTJ; c++) acc[c] = 0.f;
+            for (int z0 = 0; z0 < S.d; z0 += kGenDC) {
+                __syncthreads();
+                // X chunk: warp w loads rows w*32 .. w*32+31, lane = dimension
+                for (int rr = 0; rr < 32; rr++) {
+                    int r = warp * 32 + rr;
+                    int64_t gr = rows_s[r];
+                    int z = z0 + lane;
+                    xs[lane][r] = (gr >= 0 && z < S.d) ? __ldg(S.X32 + gr * S.ldx + z) : 0.f;
+                }
+                for (int e = threadIdx.x; e < kGenDC * kGenTJ; e += kThreads) {
+                    int jj = e / kGenDC, z = e - jj * kGenDC;
+                    int j = j0 + jj, zz = z0 + z;
+                    cs[z][jj] = (j < S.k && zz < S.d) ? S.C32[(int64_t)j * S.ldc + zz] : 0.f;
+                }
+                __syncthreads();
+#pragma unroll 4
+                for (int z = 0; z < kGenDC; z++) {
+                    float xv = xs[z][threadIdx.x];
+                    if (j0 == 0) xn2 = fmaf(xv, xv, xn2);
+#pragma unroll
+                    for (int c4 = 0; c4 < kGenTJ; c4 += 4) {
+                        float4 cv = *reinterpret_cast<const float4*>(&cs[z][c4]);
+                        float t0 = xv - cv.x, t1 = xv - cv.y, t2 = xv - cv.z, t3 = xv - cv.w;
+                        acc[c4] = fmaf(t0, t0, acc[c4]);
+                        acc[c4 + 1] = fmaf(t1, t1, acc[c4 + 1]);
+                        acc[c4 + 2] = fmaf(t2, t2, acc[c4 + 2]);
+                        acc[c4 + 3] = fmaf(t3, t3, acc[c4 + 3]);
+                    }
+                }
+            }
+            const int nj = min(kGenTJ, S.k - j0);
+#pragma unroll
+            for (int c = 0; c < kGenTJ; c++)
+                if (c < nj) top2_push(acc[c], j0 + c, b1, j1, b2);
+        }
+        float U1 = 0.f, L2 = 0.f;
+        if (valid) simt_bounds(S, b1, j1, b2, sqrtf(xn2), U1, L2);
+        row_finish(S, valid, valid ? rows_s[threadIdx.x] : 0, j1, U1, L2, stat);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1x: exact fp64 recheck, numpy pairwise order (one warp per flagged row)
+
+constexpr int kRcWarps = 4;
+
+// Sum of (x_z - c_z)^2 over [start, start+len) exactly as numpy's pairwise_sum
+// leaf does it: sequential from 0 below 8 terms, else 8 strided accumulators
+// combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail in order.
+__device__ __forceinline__ double pw_leaf(const double* x, const double* c, int start, int len) {
+    if (len < 8) {
+        double res = 0.0;
+        for (int z = start; z < start + len; z++) {
+            double t = __dsub_rn(x[z], c[z]);
+            res = __dadd_rn(res, __dmul_rn(t, t));
+        }
+        return res;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        double t = __dsub_rn(x[start + j], c[start + j]);
+        r[j] = __dmul_rn(t, t);
+    }
+    int i = 8;
+    const int main_end = len - (len % 8);
+    for (; i < main_end; i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            double t = __dsub_rn(x[start + i + j], c[start + i + j]);
+            r[j] = __dadd_rn(r[j], __dmul_rn(t, t));
+        }
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < len; i++) {
+        double t = __dsub_rn(x[start + i], c[start + i]);
+        res = __dadd_rn(res, __dmul_rn(t, t));
+    }
+    return res;
+}
+
+__device__ double pw_dist2(const double* x, const double* c, const int32_t* prog, int plen) {
+    if (plen == 3) return pw_leaf(x, c, __ldg(prog + 1), __ldg(prog + 2));
+    double st[24];
+    int sp = 0;
+    for (int p = 0; p < plen; p += 3) {
+        int op = __ldg(prog + p);
+        if (op == 0) {
+            st[sp++] = pw_leaf(x, c, __ldg(prog + p + 1), __ldg(prog + p + 2));
+        } else {
+            double b = st[--sp];
+            double a = st[--sp];
+            st[sp++] = __dadd_rn(a, b);
+        }
+    }
+    return st[0];
+}
+
+__global__ void __launch_bounds__(kRcWarps * 32) k_recheck_fp64(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    extern __shared__ double xsh[];  // [kRcWarps][d]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* xr = xsh + (int64_t)warp * S.d;
+    const int64_t m = stat[LK_STAT_FLAGGED];
+    for (int64_t f = (int64_t)blockIdx.x * kRcWarps + warp; f < m;
+         f += (int64_t)gridDim.x * kRcWarps) {
+        const int64_t row = S.flagged[f];
+        __syncwarp();
+        for (int z = lane; z < S.d; z += 32)
+            xr[z] = S.X64 ? S.X64[row * S.d + z] : (double)S.X32[row * S.ldx + z];
+        __syncwarp();
+        double b1 = INFINITY, b2 = INFINITY;
+        int j1 = 0x7fffffff;
+        for (int j = lane; j < S.k; j += 32) {
+            double dd = __dsqrt_rn(pw_dist2(xr, S.C64 + (int64_t)j * S.d, S.pw_prog, S.pw_len));
+            if (dd < b1) { b2 = b1; b1 = dd; j1 = j; }
+            else b2 = fmin(b2, dd);
+        }
+        // warp merge of (b1, j1, b2): lexicographic (value, index) minimum
+        for (int o = 16; o > 0; o >>= 1) {
+            double ob1 = __shfl_xor_sync(LK_FULL_MASK, b1, o);
+            double ob2 = __shfl_xor_sync(LK_FULL_MASK, b2, o);
+            int oj1 = __shfl_xor_sync(LK_FULL_MASK, j1, o);
+            bool mine = (b1 < ob1) || (b1 == ob1 && j1 < oj1);
+            if (mine) {
+                b2 = fmin(b2, ob1);
+            } else {
+                b2 = fmin(ob2, b1);
+                b1 = ob1;
+                j1 = oj1;
+            }
+        }
+        int old = S.labels[row];
+        bool mv = false;
+        if (lane == 0) {
+            mv = (old != j1);
+            S.labels[row] = j1;
+            if (S.strategy != LK_STRAT_LLOYD) {
+                S.ub[row] = __double2float_ru(b1 * (1.0 + 1e-12));
+                S.lb[row * S.nlb] = isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12));
+            }
+            if (mv) {
+                unsigned long long p =
+                    atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), 1ull);
+                S.moved[p] = make_int2((int)row, old);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: Hamerly bound decay + gate + tighten + compaction of the rows to rescan
+
+__global__ void __launch_bounds__(kThreads) k_filter_hamerly(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    const float dmax1 = S.scal[1], dmax2 = S.scal[2];
+    const int amax = __float_as_int(S.scal[3]);
+    const float rho = simt_rel_err(S.d);
+    const int64_t n = S.n;
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < n;
+         base += (int64_t)gridDim.x * kThreads) {
+        int64_t i = base + threadIdx.x;
+        bool valid = i < n;
+        bool active = false, need = false;
+        if (valid) {
+            int a = S.labels[i];
+            float u = __fadd_ru(S.ub[i], S.drift[a]);
+            float l = fmaxf(__fsub_rd(S.lb[i], a == amax ? dmax2 : dmax1), 0.f);
+            float gate = fmaxf(l, S.s_half[a]);
+            if (!(gate > u)) {
+                active = true;
+                const float* xp = S.X32 + i * S.ldx;
+                const float* cp = S.C32 + (int64_t)a * S.ldc;
+                float acc = 0.f, xn2 = 0.f;
+                for (int z = 0; z < S.d; z++) {
+                    float xv = __ldg(xp + z);
+                    float t = xv - __ldg(cp + z);
+                    acc = fmaf(t, t, acc);
+                    xn2 = fmaf(xv, xv, xn2);
+                }
+                float U = (sqrtf(acc) + kU32 * (sqrtf(xn2) + S.cnorm[a])) * (1.0f + rho);
+                u = fminf(u, U);
+                need = !(gate > u);
+            }
+            S.ub[i] = u;
+            S.lb[i] = l;
+        }
+        warp_count(active, stat + LK_STAT_ACTIVE);
+        int64_t pos = warp_append(need, (unsigned long long*)(stat + LK_STAT_WORK));
+        if (need) S.work[pos] = (int)i;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: fixed-point member-sum deltas of the moved rows
+
+__device__ __forceinline__ double load_x(const DevState& S, int64_t row, int z) {
+    return S.X64 ? S.X64[row * S.d + z] : (double)__ldg(S.X32 + row * S.ldx + z);
+}
+
+// G lanes per moved row (G = power of two >= min(d, 32)); warp-uniform loop.
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_refine_moved(DevState S, int64_t* stat,
+                                                           const double* qscale) {
+    if (*S.done) return;
+    const int64_t m = stat[LK_STAT_CHANGED];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane % G;
+    constexpr int kGroupsPerWarp = 32 / G;
+    int64_t* dS = S.delta;
+    int64_t* dN = S.delta + (int64_t)S.k * S.d;
+    int64_t* dQ = dN + S.k;
+    const int64_t stride = (int64_t)gridDim.x * (kThreads / 32) * kGroupsPerWarp;
+    for (int64_t wb = ((int64_t)blockIdx.x * (kThreads / 32) + warp) * kGroupsPerWarp; wb < m;
+         wb += stride) {
+        const int64_t e = wb + lane / G;
+        const bool ok = e < m;
+        double x2 = 0.0;
+        int64_t row = 0;
+        int old = -1, nw = 0;
+        if (ok) {
+            int2 mv = S.moved[e];
+            row = mv.x;
+            old = mv.y;
+            nw = S.labels[row];
+            for (int z = sub; z < S.d; z += G) {
+                double v = load_x(S, row, z);
+                x2 = fma(v, v, x2);
+                long long q = __double2ll_rn(v * qscale[z]);
+                if (q) {
+                    atomicAdd((unsigned long long*)(dS + (int64_t)nw * S.d + z),
+                              (unsigned long long)q);
+                    if (old >= 0)
+                        atomicAdd((unsigned long long*)(dS + (int64_t)old * S.d + z),
+                                  (unsigned long long)(-q));
+                }
+            }
+        }
+        // deterministic group reduction of ||x||^2 (fixed xor tree)
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) x2 += __shfl_xor_sync(LK_FULL_MASK, x2, o, G);
+        if (ok && sub == 0) {
+            long long qq = __double2ll_rn(x2 * qscale[S.d]);
+            atomicAdd((unsigned long long*)(dN + nw), 1ull);
+            atomicAdd((unsigned long long*)(dQ + nw), (unsigned long long)qq);
+            if (old >= 0) {
+                atomicAdd((unsigned long long*)(dN + old), (unsigned long long)(-1ll));
+                atomicAdd((unsigned long long*)(dQ + old), (unsigned long long)(-qq));
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // local changed count rides along in the all-reduce payload
+        S.delta[(int64_t)S.k * S.d + 2 * S.k] = m;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: centroid update (one warp per centroid) and global scalars
+
+__global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const double* qscale,
+                                                               const double* qinv,
+                                                               double* sse_part) {
+    if (*S.done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (kThreads / 32) + warp;
+    if (j >= S.k) return;
+    const int64_t* dS = S.delta;
+    const int64_t* dN = S.delta + (int64_t)S.k * S.d;
+    const int64_t* dQ = dN + S.k;
+    int64_t cnt = S.counts[j] + dN[j];
+    int64_t qs = S.qsum[j] + dQ[j];
+    double s2 = 0.0, drift2 = 0.0, cn2 = 0.0;
+    for (int z = lane; z < S.d; z += 32) {
+        int64_t sv = S.sums[(int64_t)j * S.d + z] + dS[(int64_t)j * S.d + z];
+        S.sums[(int64_t)j * S.d + z] = sv;
+        double old = S.C64[(int64_t)j * S.d + z];
+        double c = old;
+        if (cnt > 0) {
+            double sr = (double)sv * qinv[z];
+            c = sr / (double)cnt;
+            s2 = fma(sr, sr, s2);
+        }
+        S.C64_prev[(int64_t)j * S.d + z] = old;
+        S.C64[(int64_t)j * S.d + z] = c;
+        double dd = c - old;
+        drift2 = fma(dd, dd, drift2);
+        float c32 = (float)c;
+        S.C32[(int64_t)j * S.ldc + z] = c32;
+        cn2 = fma((double)c32, (double)c32, cn2);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s2 += __shfl_xor_sync(LK_FULL_MASK, s2, o);
+        drift2 += __shfl_xor_sync(LK_FULL_MASK, drift2, o);
+        cn2 += __shfl_xor_sync(LK_FULL_MASK, cn2, o);
+    }
+    if (lane == 0) {
+        S.counts[j] = cnt;
+        S.qsum[j] = qs;
+        S.drift[j] = drift2 > 0.0 ? __double2float_ru(sqrt(drift2) * (1.0 + 1e-12)) : 0.f;
+        S.cnorm[j] = __double2float_ru(sqrt(cn2) * (1.0 + 1e-12));
+        sse_part[j] = cnt > 0 ? ((double)qs * qinv[S.d] - s2 / (double)cnt) : 0.0;
+    }
+}
+
+// Single block: SSE (fixed reduction order), max ||c||, top-2 drift, group
+// drifts, done flag.
+__global__ void __launch_bounds__(1024) k_update_global(DevState S, const double* sse_part,
+                                                        int t) {
+    if (*S.done) return;
+    __shared__ double ssum[1024];
+    __shared__ float smax[1024], sd1[1024], sd2[1024];
+    __shared__ int sarg[1024];
+    const int tid = threadIdx.x;
+    double acc = 0.0;
+    float cm = 0.f, d1 = -1.f, d2 = -1.f;
+    int a1 = -1;
+    for (int j = tid; j < S.k; j += blockDim.x) {
+        acc += sse_part[j];
+        cm = fmaxf(cm, S.cnorm[j]);
+        float dj = S.drift[j];
+        if (dj > d1) { d2 = d1; d1 = dj; a1 = j; }
+        else d2 = fmaxf(d2, dj);
+    }
+    ssum[tid] = acc; smax[tid] = cm; sd1[tid] = d1; sd2[tid] = d2; sarg[tid] = a1;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (tid < s) {
+            ssum[tid] += ssum[tid + s];
+            smax[tid] = fmaxf(smax[tid], smax[tid + s]);
+            float od1 = sd1[tid + s], od2 = sd2[tid + s];
+            int oa = sarg[tid + s];
+            if (od1 > sd1[tid] || (od1 == sd1[tid] && oa >= 0 && (sarg[tid] < 0 || oa < sarg[tid]))) {
+                sd2[tid] = fmaxf(sd1[tid], od2);
+                sd1[tid] = od1;
+                sarg[tid] = oa;
+            } else {
+                sd2[tid] = fmaxf(sd2[tid], od1);
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        S.sse[t - 1] = ssum[0];
+        S.scal[0] = smax[0];
+        S.scal[1] = fmaxf(sd1[0], 0.f);
+        S.scal[2] = fmaxf(sd2[0], 0.f);
+        S.scal[3] = __int_as_float(sarg[0]);
+        int64_t changed = S.delta[(int64_t)S.k * S.d + 2 * S.k];
+        S.stats[(int64_t)(t - 1) * LK_NSTAT + LK_STAT_CHANGED_GLOBAL] = changed;
+        if (changed == 0) *S.done = 1;
+    }
+    // group drifts (Yinyang): max drift over each group's members
+    if (S.gdrift) {
+        __syncthreads();
+        for (int g = tid; g < S.t_groups; g += blockDim.x) S.gdrift[g] = 0.f;
+        __syncthreads();
+        for (int j = tid; j < S.k; j += blockDim.x) atomic_max_pos(S.gdrift + S.group_of[j], S.drift[j]);
+    }
+}
+
+// s_j = 1/2 min_{j' != j} |c_j - c_j'|, certified lower bound (fp32 diff form).
+__global__ void __launch_bounds__(kThreads) k_half_sep(DevState S) {
+    if (*S.done) return;
+    __shared__ float ct[64][33];
+    __shared__ float cnt_s[64];
+    const int j = blockIdx.x * kThreads + threadIdx.x;
+    const float rho = simt_rel_err(S.d);
+    float best = INFINITY;
+    for (int j0 = 0; j0 < S.k; j0 += 64) {
+        float acc[64];
+#pragma unroll
+        for (int c = 0; c < 64; c++) acc[c] = 0.f;
+        for (int z0 = 0; z0 < S.d; z0 += 32) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < 64 * 32; e += kThreads) {
+                int jj = e / 32, z = e % 32;
+                ct[jj][z] = (j0 + jj < S.k && z0 + z < S.d) ? S.C32[(int64_t)(j0 + jj) * S.ldc + z0 + z] : 0.f;
+            }
+            if (threadIdx.x < 64) cnt_s[threadIdx.x] = (j0 + threadIdx.x < S.k) ? S.cnorm[j0 + threadIdx.x] : 0.f;
+            __syncthreads();
+            if (j < S.k) {
+                for (int z = 0; z < 32 && z0 + z < S.d; z++) {
+                    float xv = S.C32[(int64_t)j * S.ldc + z0 + z];
+#pragma unroll
+                    for (int c = 0; c < 64; c++) {
+                        float t = xv - ct[c][z];
+                        acc[c] = fmaf(t, t, acc[c]);
+                    }
+                }
+            }
+        }
+        if (j < S.k) {
+            float cj = S.cnorm[j];
+#pragma unroll
+            for (int c = 0; c < 64; c++) {
+                int jj = j0 + c;
+                if (jj < S.k && jj != j) {
+                    float lbd = (sqrtf(acc[c]) - kU32 * (cj + cnt_s[c])) * (1.0f - rho);
+                    best = fminf(best, lbd);
+                }
+            }
+        }
+    }
+    if (j < S.k) S.s_half[j] = isinf(best) ? INFINITY : fmaxf(0.5f * best * (1.0f - kU32 * 4), 0.f);
+}
+
+// Per-dimension max |x| exponents (frexp convention: |x| < 2^e) of the local
+// rows, and the exponent of max ||x||^2 in qexp[d].  One warp per row, lanes
+// over dimensions; per-warp maxima in shared memory, then global atomicMax.
+__global__ void __launch_bounds__(kThreads) k_scan_exp(DevState S) {
+    extern __shared__ int wexp[];  // [8 warps][d + 1]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* we = wexp + warp * (S.d + 1);
+    for (int z = lane; z <= S.d; z += 32) we[z] = -1100;
+    __syncwarp();
+    for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < S.n; i += (int64_t)gridDim.x * 8) {
+        double s = 0.0;
+        for (int z = lane; z < S.d; z += 32) {
+            double v = load_x(S, i, z);
+            s = fma(v, v, s);
+            if (v != 0.0) {
+                int ex;
+                frexp(fabs(v), &ex);
+                we[z] = max(we[z], ex);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(LK_FULL_MASK, s, o);
+        if (lane == 0 && s > 0.0) {
+            int ex;
+            frexp(s * (1.0 + 1e-9), &ex);
+            we[S.d] = max(we[S.d], ex);
+        }
+    }
+    __syncwarp();
+    for (int z = lane; z <= S.d; z += 32) atomicMax(S.qexp + z, we[z]);
+}
+
+}  // namespace lk
+
+// ---------------------------------------------------------------------------
+// launchers
+
+namespace lkh {
+
+using namespace lk;
+
+static int grid_for(int64_t work_items, int per_block, int max_blocks) {
+    int64_t b = (work_items + per_block - 1) / per_block;
+    if (b < 1) b = 1;
+    if (b > max_blocks) b = max_blocks;
+    return (int)b;
+}
+
+template <int DP, int RPT>
+static lk_status launch_reg(const DevState& S, const int32_t* rowlist, const int64_t* rowcount,
+                            int64_t* stat, int64_t max_rows, int sms, cudaStream_t st) {
+    int tile_k = S.k;
+    const int smem_cap = 96 * 1024;
+    if ((int64_t)tile_k * DP * 4 > smem_cap) tile_k = smem_cap / (DP * 4);
+    size_t smem = (size_t)tile_k * DP * 4;
+    static bool attr_set = false;
+    if (!attr_set) {
+        LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_reg<DP, RPT>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+        attr_set = true;
+    }
+    int grid = grid_for(max_rows, kThreads * RPT, sms * 4);
+    k_assign_reg<DP, RPT><<<grid, kThreads, smem, st>>>(S, rowlist, rowcount, stat, tile_k);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_assign_simt(const DevState& S, const int32_t* rowlist, const int64_t* rowcount,
+                             int64_t* stat, int64_t max_rows, int sms, cudaStream_t st) {
+    const int d = S.d;
+    if (d <= 2) return launch_reg<2, 2>(S, rowlist, rowcount, stat, max_rows, sms, st);
+    if (d <= 4) return launch_reg<4, 2>(S, rowlist, rowcount, stat, max_rows, sms, st);
+    if (d <= 8) return launch_reg<8, 2>(S, rowlist, rowcount, stat, max_rows, sms, st);
+    if (d <= 16) return launch_reg<16, 2>(S, rowlist, rowcount, stat, max_rows, sms, st);
+    if (d <= 32) return launch_reg<32, 1>(S, rowlist, rowcount, stat, max_rows, sms, st);
+    int grid = grid_for(max_rows, kThreads, sms * 4);
+    k_assign_gen<<<grid, kThreads, 0, st>>>(S, rowlist, rowcount, stat);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_recheck(const DevState& S, int64_t* stat, int64_t max_rows, int sms,
+                         cudaStream_t st) {
+    size_t smem = (size_t)kRcWarps * S.d * sizeof(double);
+    static bool attr_set = false;
+    if (!attr_set) {
+        LK_CUDA_CHECK(cudaFuncSetAttribute(k_recheck_fp64,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = true;
+    }
+    int grid = grid_for(max_rows, kRcWarps, sms * 8);
+    k_recheck_fp64<<<grid, kRcWarps * 32, smem, st>>>(S, stat);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_filter_hamerly(const DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    int grid = grid_for(S.n, kThreads, sms * 8);
+    k_filter_hamerly<<<grid, kThreads, 0, st>>>(S, stat);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_refine(const DevState& S, int64_t* stat, const double* qscale, int64_t max_rows,
+                        int sms, cudaStream_t st) {
+    int g = 32;
+    if (S.d <= 1) g = 1;
+    else if (S.d <= 2) g = 2;
+    else if (S.d <= 4) g = 4;
+    else if (S.d <= 8) g = 8;
+    else if (S.d <= 16) g = 16;
+    int grid = grid_for(max_rows, kThreads / g, sms * 8);
+    switch (g) {
+        case 1: k_refine_moved<1><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
+        case 2: k_refine_moved<2><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
+        case 4: k_refine_moved<4><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
+        case 8: k_refine_moved<8><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
+        case 16: k_refine_moved<16><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
+        default: k_refine_moved<32><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
+    }
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_update(const DevState& S, const double* qscale, const double* qinv,
+                        double* sse_part, int t, bool need_half, cudaStream_t st) {
+    int grid = (S.k + (kThreads / 32) - 1) / (kThreads / 32);
+    k_update_centroids<<<grid, kThreads, 0, st>>>(S, qscale, qinv, sse_part);
+    LK_LAUNCH_CHECK();
+    k_update_global<<<1, 1024, 0, st>>>(S, sse_part, t);
+    LK_LAUNCH_CHECK();
+    if (need_half) {
+        k_half_sep<<<(S.k + kThreads - 1) / kThreads, kThreads, 0, st>>>(S);
+        LK_LAUNCH_CHECK();
+    }
+    return LK_OK;
+}
+
+lk_status launch_scan_exp(const DevState& S, int sms, cudaStream_t st) {
+    size_t smem = (size_t)8 * (S.d + 1) * sizeof(int);
+    if (smem > 48 * 1024)
+        LK_CUDA_CHECK(cudaFuncSetAttribute(k_scan_exp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+    k_scan_exp<<<grid_for(S.n, 8, sms * 4), kThreads, smem, st>>>(S);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+}  // namespace lkh

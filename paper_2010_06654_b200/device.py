@@ -1,0 +1,271 @@
+"""Device-resident Lloyd engine: binds one block of points to one GPU and runs
+the exact iteration through the C ABI (include/lloydkit_b200.h).
+
+Layout in HBM (one torch uint8 workspace, carved by the library):
+  X32 [n, ldx] fp32 points (ldx = d rounded up to 4 for d > 2), optional X64
+  [n, d] when the input is not fp32-exact; C64 [k, d] fp64 master centroids
+  plus an fp32 copy; labels int32 [n]; ub fp32 [n] and lb fp32 [n, nlb] for the
+  bounded strategies; fixed-point member sums int64 [k, d] + counts + sum of
+  squared norms; the all-reduce payload int64 [k*d + 2k + 8]; worklists.
+
+One process drives one GPU.  With ``comm`` (a torch.distributed group) the
+rows are one shard of a larger matrix and the per-iteration delta buffer is
+summed across ranks between the assignment and the update phase.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .core import ContractError
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class IterRecord:
+    changed: int
+    flagged: int
+    active: int
+    work: int
+    sse: float
+    assign_ms: float
+    update_ms: float
+
+
+class DeviceLloyd:
+    """One GPU context over an (n, d) block of rows."""
+
+    def __init__(self, data, k: int, strategy: str = "lloyd", t_max: int = 10, *,
+                 device=None, kernel: str = "auto", groups: int = 0, comm=None,
+                 n_total: int | None = None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise nat.NativeError("no CUDA device: the B200 path has no CPU fallback")
+        self.lib = nat.load()
+        if strategy not in nat.STRAT_IDS:
+            raise ContractError(f"strategy {strategy!r} has no GPU implementation")
+        if kernel not in nat.KERNEL_IDS:
+            raise ContractError(f"unknown kernel {kernel!r}")
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None
+                                else (device.index if isinstance(device, torch.device)
+                                      else int(device)))
+        self.comm = comm
+        self.strategy = strategy
+        self.k = int(k)
+        self.t_max = int(t_max)
+
+        src = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(data))
+        if src.ndim != 2:
+            raise ContractError(f"expected a 2-D array, got shape {tuple(src.shape)}")
+        self.n, self.d = int(src.shape[0]), int(src.shape[1])
+        has_x64 = False
+        if src.dtype == torch.float64:
+            s32 = src.to(torch.float32)
+            has_x64 = not bool(torch.equal(s32.to(torch.float64), src))
+        if n_total is None:
+            n_total = self.n
+            if comm is not None:
+                import torch.distributed as dist
+                t = torch.tensor([self.n], dtype=torch.int64, device=self.dev)
+                dist.all_reduce(t, group=comm)
+                n_total = int(t.item())
+        self.n_total = int(n_total)
+
+        cfg = nat.LkConfig(n_local=self.n, n_total=self.n_total, d=self.d, k=self.k,
+                           strategy=nat.STRAT_IDS[strategy], groups=int(groups),
+                           t_max=max(1, self.t_max), kernel=nat.KERNEL_IDS[kernel],
+                           has_x64=int(has_x64), device=self.dev.index)
+        self.cfg = cfg
+        nbytes = ctypes.c_uint64(0)
+        nat.check(self.lib.lk_workspace_bytes(ctypes.byref(cfg), ctypes.byref(nbytes)),
+                  "lk_workspace_bytes")
+        with torch.cuda.device(self.dev):
+            self.ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.dev)
+        h = ctypes.c_void_p()
+        nat.check(self.lib.lk_ctx_create(ctypes.byref(h), ctypes.byref(cfg),
+                                          ctypes.c_void_p(self.ws.data_ptr()), nbytes.value),
+                  "lk_ctx_create")
+        self.ctx = h
+        ldx, dl, nlb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        nat.check(self.lib.lk_layout(h, ctypes.byref(ldx), ctypes.byref(dl), ctypes.byref(nlb)),
+                  "lk_layout")
+        self.ldx, self.delta_len, self.nlb = ldx.value, dl.value, nlb.value
+
+        self.x32 = self._view("x32", torch.float32, (self.n, self.ldx))
+        self.x64 = self._view("x64", torch.float64, (self.n, self.d)) if has_x64 else None
+        self.c64 = self._view("c64", torch.float64, (self.k, self.d))
+        self.labels = self._view("labels", torch.int32, (self.n,))
+        self.delta = self._view("delta", torch.int64, (self.delta_len,))
+        self.stats = self._view("stats", torch.int64, (max(1, self.t_max), nat.NSTAT))
+        self.sse_buf = self._view("sse", torch.float64, (max(1, self.t_max),))
+        self.qexp = self._view("qexp", torch.int32, (self.d + 1,))
+        self.counts = self._view("counts", torch.int64, (self.k,))
+        if strategy != "lloyd":
+            self.ub = self._view("ub", torch.float32, (self.n,))
+            self.lb = self._view("lb", torch.float32, (self.n, self.nlb))
+        self.h2d_bytes = 0
+        self._bind(src, has_x64)
+
+    # -- plumbing ---------------------------------------------------------
+    def _view(self, name, dtype, shape):
+        torch = _torch()
+        off, size = ctypes.c_uint64(), ctypes.c_uint64()
+        nat.check(self.lib.lk_buffer(self.ctx, nat.BUF[name], ctypes.byref(off),
+                                     ctypes.byref(size)), "lk_buffer")
+        numel = int(np.prod(shape))
+        esz = torch.empty((), dtype=dtype).element_size()
+        if numel * esz > size.value:
+            raise nat.NativeError(f"buffer {name} too small ({size.value} < {numel * esz})")
+        return self.ws[off.value: off.value + numel * esz].view(dtype).view(*shape)
+
+    def stream_handle(self):
+        torch = _torch()
+        return ctypes.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def _bind(self, src, has_x64):
+        torch = _torch()
+        with torch.cuda.device(self.dev):
+            if self.ldx != self.d:
+                self.x32.zero_()
+            if has_x64:
+                self.x64.copy_(src, non_blocking=True)
+                self.x32[:, : self.d].copy_(self.x64.to(torch.float32))
+                self.h2d_bytes += src.numel() * 8
+            else:
+                s32 = src if src.dtype == torch.float32 else src.to(torch.float32)
+                if self.ldx == self.d:
+                    self.x32.copy_(s32, non_blocking=True)
+                else:
+                    self.x32[:, : self.d].copy_(s32, non_blocking=True)
+                self.h2d_bytes += s32.numel() * 4
+            st = self.stream_handle()
+            nat.check(self.lib.lk_scan_points(self.ctx, st), "lk_scan_points")
+            if self.comm is not None:
+                import torch.distributed as dist
+                dist.all_reduce(self.qexp, op=dist.ReduceOp.MAX, group=self.comm)
+            nat.check(self.lib.lk_set_quant(self.ctx, st), "lk_set_quant")
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.lk_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- iteration --------------------------------------------------------
+    def set_centroids(self, init):
+        torch = _torch()
+        with torch.cuda.device(self.dev):
+            c = torch.as_tensor(np.ascontiguousarray(init, dtype=np.float64)) \
+                if not isinstance(init, torch.Tensor) else init.to(torch.float64)
+            self.c64.copy_(c, non_blocking=True)
+            self.h2d_bytes += c.numel() * 8
+            nat.check(self.lib.lk_set_centroids(self.ctx, ctypes.c_void_p(self.c64.data_ptr()),
+                                                self.stream_handle()), "lk_set_centroids")
+
+    def step(self, t: int):
+        """One iteration: assign (+recheck, +deltas), all-reduce, update."""
+        st = self.stream_handle()
+        nat.check(self.lib.lk_step_assign(self.ctx, int(t), st), "lk_step_assign")
+        if self.comm is not None:
+            import torch.distributed as dist
+            dist.all_reduce(self.delta, group=self.comm)
+        nat.check(self.lib.lk_step_update(self.ctx, int(t), st), "lk_step_update")
+
+    def launch_count(self) -> int:
+        return int(self.lib.lk_launch_count(self.ctx))
+
+    def profile(self, enable: bool):
+        nat.check(self.lib.lk_profile(self.ctx, int(enable)), "lk_profile")
+
+    def profile_read(self, cls: int):
+        ms, nl = ctypes.c_double(), ctypes.c_int64()
+        nat.check(self.lib.lk_profile_read(self.ctx, cls, ctypes.byref(ms), ctypes.byref(nl)),
+                  "lk_profile_read")
+        return ms.value, nl.value
+
+    def run(self, init, *, record_history: bool = True, check_every: int = 1):
+        """Run up to t_max iterations from ``init``; stop after the first with
+        changed == 0 (lloyd.py:169-171).  Returns a dict of host arrays."""
+        torch = _torch()
+        self.set_centroids(init)
+        T = self.t_max
+        res = {"iterations": 0, "converged": False, "history": [], "records": []}
+        if T <= 0:
+            res["centroids"] = np.array(init, dtype=np.float64, copy=True)
+            res["labels"] = np.full(self.n, -1, dtype=np.int64)
+            return res
+        with torch.cuda.device(self.dev):
+            stream = torch.cuda.current_stream(self.dev)
+            hist = (torch.empty((T, self.n), dtype=torch.int32, pin_memory=True)
+                    if record_history else None)
+            chg = torch.zeros(T, dtype=torch.int64, pin_memory=True)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                   torch.cuda.Event(enable_timing=True)) for _ in range(T)]
+            iters = T
+            converged = False
+            checked = 0
+            for t in range(1, T + 1):
+                e0, e1, e2 = ev[t - 1]
+                e0.record(stream)
+                st = self.stream_handle()
+                nat.check(self.lib.lk_step_assign(self.ctx, t, st), "lk_step_assign")
+                if self.comm is not None:
+                    import torch.distributed as dist
+                    dist.all_reduce(self.delta, group=self.comm)
+                e1.record(stream)
+                nat.check(self.lib.lk_step_update(self.ctx, t, st), "lk_step_update")
+                e2.record(stream)
+                if hist is not None:
+                    hist[t - 1].copy_(self.labels, non_blocking=True)
+                chg[t - 1].copy_(self.stats[t - 1, nat.STAT["changed_global"]], non_blocking=True)
+                if t % check_every == 0 or t == T:
+                    stream.synchronize()
+                    z = np.nonzero(chg[checked:t].numpy() == 0)[0]
+                    if len(z):
+                        iters = checked + int(z[0]) + 1
+                        converged = True
+                        break
+                    checked = t
+            stream.synchronize()
+            stats = self.stats[:iters].to("cpu").numpy().copy()
+            sse = self.sse_buf[:iters].to("cpu").numpy().copy()
+            if self.comm is not None:
+                import torch.distributed as dist
+                st_t = torch.as_tensor(stats, device=self.dev)
+                dist.all_reduce(st_t, group=self.comm)
+                g = st_t.to("cpu").numpy()
+                g[:, nat.STAT["changed_global"]] = stats[:, nat.STAT["changed_global"]]
+                stats = g
+            recs = []
+            for t in range(iters):
+                e0, e1, e2 = ev[t]
+                recs.append(IterRecord(
+                    changed=int(stats[t, nat.STAT["changed_global"]]),
+                    flagged=int(stats[t, nat.STAT["flagged"]]),
+                    active=int(stats[t, nat.STAT["active"]]),
+                    work=int(stats[t, nat.STAT["work"]]),
+                    sse=float(sse[t]),
+                    assign_ms=e0.elapsed_time(e1),
+                    update_ms=e1.elapsed_time(e2)))
+            res["iterations"] = iters
+            res["converged"] = converged
+            res["records"] = recs
+            res["centroids"] = self.c64.to("cpu").numpy().copy()
+            res["labels"] = self.labels.to("cpu").numpy().astype(np.int64)
+            if hist is not None:
+                h = hist[:iters].numpy()
+                res["history"] = [h[t].astype(np.int64) for t in range(iters)]
+        return res

