@@ -211,3 +211,137 @@ int32_t lko_run_lloyd(const double *X, int64_t n, int32_t d, int32_t k, const do
     free(C); free(Cn); free(prev); free(cur);
     return it;
 }
+
+/* ------------------------------------------------------------------------
+ * Hamerly (pruners.py:222-264 + run_pruner :862-923) in fp64: the reference's
+ * bounded strategy, restated for the CPU baseline.  Pruning uses the bounds
+ * with a 1e-10 relative safety margin, and every rescanned row uses the exact
+ * numpy-order distances, so labels are identical to lko_run_lloyd.
+ */
+typedef struct {
+    const double *X, *C;
+    const double *s, *drift;
+    double dmax1, dmax2;
+    int32_t amax;
+    int64_t r0, r1;
+    int32_t d, k, first;
+    int64_t *lab;
+    double *ub, *lb;
+    int64_t dist;     /* distances evaluated (reference accounting) */
+} ham_job;
+
+static void *ham_worker(void *arg)
+{
+    ham_job *jb = (ham_job *)arg;
+    const int32_t d = jb->d, k = jb->k;
+    double *dist = (double *)malloc(sizeof(double) * (size_t)k);
+    double *scr = (double *)malloc(sizeof(double) * (size_t)(d > 0 ? d : 1));
+    int64_t nd = 0;
+    for (int64_t i = jb->r0; i < jb->r1; i++) {
+        const double *x = jb->X + i * d;
+        if (!jb->first) {
+            int64_t a = jb->lab[i];
+            double u = jb->ub[i] + jb->drift[a];
+            double l = jb->lb[i] - (a == jb->amax ? jb->dmax2 : jb->dmax1);
+            double gate = l > jb->s[a] ? l : jb->s[a];
+            jb->ub[i] = u;
+            jb->lb[i] = l;
+            if (gate > u * (1.0 + 1e-10)) continue;
+            lko_dist_row(x, jb->C + a * d, 1, d, &u, scr);
+            nd += 1;
+            jb->ub[i] = u;
+            if (gate > u * (1.0 + 1e-10)) continue;
+            nd += k - 1;
+        } else {
+            nd += k;
+        }
+        lko_dist_row(x, jb->C, k, d, dist, scr);
+        double b1, b2;
+        row_top2(dist, k, jb->lab + i, &b1, &b2);
+        jb->ub[i] = b1;
+        jb->lb[i] = b2;
+    }
+    jb->dist = nd;
+    free(dist);
+    free(scr);
+    return NULL;
+}
+
+int32_t lko_run_hamerly(const double *X, int64_t n, int32_t d, int32_t k, const double *init,
+                        int32_t t_max, int32_t nthreads, int64_t *history, double *centroids_out,
+                        int64_t *labels_out, int64_t *changed_out, int64_t *dist_out,
+                        int32_t *converged)
+{
+    size_t kd = (size_t)k * (size_t)d;
+    double *C = (double *)malloc(sizeof(double) * kd);
+    double *Cn = (double *)malloc(sizeof(double) * kd);
+    double *s = (double *)malloc(sizeof(double) * (size_t)k);
+    double *drift = (double *)calloc((size_t)k, sizeof(double));
+    double *tmp = (double *)malloc(sizeof(double) * (size_t)k);
+    double *scr = (double *)malloc(sizeof(double) * (size_t)(d > 0 ? d : 1));
+    int64_t *prev = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t *cur = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    double *ub = (double *)malloc(sizeof(double) * (size_t)n);
+    double *lb = (double *)malloc(sizeof(double) * (size_t)n);
+    memcpy(C, init, sizeof(double) * kd);
+    for (int64_t i = 0; i < n; i++) prev[i] = -1;
+    if (nthreads < 1) nthreads = 1;
+    if ((int64_t)nthreads > n) nthreads = (int32_t)(n > 0 ? n : 1);
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    ham_job *jobs = (ham_job *)malloc(sizeof(ham_job) * (size_t)nthreads);
+    *converged = 0;
+    int32_t it = 0;
+    double dmax1 = 0, dmax2 = 0;
+    int32_t amax = -1;
+    while (it < t_max) {
+        if (it > 0) {
+            /* s_j = 1/2 min_{j' != j} |c_j - c_j'| (bounds.py:38-47) */
+            for (int32_t j = 0; j < k; j++) {
+                lko_dist_row(C + (int64_t)j * d, C, k, d, tmp, scr);
+                double m = INFINITY;
+                for (int32_t jj = 0; jj < k; jj++)
+                    if (jj != j && tmp[jj] < m) m = tmp[jj];
+                s[j] = 0.5 * m * (1.0 - 1e-10);
+            }
+        }
+        if (it > 0) memcpy(cur, prev, sizeof(int64_t) * (size_t)n);
+        for (int32_t t = 0; t < nthreads; t++) {
+            ham_job *jb = &jobs[t];
+            jb->X = X; jb->C = C; jb->s = s; jb->drift = drift;
+            jb->dmax1 = dmax1; jb->dmax2 = dmax2; jb->amax = amax;
+            jb->r0 = n * t / nthreads; jb->r1 = n * (t + 1) / nthreads;
+            jb->d = d; jb->k = k; jb->first = (it == 0);
+            jb->lab = cur; jb->ub = ub; jb->lb = lb; jb->dist = 0;
+            if (nthreads == 1) ham_worker(jb);
+            else pthread_create(&th[t], NULL, ham_worker, jb);
+        }
+        int64_t nd = 0;
+        for (int32_t t = 0; t < nthreads; t++) {
+            if (nthreads > 1) pthread_join(th[t], NULL);
+            nd += jobs[t].dist;
+        }
+        int64_t ch = 0;
+        for (int64_t i = 0; i < n; i++) ch += (cur[i] != prev[i]);
+        lko_refine_full(X, n, d, cur, k, C, Cn, NULL);
+        /* drifts (bounds.py:31-35), top-2 for _max_other (pruners.py:58-67) */
+        dmax1 = 0; dmax2 = 0; amax = -1;
+        for (int32_t j = 0; j < k; j++) {
+            lko_dist_row(Cn + (int64_t)j * d, C + (int64_t)j * d, 1, d, &drift[j], scr);
+            drift[j] *= (1.0 + 1e-10);
+            if (drift[j] > dmax1) { dmax2 = dmax1; dmax1 = drift[j]; amax = j; }
+            else if (drift[j] > dmax2) dmax2 = drift[j];
+        }
+        memcpy(C, Cn, sizeof(double) * kd);
+        if (history) memcpy(history + (int64_t)it * n, cur, sizeof(int64_t) * (size_t)n);
+        if (changed_out) changed_out[it] = ch;
+        if (dist_out) dist_out[it] = nd;
+        memcpy(prev, cur, sizeof(int64_t) * (size_t)n);
+        it++;
+        if (ch == 0) { *converged = 1; break; }
+    }
+    memcpy(centroids_out, C, sizeof(double) * kd);
+    if (labels_out) memcpy(labels_out, prev, sizeof(int64_t) * (size_t)n);
+    free(C); free(Cn); free(s); free(drift); free(tmp); free(scr); free(prev); free(cur);
+    free(ub); free(lb); free(th); free(jobs);
+    return it;
+}

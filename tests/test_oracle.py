@@ -61,3 +61,20 @@ def test_threads_do_not_change_results(oracle):
     b = oracle.assign_full(g["data"], g["init"], nthreads=7)
     for u, v in zip(a, b):
         assert np.array_equal(u, v)
+
+
+@pytest.mark.parametrize("name", ["pruners_blobs", "pruners_dups", "pruners_uniform",
+                                  "cfg1_small", "cfg2_small", "cfg5_small", "ac01_c8_s1"])
+def test_oracle_hamerly_is_label_identical(oracle, name):
+    """The CPU Hamerly port (bench baseline) reproduces the reference trajectory."""
+    g = load_golden(name)
+    k, t_max = int(g["k"]), int(g["t_max"])
+    out = oracle.run_hamerly(g["data"], k, g["init"], t_max, nthreads=3)
+    assert out["iterations"] == len(g["history"])
+    for a, b in zip(out["history"], g["history"]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(out["centroids"], g["centroids"])
+    n = g["data"].shape[0]
+    assert out["dist_comps"][0] == n * k
+    if len(out["dist_comps"]) > 2:
+        assert min(out["dist_comps"][1:]) < n * k
