@@ -548,49 +548,75 @@ __global__ void __launch_bounds__(1024) k_update_global(DevState S, const double
 }
 
 // s_j = 1/2 min_{j' != j} |c_j - c_j'|, certified lower bound (fp32 diff form).
+// 64 x 64 (j, j') tiles per block, 4 x 4 pairs per thread, d streamed in
+// chunks of 32 through shared memory; per-j minima combined with atomicMin
+// on the (nonnegative) float bits.  s_half must be +inf-filled beforehand.
+constexpr int kHsT = 64;
+constexpr int kHsDC = 32;
+
 __global__ void __launch_bounds__(kThreads) k_half_sep(DevState S) {
     if (*S.done) return;
-    __shared__ float ct[64][33];
-    __shared__ float cnt_s[64];
-    const int j = blockIdx.x * kThreads + threadIdx.x;
-    const float rho = simt_rel_err(S.d);
-    float best = INFINITY;
-    for (int j0 = 0; j0 < S.k; j0 += 64) {
-        float acc[64];
+    __shared__ float ta[kHsDC][kHsT + 4];
+    __shared__ float tb[kHsDC][kHsT + 4];
+    const int j0 = blockIdx.y * kHsT, jp0 = blockIdx.x * kHsT;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads
+    float acc[4][4];
 #pragma unroll
-        for (int c = 0; c < 64; c++) acc[c] = 0.f;
-        for (int z0 = 0; z0 < S.d; z0 += 32) {
-            __syncthreads();
-            for (int e = threadIdx.x; e < 64 * 32; e += kThreads) {
-                int jj = e / 32, z = e % 32;
-                ct[jj][z] = (j0 + jj < S.k && z0 + z < S.d) ? S.C32[(int64_t)(j0 + jj) * S.ldc + z0 + z] : 0.f;
-            }
-            if (threadIdx.x < 64) cnt_s[threadIdx.x] = (j0 + threadIdx.x < S.k) ? S.cnorm[j0 + threadIdx.x] : 0.f;
-            __syncthreads();
-            if (j < S.k) {
-                for (int z = 0; z < 32 && z0 + z < S.d; z++) {
-                    float xv = S.C32[(int64_t)j * S.ldc + z0 + z];
+    for (int a = 0; a < 4; a++)
 #pragma unroll
-                    for (int c = 0; c < 64; c++) {
-                        float t = xv - ct[c][z];
-                        acc[c] = fmaf(t, t, acc[c]);
-                    }
-                }
-            }
+        for (int b = 0; b < 4; b++) acc[a][b] = 0.f;
+    for (int z0 = 0; z0 < S.d; z0 += kHsDC) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kHsT * kHsDC; e += kThreads) {
+            int r = e / kHsDC, z = e % kHsDC;
+            int zz = z0 + z;
+            ta[z][r] = (j0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(j0 + r) * S.ldc + zz] : 0.f;
+            tb[z][r] = (jp0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(jp0 + r) * S.ldc + zz] : 0.f;
         }
-        if (j < S.k) {
-            float cj = S.cnorm[j];
+        __syncthreads();
+#pragma unroll 8
+        for (int z = 0; z < kHsDC; z++) {
+            float av[4], bv[4];
 #pragma unroll
-            for (int c = 0; c < 64; c++) {
-                int jj = j0 + c;
-                if (jj < S.k && jj != j) {
-                    float lbd = (sqrtf(acc[c]) - kU32 * (cj + cnt_s[c])) * (1.0f - rho);
-                    best = fminf(best, lbd);
+            for (int a = 0; a < 4; a++) av[a] = ta[z][ty + 16 * a];
+#pragma unroll
+            for (int b = 0; b < 4; b++) bv[b] = tb[z][tx + 16 * b];
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    float t = av[a] - bv[b];
+                    acc[a][b] = fmaf(t, t, acc[a][b]);
                 }
-            }
         }
     }
-    if (j < S.k) S.s_half[j] = isinf(best) ? INFINITY : fmaxf(0.5f * best * (1.0f - kU32 * 4), 0.f);
+    const float rho = simt_rel_err(S.d);
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+        const int j = j0 + ty + 16 * a;
+        float best = INFINITY;
+        if (j < S.k) {
+            const float cj = S.cnorm[j];
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int jp = jp0 + tx + 16 * b;
+                if (jp < S.k && jp != j) {
+                    float lbd = (sqrtf(acc[a][b]) - kU32 * (cj + S.cnorm[jp])) * (1.0f - rho);
+                    best = fminf(best, fmaxf(0.5f * lbd * (1.0f - 4.0f * kU32), 0.f));
+                }
+            }
+        }
+        // min over the 16 threads sharing row j (same ty, lanes tx 0..15)
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) best = fminf(best, __shfl_xor_sync(LK_FULL_MASK, best, o, 16));
+        if (tx == 0 && j < S.k && best < INFINITY) atomicMin((int*)(S.s_half + j), __float_as_int(best));
+    }
+}
+
+__global__ void k_fill_inf(DevState S) {
+    if (*S.done) return;
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < S.k) S.s_half[j] = INFINITY;
 }
 
 // Per-dimension max |x| exponents (frexp convention: |x| < 2^e) of the local
@@ -724,7 +750,10 @@ lk_status launch_update(const DevState& S, const double* qscale, const double* q
     k_update_global<<<1, 1024, 0, st>>>(S, sse_part, t);
     LK_LAUNCH_CHECK();
     if (need_half) {
-        k_half_sep<<<(S.k + kThreads - 1) / kThreads, kThreads, 0, st>>>(S);
+        k_fill_inf<<<(S.k + kThreads - 1) / kThreads, kThreads, 0, st>>>(S);
+        LK_LAUNCH_CHECK();
+        dim3 g((S.k + kHsT - 1) / kHsT, (S.k + kHsT - 1) / kHsT);
+        k_half_sep<<<g, kThreads, 0, st>>>(S);
         LK_LAUNCH_CHECK();
     }
     return LK_OK;
