@@ -37,6 +37,7 @@ enum InternalBuf {
     // internal
     B_C64_PREV, B_C32, B_CNORM, B_DRIFT, B_SHALF, B_GDRIFT, B_SCAL, B_MOVED, B_FLAGGED, B_WORK,
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
+    B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO,
     B_COUNT_
 };
 
@@ -61,6 +62,10 @@ static int32_t nlb_for(const lk_config& c, int32_t* groups) {
     if (g > c.k) g = c.k;
     *groups = g;
     return g < 1 ? 1 : g;
+}
+
+static bool tc_enabled(const lk_config& c) {
+    return c.kernel == LK_KERNEL_TC || (c.kernel == LK_KERNEL_AUTO && c.d >= 32);
 }
 
 static bool make_layout(const lk_config& c, Layout* L) {
@@ -102,6 +107,18 @@ static bool make_layout(const lk_config& c, Layout* L) {
     L->size[B_DONE] = 16;
     L->size[B_SSE_PART] = (uint64_t)k * 8;
     L->size[B_PW_PROG] = 4096 * 4;
+    if (tc_enabled(c) && L->ldx % 4 == 0) {
+        const int64_t kpad = (k + 255) / 256 * 256;
+        L->size[B_XLO] = (uint64_t)n * L->ldx * 4;
+        L->size[B_XN2] = (uint64_t)n * 4;
+        L->size[B_CHI] = (uint64_t)kpad * L->ldc * 4;
+        L->size[B_CLO] = (uint64_t)kpad * L->ldc * 4;
+        L->size[B_CN2] = (uint64_t)kpad * 4;
+        if (c.strategy != LK_STRAT_LLOYD) {
+            L->size[B_XG_HI] = (uint64_t)n * L->ldx * 4;
+            L->size[B_XG_LO] = (uint64_t)n * L->ldx * 4;
+        }
+    }
     uint64_t off = 0;
     for (int b = 0; b < B_COUNT_; b++) {
         L->off[b] = off;
@@ -280,6 +297,13 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.stats = buf<int64_t>(c, B_STATS);
     S.sse = buf<double>(c, B_SSE);
     S.pw_prog = buf<int32_t>(c, B_PW_PROG);
+    S.Xlo = buf<float>(c, B_XLO);
+    S.xn2 = buf<float>(c, B_XN2);
+    S.Chi = buf<float>(c, B_CHI);
+    S.Clo = buf<float>(c, B_CLO);
+    S.cn2 = buf<float>(c, B_CN2);
+    S.Xg_hi = buf<float>(c, B_XG_HI);
+    S.Xg_lo = buf<float>(c, B_XG_LO);
 
     std::vector<int32_t> prog;
     build_pw(0, cfg->d, prog);
@@ -336,7 +360,13 @@ lk_status lk_scan_points(lk_ctx* c, void* stream) {
     k_fill_i32<<<1, 256, 0, st>>>(c->S.qexp, c->cfg.d + 1, -1100);
     LK_LAUNCH_CHECK();
     c->launches += 2;
-    return lkh::launch_scan_exp(c->S, c->sms, st);
+    lk_status s = lkh::launch_scan_exp(c->S, c->sms, st);
+    if (s != LK_OK) return s;
+    if (c->S.Xlo) {
+        c->launches += 1;
+        return lkh::launch_tc_prep_points(c->S, c->sms, st);
+    }
+    return LK_OK;
 }
 
 lk_status lk_set_quant(lk_ctx* c, void* stream) {
@@ -366,19 +396,33 @@ lk_status lk_set_quant(lk_ctx* c, void* stream) {
     return LK_OK;
 }
 
-static __global__ void k_init_centroids(lk::DevState S) {
+static __global__ void k_init_centroids(lk::DevState S, int kpad) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = blockIdx.x * (blockDim.x / 32) + warp;
-    if (j >= S.k) return;
-    double cn2 = 0.0;
-    for (int z = lane; z < S.ldc; z += 32) {
-        float v = z < S.d ? (float)S.C64[(int64_t)j * S.d + z] : 0.f;
-        S.C32[(int64_t)j * S.ldc + z] = v;
-        if (z < S.d) S.C64_prev[(int64_t)j * S.d + z] = S.C64[(int64_t)j * S.d + z];
-        cn2 = fma((double)v, (double)v, cn2);
+    if (j >= S.k) {
+        if (j < kpad && S.cn2 && lane == 0) S.cn2[j] = INFINITY;
+        return;
     }
-    for (int o = 16; o > 0; o >>= 1) cn2 += __shfl_xor_sync(LK_FULL_MASK, cn2, o);
+    double cn2 = 0.0, c2 = 0.0;
+    for (int z = lane; z < S.ldc; z += 32) {
+        double c = z < S.d ? S.C64[(int64_t)j * S.d + z] : 0.0;
+        float v = (float)c;
+        S.C32[(int64_t)j * S.ldc + z] = v;
+        if (z < S.d) S.C64_prev[(int64_t)j * S.d + z] = c;
+        cn2 = fma((double)v, (double)v, cn2);
+        c2 = fma(c, c, c2);
+        if (S.Chi) {
+            float hi = lk::tf32_trunc(v);
+            S.Chi[(int64_t)j * S.ldc + z] = hi;
+            S.Clo[(int64_t)j * S.ldc + z] = v - hi;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        cn2 += __shfl_xor_sync(LK_FULL_MASK, cn2, o);
+        c2 += __shfl_xor_sync(LK_FULL_MASK, c2, o);
+    }
     if (lane == 0) {
+        if (S.cn2) S.cn2[j] = (float)c2;
         float cn = __double2float_ru(sqrt(cn2) * (1.0 + 1e-12));
         S.cnorm[j] = cn;
         S.drift[j] = 0.f;
@@ -402,7 +446,8 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     LK_CUDA_CHECK(cudaMemsetAsync(S.done, 0, 16, st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.stats, 0, c->L.size[B_STATS], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.sse, 0, c->L.size[B_SSE], st));
-    k_init_centroids<<<(int)((k + 7) / 8), 256, 0, st>>>(S);
+    const int kpad = (int)((k + 255) / 256 * 256);
+    k_init_centroids<<<(kpad + 7) / 8, 256, 0, st>>>(S, kpad);
     LK_LAUNCH_CHECK();
     c->launches += 1;
     c->centroids_set = true;
@@ -424,9 +469,7 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
     int64_t* stat = S.stats + (int64_t)(t - 1) * LK_NSTAT;
     LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
     const int64_t n = c->cfg.n_local;
-    const bool use_tc = (c->cfg.kernel == LK_KERNEL_TC ||
-                         (c->cfg.kernel == LK_KERNEL_AUTO && c->cfg.d >= 32)) &&
-                        lkh::tc_supported(S);
+    const bool use_tc = lkh::tc_supported(S);
     lk_status s;
     if (n > 0) {
         if (c->cfg.strategy == LK_STRAT_LLOYD || t == 1) {
@@ -442,7 +485,8 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
                 if (s != LK_OK) return s;
             }
             ProfScope p(c, 0, st);
-            s = lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
+            s = use_tc ? lkh::launch_assign_tc(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st)
+                       : lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
             if (s != LK_OK) return s;
             c->launches += 2;
         }

@@ -51,7 +51,19 @@ struct DevState {
     double* sse;            // [t_max]
     int32_t* pw_prog;       // numpy pairwise-sum program for the fp64 recheck
     int32_t pw_len;
+    // tensor-core (3xTF32) path; null when disabled
+    float* Xlo;             // [n, ldx] x - trunc_tf32(x)
+    float* xn2;             // [n] ||x||^2 (fp64 rounded to fp32)
+    float* Chi;             // [k, ldc] trunc_tf32(c32)
+    float* Clo;             // [k, ldc] c32 - Chi
+    float* cn2;             // [k_pad] ||c||^2, +inf beyond k
+    float* Xg_hi;           // [n, ldx] gathered rescan rows
+    float* Xg_lo;           // [n, ldx]
 };
+
+__device__ __forceinline__ float tf32_trunc(float x) {
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
 
 __device__ __forceinline__ unsigned lane_id() {
     unsigned r;
@@ -86,6 +98,36 @@ __device__ __forceinline__ void warp_count(bool pred, int64_t* counter) {
 __device__ __forceinline__ void warp_add(int64_t v, int64_t* counter) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(LK_FULL_MASK, v, o);
     if (lane_id() == 0 && v) atomicAdd((unsigned long long*)counter, (unsigned long long)v);
+}
+
+// Block-aggregated append: one global atomic per block per call.  Every
+// thread of the block must call it (block-uniform control flow); scratch is
+// >= (blockDim/32 + 1) ints of shared memory.  Returns the slot (or -1).
+__device__ __forceinline__ int64_t block_append(bool pred, unsigned long long* counter,
+                                                unsigned long long* scratch) {
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned m = __ballot_sync(LK_FULL_MASK, pred);
+    if (lane_id() == 0) scratch[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < nw; w++) {
+            unsigned long long c = scratch[w];
+            scratch[w] = tot;
+            tot += c;
+        }
+        scratch[nw] = tot ? atomicAdd(counter, tot) : 0ull;
+    }
+    __syncthreads();
+    int64_t pos = pred ? (int64_t)(scratch[nw] + scratch[warp] + __popc(m & lanemask_lt())) : -1;
+    __syncthreads();  // scratch reusable by the next call
+    return pos;
+}
+
+// Block-aggregated counter increment (block-uniform).
+__device__ __forceinline__ void block_count(bool pred, int64_t* counter,
+                                            unsigned long long* scratch) {
+    block_append(pred, (unsigned long long*)counter, scratch);
 }
 
 // Nonnegative-float atomic max via integer ordering.

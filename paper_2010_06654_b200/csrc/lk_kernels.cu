@@ -30,7 +30,7 @@ constexpr int kThreads = 256;
 
 // U1: certified upper bound on the true distance to candidate j1.
 // L2: certified lower bound on the true distance to every other centroid.
-// Must be called by all 32 lanes of a warp (valid=false lanes just vote).
+// Must be called by every thread of the block (valid=false threads just vote).
 __device__ __forceinline__ void row_finish(const DevState& S, bool valid, int64_t row, int j1,
                                            float U1, float L2, int64_t* stat) {
     bool certain = valid && (L2 > U1);
@@ -46,9 +46,10 @@ __device__ __forceinline__ void row_finish(const DevState& S, bool valid, int64_
             S.lb[row * S.nlb] = fmaxf(L2, 0.0f);
         }
     }
-    int64_t pos = warp_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED));
+    __shared__ unsigned long long scr[kThreads / 32 + 1];
+    int64_t pos = block_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
     if (moved) S.moved[pos] = make_int2((int)row, old);
-    int64_t fpos = warp_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED));
+    int64_t fpos = block_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED), scr);
     if (flag) S.flagged[fpos] = (int)row;
 }
 
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(kRcWarps * 32) k_recheck_fp64(DevState S, int6
 
 __global__ void __launch_bounds__(kThreads) k_filter_hamerly(DevState S, int64_t* stat) {
     if (*S.done) return;
+    __shared__ unsigned long long scr[kThreads / 32 + 1];
     const float dmax1 = S.scal[1], dmax2 = S.scal[2];
     const int amax = __float_as_int(S.scal[3]);
     const float rho = simt_rel_err(S.d);
@@ -373,8 +375,8 @@ __global__ void __launch_bounds__(kThreads) k_filter_hamerly(DevState S, int64_t
             S.ub[i] = u;
             S.lb[i] = l;
         }
-        warp_count(active, stat + LK_STAT_ACTIVE);
-        int64_t pos = warp_append(need, (unsigned long long*)(stat + LK_STAT_WORK));
+        block_count(active, stat + LK_STAT_ACTIVE, scr);
+        int64_t pos = block_append(need, (unsigned long long*)(stat + LK_STAT_WORK), scr);
         if (need) S.work[pos] = (int)i;
     }
 }
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
     const int64_t* dQ = dN + S.k;
     int64_t cnt = S.counts[j] + dN[j];
     int64_t qs = S.qsum[j] + dQ[j];
-    double s2 = 0.0, drift2 = 0.0, cn2 = 0.0;
+    double s2 = 0.0, drift2 = 0.0, cn2 = 0.0, c2 = 0.0;
     for (int z = lane; z < S.d; z += 32) {
         int64_t sv = S.sums[(int64_t)j * S.d + z] + dS[(int64_t)j * S.d + z];
         S.sums[(int64_t)j * S.d + z] = sv;
@@ -476,13 +478,21 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
         float c32 = (float)c;
         S.C32[(int64_t)j * S.ldc + z] = c32;
         cn2 = fma((double)c32, (double)c32, cn2);
+        if (S.Chi) {
+            float hi = tf32_trunc(c32);
+            S.Chi[(int64_t)j * S.ldc + z] = hi;
+            S.Clo[(int64_t)j * S.ldc + z] = c32 - hi;
+            c2 = fma(c, c, c2);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         s2 += __shfl_xor_sync(LK_FULL_MASK, s2, o);
         drift2 += __shfl_xor_sync(LK_FULL_MASK, drift2, o);
         cn2 += __shfl_xor_sync(LK_FULL_MASK, cn2, o);
+        c2 += __shfl_xor_sync(LK_FULL_MASK, c2, o);
     }
     if (lane == 0) {
+        if (S.cn2) S.cn2[j] = (float)c2;
         S.counts[j] = cnt;
         S.qsum[j] = qs;
         S.drift[j] = drift2 > 0.0 ? __double2float_ru(sqrt(drift2) * (1.0 + 1e-12)) : 0.f;
@@ -679,7 +689,7 @@ static lk_status launch_reg(const DevState& S, const int32_t* rowlist, const int
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
         attr_set = true;
     }
-    int grid = grid_for(max_rows, kThreads * RPT, sms * 4);
+    int grid = grid_for(max_rows, kThreads * RPT, sms * 6);
     k_assign_reg<DP, RPT><<<grid, kThreads, smem, st>>>(S, rowlist, rowcount, stat, tile_k);
     LK_LAUNCH_CHECK();
     return LK_OK;

@@ -1,15 +1,495 @@
-// lk_tc.cu -- tcgen05 (5th-gen tensor core) assignment path.  Placeholder
-// until the 3xTF32 kernel lands: reports unsupported so the SIMT path runs.
+// lk_tc.cu -- tcgen05 (5th-gen tensor core) assignment kernel for d >= 32.
+//
+// Replaces the fp32 SIMT scan of assign_full (lloyd.py:69-75 / dist_matrix
+// core.py:98-108) with a dot-product contraction on the tensor cores:
+//
+//   D'(i, j) = ||c_j||^2 - 2 x_i . c_j      (order-equivalent to ||x_i - c_j||^2)
+//
+// x . c is computed in 3xTF32 (x = x_hi + x_lo, c = c_hi + c_lo;
+// x_hi c_hi + x_hi c_lo + x_lo c_hi) with fp32 accumulation in TMEM.  The
+// epilogue keeps a per-row top-2 and certifies the winner with a rigorous
+// error bound; rows it cannot certify go to
+// the exact fp64 recheck, so labels equal the fp64 oracle's.
+//
+// Structure (one persistent CTA per SM, 192 threads):
+//   warp 0      TMA producer (one elected lane): A = point rows (x_hi, x_lo),
+//               B = centroid rows (c_hi, c_lo), 32-float K chunks, 128B swizzle
+//   warp 1      MMA issuer (one elected lane) + TMEM allocator
+//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, top-2 per row
+// TMEM holds two BN-column fp32 accumulators (double buffer), so the epilogue
+// of centroid tile t overlaps the MMAs of tile t+1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "lk_common.cuh"
 #include "lk_internal.h"
+
+namespace lk {
+namespace tc {
+
+constexpr int BM = 128;        // rows per tile (UMMA M)
+constexpr int KC = 32;         // fp32 elements per K chunk (128 bytes)
+constexpr int UK = 8;          // UMMA K for kind::tf32
+constexpr int kEpiWarps = 4;
+constexpr int kThreadsTC = 64 + 32 * kEpiWarps;
+
+template <int BN>
+struct Smem {
+    static constexpr int A_BYTES = BM * KC * 4;   // 16 KB
+    static constexpr int B_BYTES = BN * KC * 4;   // 16/32 KB
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int STAGES = BN == 256 ? 2 : 3;
+    static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// ---- PTX helpers -----------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    while (!mbar_try(addr, parity)) {
+    }
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
+}
+
+// K-major, 128B-swizzled UMMA shared-memory descriptor (SBO = 8 rows x 128 B).
+__device__ __forceinline__ uint64_t umma_desc(const void* p) {
+    uint64_t a = (uint64_t)(smem_u32(p) >> 4) & 0x3FFF;
+    return a | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, K-major A and B.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+// ---- certification (D-space error bound) ------------------------------------
+
+// |D_true - D~| <= kappa * |x| |c| + 8u (|x|^2 + |c|^2) for the 3xTF32 form;
+// kappa = 2 (3.1 * 2^-20 + (3d + 1) * 2^-22 * 1.01)  (split truncation terms +
+// fp32 accumulation with a truncation-safe unit).
+__device__ __forceinline__ float tc_kappa(int d) {
+    return 2.0f * (3.1f * 9.5367431640625e-07f + (float)(3 * d + 1) * 2.384185791015625e-07f * 1.01f);
+}
+
+// ---- the kernel --------------------------------------------------------------
+
+struct TcArgs {
+    int64_t m;            // rows of A (n for a full scan, worklist size for a rescan)
+    const int32_t* rowlist;   // A row r -> global row (nullptr: identity)
+    const int64_t* rowcount;  // device row count (overrides m when non-null)
+    int n_ct;             // centroid tiles
+    int n_kc;             // K chunks
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    k_assign_tc(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                DevState S, TcArgs A, int64_t* stat) {
+    if (*S.done) return;
+    using SM = Smem<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + SM::STAGES * SM::STAGE_BYTES);
+    uint64_t* empty = full + SM::STAGES;
+    uint64_t* tfull = empty + SM::STAGES;   // [2]
+    uint64_t* tempty = tfull + 2;           // [2]
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t m = A.rowcount ? *A.rowcount : A.m;
+    const int64_t n_rt = (m + BM - 1) / BM;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < SM::STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], kEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_map(&map_ahi);
+        prefetch_map(&map_alo);
+        prefetch_map(&map_bhi);
+        prefetch_map(&map_blo);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x) {
+                for (int ct = 0; ct < A.n_ct; ct++) {
+                    for (int kc = 0; kc < A.n_kc; kc++) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* st = smem + stage * SM::STAGE_BYTES;
+                        mbar_expect_tx(&full[stage], SM::STAGE_BYTES);
+                        const int k0 = kc * KC;
+                        tma_load_2d(&map_ahi, &full[stage], st, k0, (int)(rt * BM));
+                        tma_load_2d(&map_alo, &full[stage], st + SM::A_BYTES, k0, (int)(rt * BM));
+                        tma_load_2d(&map_bhi, &full[stage], st + 2 * SM::A_BYTES, k0, ct * BN);
+                        tma_load_2d(&map_blo, &full[stage], st + 2 * SM::A_BYTES + SM::B_BYTES, k0,
+                                    ct * BN);
+                        if (++stage == SM::STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x) {
+                for (int ct = 0; ct < A.n_ct; ct++) {
+                    mbar_wait(&tempty[acc], acc_phase ^ 1);
+                    tc_fence_after();
+                    const uint32_t tmem_d = tmem_base + acc * BN;
+                    for (int kc = 0; kc < A.n_kc; kc++) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        uint8_t* st = smem + stage * SM::STAGE_BYTES;
+                        const uint64_t dahi = umma_desc(st);
+                        const uint64_t dalo = umma_desc(st + SM::A_BYTES);
+                        const uint64_t dbhi = umma_desc(st + 2 * SM::A_BYTES);
+                        const uint64_t dblo = umma_desc(st + 2 * SM::A_BYTES + SM::B_BYTES);
+#pragma unroll
+                        for (int k = 0; k < KC / UK; k++) {
+                            const uint64_t off = (uint64_t)((k * UK * 4) >> 4);
+                            // small terms first, then the dominant hi*hi term
+                            mma_tf32(tmem_d, dalo + off, dbhi + off, idesc, (kc | k) != 0);
+                            mma_tf32(tmem_d, dahi + off, dblo + off, idesc, 1);
+                            mma_tf32(tmem_d, dahi + off, dbhi + off, idesc, 1);
+                        }
+                        mma_commit(&empty[stage]);
+                        if (++stage == SM::STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    mma_commit(&tfull[acc]);
+                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                }
+            }
+        }
+    } else {
+        // ===== epilogue: warps 2..5, lane quarter = warp % 4 =====
+        const int q = warp & 3;
+        const int row_in_tile = q * 32 + lane;
+        const float kappa = tc_kappa(S.d);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x) {
+            float b1 = INFINITY, b2 = INFINITY;
+            int j1 = 0;
+            for (int ct = 0; ct < A.n_ct; ct++) {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+                const int jbase = ct * BN;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(taddr + c0, v);
+                    const int jb = jbase + c0;
+                    // cn2 is padded with +inf beyond k (zero-filled B rows give v = 0)
+                    const float4* cp = reinterpret_cast<const float4*>(S.cn2 + jb);
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; c4++) {
+                        const float4 cv = __ldg(cp + c4);
+                        const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            const float dp = fmaf(-2.0f, v[c4 * 4 + e], cc[e]);
+                            if (dp < b1) { b2 = b1; b1 = dp; j1 = jb + c4 * 4 + e; }
+                            else b2 = fminf(b2, dp);
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+            // certify this row
+            const int64_t r = rt * BM + row_in_tile;
+            const bool valid = r < m;
+            int64_t row = 0;
+            bool certain = false, flag = false, moved = false;
+            int old = 0;
+            if (valid) {
+                row = A.rowlist ? (int64_t)A.rowlist[r] : r;
+                const float xn2 = S.xn2[row];
+                const float xn = sqrtf(xn2) * (1.0f + 2 * kU32);
+                const float cn1 = S.cnorm[j1];
+                const float cmax = S.scal[0];
+                const float e1 = kappa * xn * cn1 + 8.0f * kU32 * (xn2 + cn1 * cn1);
+                const float e2 = kappa * xn * cmax + 8.0f * kU32 * (xn2 + cmax * cmax);
+                const float D1 = xn2 + b1, D2 = xn2 + b2;
+                const float U = D1 + e1;
+                const float L = D2 - e2;
+                certain = L > U;
+                flag = !certain;
+                if (certain) {
+                    old = S.labels[row];
+                    moved = old != j1;
+                    S.labels[row] = j1;
+                    if (S.strategy != LK_STRAT_LLOYD) {
+                        S.ub[row] = __fsqrt_ru(fmaxf(U, 0.f));
+                        S.lb[row * S.nlb] = isinf(L) ? INFINITY : __fsqrt_rd(fmaxf(L, 0.f));
+                    }
+                }
+            }
+            int64_t pos = warp_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED));
+            if (moved) S.moved[pos] = make_int2((int)row, old);
+            int64_t fpos = warp_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED));
+            if (flag) S.flagged[fpos] = (int)row;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(2 * BN));
+    }
+}
+
+// ---- prep kernels -----------------------------------------------------------
+
+// x_lo = x - trunc_tf32(x) (exact in fp32) and ||x||^2 (fp64, rounded to fp32).
+__global__ void k_split_points(DevState S) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < S.n; i += nwarps) {
+        double s = 0.0;
+        for (int z = lane; z < S.ldx; z += 32) {
+            float x = z < S.d ? S.X32[i * S.ldx + z] : 0.f;
+            float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+            S.Xlo[i * S.ldx + z] = x - hi;
+            double xv = S.X64 && z < S.d ? S.X64[i * S.d + z] : (double)x;
+            s = fma(xv, xv, s);
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(LK_FULL_MASK, s, o);
+        if (lane == 0) S.xn2[i] = (float)s;
+    }
+}
+
+// Gather worklist rows into the contiguous rescan buffers (hi = x, lo = split).
+__global__ void k_gather_rows(DevState S, const int32_t* rows, const int64_t* count) {
+    if (*S.done) return;
+    const int64_t m = *count;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < m; r += nwarps) {
+        const int64_t row = rows[r];
+        for (int z = lane * 4; z < S.ldx; z += 128) {
+            float4 h = *reinterpret_cast<const float4*>(S.X32 + row * S.ldx + z);
+            float4 l = *reinterpret_cast<const float4*>(S.Xlo + row * S.ldx + z);
+            *reinterpret_cast<float4*>(S.Xg_hi + r * S.ldx + z) = h;
+            *reinterpret_cast<float4*>(S.Xg_lo + r * S.ldx + z) = l;
+        }
+    }
+}
+
+}  // namespace tc
+}  // namespace lk
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps through the driver entry point (no -lcuda needed)
 
 namespace lkh {
 
-bool tc_supported(const lk::DevState&) { return false; }
+using namespace lk;
+using namespace lk::tc;
 
-lk_status launch_assign_tc(const lk::DevState&, const int32_t*, const int64_t*, int64_t*,
-                           int64_t, int, cudaStream_t) {
-    set_error("tcgen05 path not built");
-    return LK_ERR_UNSUPPORTED;
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled)p;
+    }
+    return fn;
+}
+
+static bool make_map(CUtensorMap* map, const float* base, int64_t rows, int cols, int ld,
+                     int box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)(rows > 0 ? rows : 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool tc_supported(const DevState& S) {
+    return S.Xlo != nullptr && S.d >= 8 && (S.ldx % 4) == 0 && get_encode() != nullptr;
+}
+
+lk_status launch_tc_prep_points(const DevState& S, int sms, cudaStream_t st) {
+    if (!S.Xlo) return LK_OK;
+    k_split_points<<<sms * 8, 256, 0, st>>>(S);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+template <int BN>
+static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo, int64_t a_rows,
+                           const int32_t* rowlist, const int64_t* rowcount, int64_t max_rows,
+                           int64_t* stat, int sms, cudaStream_t st) {
+    CUtensorMap mah, mal, mbh, mbl;
+    if (!make_map(&mah, ahi, a_rows, S.d, S.ldx, BM) || !make_map(&mal, alo, a_rows, S.d, S.ldx, BM) ||
+        !make_map(&mbh, S.Chi, S.k, S.d, S.ldc, BN) || !make_map(&mbl, S.Clo, S.k, S.d, S.ldc, BN)) {
+        set_error("cuTensorMapEncodeTiled failed");
+        return LK_ERR_CUDA;
+    }
+    TcArgs A;
+    A.m = max_rows;
+    A.rowlist = rowlist;
+    A.rowcount = rowcount;
+    A.n_ct = (S.k + BN - 1) / BN;
+    A.n_kc = (S.d + KC - 1) / KC;
+    const int smem = Smem<BN>::TOTAL;
+    static bool attr = false;
+    if (!attr) {
+        LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<BN>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    int64_t tiles = (max_rows + BM - 1) / BM;
+    int grid = (int)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
+    k_assign_tc<BN><<<grid, kThreadsTC, smem, st>>>(mah, mal, mbh, mbl, S, A, stat);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_assign_tc(const DevState& S, const int32_t* rowlist, const int64_t* rowcount,
+                           int64_t* stat, int64_t max_rows, int sms, cudaStream_t st) {
+    const float* ahi = S.X32;
+    const float* alo = S.Xlo;
+    int64_t a_rows = S.n;
+    const int32_t* map_rows = nullptr;
+    if (rowlist) {
+        // gather the worklist into contiguous rescan buffers first
+        k_gather_rows<<<sms * 8, 256, 0, st>>>(S, rowlist, rowcount);
+        LK_LAUNCH_CHECK();
+        ahi = S.Xg_hi;
+        alo = S.Xg_lo;
+        map_rows = rowlist;
+    }
+    if (S.k <= 128)
+        return launch_bn<128>(S, ahi, alo, a_rows, map_rows, rowcount, max_rows, stat, sms, st);
+    return launch_bn<256>(S, ahi, alo, a_rows, map_rows, rowcount, max_rows, stat, sms, st);
 }
 
 }  // namespace lkh
