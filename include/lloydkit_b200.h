@@ -112,9 +112,10 @@ enum {
     LK_STAT_WORK = 3,      /* rows rescanned against all / some centroids */
     LK_STAT_DIST = 4,      /* point-centroid distances evaluated (dist_comps) */
     LK_STAT_BOUND_UPD = 5, /* bound values rewritten (bound_updates) */
-    LK_STAT_GROUPS = 6,    /* group scans performed (Yinyang) */
+    LK_STAT_CANDIDATE = 6, /* rows re-decided in fp64 over <= 3 certified candidates */
     LK_STAT_CHANGED_GLOBAL = 7, /* changed summed over all ranks (stop rule) */
-    LK_NSTAT = 8
+    LK_STAT_OVERFLOW = 8,  /* ambiguous rows with > LK_MAX_CAND candidates (fp32 rescan) */
+    LK_NSTAT = 16
 };
 
 int32_t lk_version(void);

@@ -37,7 +37,7 @@ enum InternalBuf {
     // internal
     B_C64_PREV, B_C32, B_CNORM, B_DRIFT, B_SHALF, B_GDRIFT, B_SCAL, B_MOVED, B_FLAGGED, B_WORK,
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
-    B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO,
+    B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_COUNT_
 };
 
@@ -114,10 +114,15 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_CHI] = (uint64_t)kpad * L->ldc * 4;
         L->size[B_CLO] = (uint64_t)kpad * L->ldc * 4;
         L->size[B_CN2] = (uint64_t)kpad * 4;
-        if (c.strategy != LK_STRAT_LLOYD) {
-            L->size[B_XG_HI] = (uint64_t)n * L->ldx * 4;
-            L->size[B_XG_LO] = (uint64_t)n * L->ldx * 4;
-        }
+        L->size[B_CAND_ROWS] = (uint64_t)n * 4;
+        L->size[B_CAND_THR] = (uint64_t)n * 4;
+        L->size[B_CAND_LB] = (uint64_t)n * 4;
+        L->size[B_CAND_SLOTS] = (uint64_t)n * 4 * LK_MAX_CAND;
+        L->size[B_CAND_CNT] = (uint64_t)n * 4;
+        L->size[B_OVF] = (uint64_t)n * 4;
+        L->size[B_XG_HI] = (uint64_t)n * L->ldx * 4;
+        L->size[B_XG_LO] = (uint64_t)n * L->ldx * 4;
+
     }
     uint64_t off = 0;
     for (int b = 0; b < B_COUNT_; b++) {
@@ -304,6 +309,12 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.cn2 = buf<float>(c, B_CN2);
     S.Xg_hi = buf<float>(c, B_XG_HI);
     S.Xg_lo = buf<float>(c, B_XG_LO);
+    S.cand_rows = buf<int32_t>(c, B_CAND_ROWS);
+    S.cand_thr = buf<float>(c, B_CAND_THR);
+    S.cand_lb = buf<float>(c, B_CAND_LB);
+    S.cand_slots = buf<int32_t>(c, B_CAND_SLOTS);
+    S.cand_cnt = buf<int32_t>(c, B_CAND_CNT);
+    S.ovf = buf<int32_t>(c, B_OVF);
 
     std::vector<int32_t> prog;
     build_pw(0, cfg->d, prog);
@@ -492,6 +503,15 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
         }
         {
             ProfScope p(c, 2, st);
+            if (use_tc) {
+                s = lkh::launch_collect_tc(S, stat, n, c->sms, st);
+                if (s != LK_OK) return s;
+                s = lkh::launch_recheck_cand(S, stat, n, c->sms, st);
+                if (s != LK_OK) return s;
+                s = lkh::launch_assign_simt(S, S.ovf, stat + LK_STAT_OVERFLOW, stat, n, c->sms, st);
+                if (s != LK_OK) return s;
+                c->launches += 4;
+            }
             s = lkh::launch_recheck(S, stat, n, c->sms, st);
             if (s != LK_OK) return s;
         }

@@ -8,6 +8,7 @@
 #include "../../include/lloydkit_b200.h"
 
 #define LK_FULL_MASK 0xffffffffu
+#define LK_MAX_CAND 16
 
 namespace lk {
 
@@ -59,6 +60,12 @@ struct DevState {
     float* cn2;             // [k_pad] ||c||^2, +inf beyond k
     float* Xg_hi;           // [n, ldx] gathered rescan rows
     float* Xg_lo;           // [n, ldx]
+    int32_t* cand_rows;     // [n] ambiguous rows of the tensor-core pass
+    float* cand_thr;        // [n] D' threshold containing every possible winner
+    float* cand_lb;         // [n] certified lower bound on every non-candidate distance
+    int32_t* cand_slots;    // [n, LK_MAX_CAND] collected candidates
+    int32_t* cand_cnt;      // [n] candidates found (> LK_MAX_CAND: overflow)
+    int32_t* ovf;           // [n] overflow rows (fp32 difference-form rescan)
 };
 
 __device__ __forceinline__ float tf32_trunc(float x) {

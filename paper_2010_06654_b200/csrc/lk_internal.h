@@ -11,6 +11,8 @@ lk_status launch_assign_simt(const lk::DevState& S, const int32_t* rowlist,
                              cudaStream_t st);
 lk_status launch_recheck(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
                          cudaStream_t st);
+lk_status launch_recheck_cand(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
+                              cudaStream_t st);
 lk_status launch_filter_hamerly(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_refine(const lk::DevState& S, int64_t* stat, const double* qscale,
                         int64_t max_rows, int sms, cudaStream_t st);
@@ -21,6 +23,8 @@ lk_status launch_scan_exp(const lk::DevState& S, int sms, cudaStream_t st);
 // tcgen05 path (lk_tc.cu): full-scan assignment with 3xTF32 products.
 bool tc_supported(const lk::DevState& S);
 lk_status launch_tc_prep_points(const lk::DevState& S, int sms, cudaStream_t st);
+lk_status launch_collect_tc(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
+                            cudaStream_t st);
 lk_status launch_assign_tc(const lk::DevState& S, const int32_t* rowlist,
                            const int64_t* rowcount, int64_t* stat, int64_t max_rows, int sms,
                            cudaStream_t st);

@@ -235,11 +235,12 @@ constexpr int kRcWarps = 4;
 // Sum of (x_z - c_z)^2 over [start, start+len) exactly as numpy's pairwise_sum
 // leaf does it: sequential from 0 below 8 terms, else 8 strided accumulators
 // combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail in order.
-__device__ __forceinline__ double pw_leaf(const double* x, const double* c, int start, int len) {
+template <typename TX>
+__device__ __forceinline__ double pw_leaf(const TX* x, const double* c, int start, int len) {
     if (len < 8) {
         double res = 0.0;
         for (int z = start; z < start + len; z++) {
-            double t = __dsub_rn(x[z], c[z]);
+            double t = __dsub_rn((double)x[z], c[z]);
             res = __dadd_rn(res, __dmul_rn(t, t));
         }
         return res;
@@ -247,7 +248,7 @@ __device__ __forceinline__ double pw_leaf(const double* x, const double* c, int 
     double r[8];
 #pragma unroll
     for (int j = 0; j < 8; j++) {
-        double t = __dsub_rn(x[start + j], c[start + j]);
+        double t = __dsub_rn((double)x[start + j], c[start + j]);
         r[j] = __dmul_rn(t, t);
     }
     int i = 8;
@@ -255,20 +256,21 @@ __device__ __forceinline__ double pw_leaf(const double* x, const double* c, int 
     for (; i < main_end; i += 8) {
 #pragma unroll
         for (int j = 0; j < 8; j++) {
-            double t = __dsub_rn(x[start + i + j], c[start + i + j]);
+            double t = __dsub_rn((double)x[start + i + j], c[start + i + j]);
             r[j] = __dadd_rn(r[j], __dmul_rn(t, t));
         }
     }
     double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
     for (; i < len; i++) {
-        double t = __dsub_rn(x[start + i], c[start + i]);
+        double t = __dsub_rn((double)x[start + i], c[start + i]);
         res = __dadd_rn(res, __dmul_rn(t, t));
     }
     return res;
 }
 
-__device__ double pw_dist2(const double* x, const double* c, const int32_t* prog, int plen) {
+template <typename TX>
+__device__ double pw_dist2(const TX* x, const double* c, const int32_t* prog, int plen) {
     if (plen == 3) return pw_leaf(x, c, __ldg(prog + 1), __ldg(prog + 2));
     double st[24];
     int sp = 0;
@@ -334,6 +336,63 @@ __global__ void __launch_bounds__(kRcWarps * 32) k_recheck_fp64(DevState S, int6
                 S.moved[p] = make_int2((int)row, old);
             }
         }
+    }
+}
+
+// K1c: exact fp64 re-decision of the tensor-core pass's ambiguous rows over
+// their collected candidates.  Every centroid outside the candidate set is
+// provably strictly farther than the best candidate's upper bound, so the
+// oracle's argmin lies in the set; the candidates' distances are computed
+// exactly as the oracle computes them (numpy order, fp64), ties to the lowest
+// index.  Rows whose set overflowed LK_MAX_CAND go to the fp32
+// difference-form rescan (tight error bound), and from there to fp64 if needed.
+__global__ void __launch_bounds__(kThreads) k_recheck_cand(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    __shared__ unsigned long long scr[kThreads / 32 + 1];
+    const int64_t m = stat[LK_STAT_CANDIDATE];
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < m;
+         base += (int64_t)gridDim.x * kThreads) {
+        const int64_t e = base + threadIdx.x;
+        bool mv = false, over = false;
+        int64_t row = 0;
+        int old = 0;
+        if (e < m) {
+            row = S.cand_rows[e];
+            const int cnt = S.cand_cnt[e];
+            if (cnt < 1 || cnt > LK_MAX_CAND) {
+                over = true;
+            } else {
+                double b1 = INFINITY, b2 = INFINITY;
+                int j1 = 0x7fffffff;
+                const int* sl = S.cand_slots + e * LK_MAX_CAND;
+                for (int i = 0; i < cnt; i++) {
+                    const int j = sl[i];
+                    const double* cp = S.C64 + (int64_t)j * S.d;
+                    double dd = S.X64 ? pw_dist2(S.X64 + row * S.d, cp, S.pw_prog, S.pw_len)
+                                      : pw_dist2(S.X32 + row * S.ldx, cp, S.pw_prog, S.pw_len);
+                    dd = __dsqrt_rn(dd);
+                    if (dd < b1 || (dd == b1 && j < j1)) {
+                        b2 = b1;
+                        b1 = dd;
+                        j1 = j;
+                    } else {
+                        b2 = fmin(b2, dd);
+                    }
+                }
+                old = S.labels[row];
+                mv = old != j1;
+                S.labels[row] = j1;
+                if (S.strategy != LK_STRAT_LLOYD) {
+                    S.ub[row] = __double2float_ru(b1 * (1.0 + 1e-12));
+                    const float l2 = isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12));
+                    S.lb[row * S.nlb] = fminf(l2, S.cand_lb[e]);
+                }
+            }
+        }
+        int64_t pos = block_append(mv, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
+        if (mv) S.moved[pos] = make_int2((int)row, old);
+        int64_t fpos = block_append(over, (unsigned long long*)(stat + LK_STAT_OVERFLOW), scr);
+        if (over) S.ovf[fpos] = (int)row;
     }
 }
 
@@ -720,6 +779,14 @@ lk_status launch_recheck(const DevState& S, int64_t* stat, int64_t max_rows, int
     }
     int grid = grid_for(max_rows, kRcWarps, sms * 8);
     k_recheck_fp64<<<grid, kRcWarps * 32, smem, st>>>(S, stat);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_recheck_cand(const DevState& S, int64_t* stat, int64_t max_rows, int sms,
+                              cudaStream_t st) {
+    int grid = grid_for(max_rows, kThreads, sms * 4);
+    k_recheck_cand<<<grid, kThreads, 0, st>>>(S, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }

@@ -32,6 +32,7 @@ constexpr int BM = 128;        // rows per tile (UMMA M)
 constexpr int KC = 32;         // fp32 elements per K chunk (128 bytes)
 constexpr int UK = 8;          // UMMA K for kind::tf32
 constexpr int kEpiWarps = 4;
+constexpr int kMaxCand = LK_MAX_CAND;
 constexpr int kThreadsTC = 64 + 32 * kEpiWarps;
 
 template <int BN>
@@ -156,6 +157,27 @@ __device__ __forceinline__ float tc_kappa(int d) {
     return 2.0f * (3.1f * 9.5367431640625e-07f + (float)(3 * d + 1) * 2.384185791015625e-07f * 1.01f);
 }
 
+// Aggregated append over the kEpiWarps epilogue warps (named barrier 1).
+__device__ __forceinline__ int64_t epi_append(bool pred, unsigned long long* counter,
+                                              unsigned long long* scr, int ew) {
+    unsigned msk = __ballot_sync(LK_FULL_MASK, pred);
+    if (lane_id() == 0) scr[ew] = __popc(msk);
+    asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
+    if (ew == 0 && lane_id() == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < kEpiWarps; w++) {
+            unsigned long long c = scr[w];
+            scr[w] = tot;
+            tot += c;
+        }
+        scr[kEpiWarps] = tot ? atomicAdd(counter, tot) : 0ull;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
+    int64_t pos = pred ? (int64_t)(scr[kEpiWarps] + scr[ew] + __popc(msk & lanemask_lt())) : -1;
+    asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
+    return pos;
+}
+
 // ---- the kernel --------------------------------------------------------------
 
 struct TcArgs {
@@ -164,9 +186,16 @@ struct TcArgs {
     const int64_t* rowcount;  // device row count (overrides m when non-null)
     int n_ct;             // centroid tiles
     int n_kc;             // K chunks
+    // collect mode
+    const float* thr;     // [m] D' threshold per A row
+    int* slots;           // [m, kMaxCand]
+    int* cnt;             // [m]
 };
 
-template <int BN>
+constexpr int kTop2 = 0;
+constexpr int kCollect = 1;
+
+template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     k_assign_tc(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -277,9 +306,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const float kappa = tc_kappa(S.d);
         int acc = 0;
         uint32_t acc_phase = 0;
+        __shared__ unsigned long long escr[kEpiWarps + 1];
         for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x) {
+            const int64_t r = rt * BM + row_in_tile;
+            const bool valid = r < m;
+            // MODE_TOP2: running top-2 of D' = |c|^2 - 2 x.c (ties keep the lower index)
+            // MODE_COLLECT: every j with D' <= thr goes into the row's candidate slots
             float b1 = INFINITY, b2 = INFINITY;
             int j1 = 0;
+            float thr = -INFINITY;
+            int cnt = 0;
+            int* slots = nullptr;
+            if (MODE == kCollect && valid) {
+                thr = A.thr[r];
+                slots = A.slots + r * kMaxCand;
+            }
             for (int ct = 0; ct < A.n_ct; ct++) {
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
@@ -299,8 +340,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
                         for (int e = 0; e < 4; e++) {
                             const float dp = fmaf(-2.0f, v[c4 * 4 + e], cc[e]);
-                            if (dp < b1) { b2 = b1; b1 = dp; j1 = jb + c4 * 4 + e; }
-                            else b2 = fminf(b2, dp);
+                            if (MODE == kTop2) {
+                                if (dp < b1) { b2 = b1; b1 = dp; j1 = jb + c4 * 4 + e; }
+                                else b2 = fminf(b2, dp);
+                            } else {
+                                if (valid && dp <= thr) {
+                                    if (cnt < kMaxCand) slots[cnt] = jb + c4 * 4 + e;
+                                    cnt++;
+                                }
+                            }
                         }
                     }
                 }
@@ -309,12 +357,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 if (lane == 0) mbar_arrive(&tempty[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
-            // certify this row
-            const int64_t r = rt * BM + row_in_tile;
-            const bool valid = r < m;
+            if (MODE == kCollect) {
+                if (valid) A.cnt[r] = cnt;
+                continue;
+            }
+            // certify this row; ambiguous rows get a candidate threshold
             int64_t row = 0;
-            bool certain = false, flag = false, moved = false;
+            bool moved = false, amb = false;
             int old = 0;
+            float thr_out = 0.f, lb_out = 0.f;
             if (valid) {
                 row = A.rowlist ? (int64_t)A.rowlist[r] : r;
                 const float xn2 = S.xn2[row];
@@ -322,26 +373,33 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 const float cn1 = S.cnorm[j1];
                 const float cmax = S.scal[0];
                 const float e1 = kappa * xn * cn1 + 8.0f * kU32 * (xn2 + cn1 * cn1);
-                const float e2 = kappa * xn * cmax + 8.0f * kU32 * (xn2 + cmax * cmax);
-                const float D1 = xn2 + b1, D2 = xn2 + b2;
-                const float U = D1 + e1;
-                const float L = D2 - e2;
-                certain = L > U;
-                flag = !certain;
-                if (certain) {
+                const float eo = kappa * xn * cmax + 8.0f * kU32 * (xn2 + cmax * cmax);
+                const float U = (xn2 + b1) + e1;
+                const float L2 = (xn2 + b2) - eo;
+                if (L2 > U) {
                     old = S.labels[row];
                     moved = old != j1;
                     S.labels[row] = j1;
                     if (S.strategy != LK_STRAT_LLOYD) {
                         S.ub[row] = __fsqrt_ru(fmaxf(U, 0.f));
-                        S.lb[row * S.nlb] = isinf(L) ? INFINITY : __fsqrt_rd(fmaxf(L, 0.f));
+                        S.lb[row * S.nlb] = isinf(L2) ? INFINITY : __fsqrt_rd(fmaxf(L2, 0.f));
                     }
+                } else {
+                    // any possible winner j has D'_j <= U - xn2 + e_j <= thr
+                    amb = true;
+                    thr_out = (b1 + e1 + eo) * (1.0f + 4 * kU32) + fabsf(b1) * 4 * kU32 + 1e-30f;
+                    lb_out = __fsqrt_rd(fmaxf(U, 0.f));
                 }
             }
-            int64_t pos = warp_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED));
+            // 128-thread aggregated appends across the epilogue warps (named barrier 1)
+            int64_t pos = epi_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED), escr, warp - 2);
             if (moved) S.moved[pos] = make_int2((int)row, old);
-            int64_t fpos = warp_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED));
-            if (flag) S.flagged[fpos] = (int)row;
+            int64_t cpos = epi_append(amb, (unsigned long long*)(stat + LK_STAT_CANDIDATE), escr, warp - 2);
+            if (amb) {
+                S.cand_rows[cpos] = (int)row;
+                S.cand_thr[cpos] = thr_out;
+                S.cand_lb[cpos] = lb_out;
+            }
         }
     }
     __syncthreads();
@@ -374,6 +432,7 @@ __global__ void k_split_points(DevState S) {
 
 // Gather worklist rows into the contiguous rescan buffers (hi = x, lo = split).
 __global__ void k_gather_rows(DevState S, const int32_t* rows, const int64_t* count) {
+    // rows: worklist of global row ids; count: device length
     if (*S.done) return;
     const int64_t m = *count;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -443,53 +502,67 @@ lk_status launch_tc_prep_points(const DevState& S, int sms, cudaStream_t st) {
     return LK_OK;
 }
 
-template <int BN>
+template <int BN, int MODE>
 static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo, int64_t a_rows,
-                           const int32_t* rowlist, const int64_t* rowcount, int64_t max_rows,
-                           int64_t* stat, int sms, cudaStream_t st) {
+                           TcArgs A, int64_t max_rows, int64_t* stat, int sms, cudaStream_t st) {
     CUtensorMap mah, mal, mbh, mbl;
     if (!make_map(&mah, ahi, a_rows, S.d, S.ldx, BM) || !make_map(&mal, alo, a_rows, S.d, S.ldx, BM) ||
         !make_map(&mbh, S.Chi, S.k, S.d, S.ldc, BN) || !make_map(&mbl, S.Clo, S.k, S.d, S.ldc, BN)) {
         set_error("cuTensorMapEncodeTiled failed");
         return LK_ERR_CUDA;
     }
-    TcArgs A;
     A.m = max_rows;
-    A.rowlist = rowlist;
-    A.rowcount = rowcount;
     A.n_ct = (S.k + BN - 1) / BN;
     A.n_kc = (S.d + KC - 1) / KC;
     const int smem = Smem<BN>::TOTAL;
     static bool attr = false;
     if (!attr) {
-        LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<BN>,
+        LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<BN, MODE>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
     int64_t tiles = (max_rows + BM - 1) / BM;
     int grid = (int)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
-    k_assign_tc<BN><<<grid, kThreadsTC, smem, st>>>(mah, mal, mbh, mbl, S, A, stat);
+    k_assign_tc<BN, MODE><<<grid, kThreadsTC, smem, st>>>(mah, mal, mbh, mbl, S, A, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
 
+template <int MODE>
+static lk_status launch_mode(const DevState& S, const float* ahi, const float* alo, TcArgs A,
+                             int64_t max_rows, int64_t* stat, int sms, cudaStream_t st) {
+    if (S.k <= 128) return launch_bn<128, MODE>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
+    return launch_bn<256, MODE>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
+}
+
 lk_status launch_assign_tc(const DevState& S, const int32_t* rowlist, const int64_t* rowcount,
                            int64_t* stat, int64_t max_rows, int sms, cudaStream_t st) {
-    const float* ahi = S.X32;
-    const float* alo = S.Xlo;
-    int64_t a_rows = S.n;
-    const int32_t* map_rows = nullptr;
+    TcArgs A = {};
+    A.rowlist = rowlist;
+    A.rowcount = rowcount;
     if (rowlist) {
         // gather the worklist into contiguous rescan buffers first
         k_gather_rows<<<sms * 8, 256, 0, st>>>(S, rowlist, rowcount);
         LK_LAUNCH_CHECK();
-        ahi = S.Xg_hi;
-        alo = S.Xg_lo;
-        map_rows = rowlist;
+        return launch_mode<kTop2>(S, S.Xg_hi, S.Xg_lo, A, max_rows, stat, sms, st);
     }
-    if (S.k <= 128)
-        return launch_bn<128>(S, ahi, alo, a_rows, map_rows, rowcount, max_rows, stat, sms, st);
-    return launch_bn<256>(S, ahi, alo, a_rows, map_rows, rowcount, max_rows, stat, sms, st);
+    return launch_mode<kTop2>(S, S.X32, S.Xlo, A, max_rows, stat, sms, st);
+}
+
+// Second pass over the ambiguous rows: collect every centroid under the row's
+// certified threshold into cand_slots (count in cand_cnt; > LK_MAX_CAND =
+// overflow, decided by the full fp64 recheck).
+lk_status launch_collect_tc(const DevState& S, int64_t* stat, int64_t max_rows, int sms,
+                            cudaStream_t st) {
+    TcArgs A = {};
+    A.rowlist = S.cand_rows;
+    A.rowcount = stat + LK_STAT_CANDIDATE;
+    A.thr = S.cand_thr;
+    A.slots = S.cand_slots;
+    A.cnt = S.cand_cnt;
+    k_gather_rows<<<sms * 8, 256, 0, st>>>(S, S.cand_rows, stat + LK_STAT_CANDIDATE);
+    LK_LAUNCH_CHECK();
+    return launch_mode<kCollect>(S, S.Xg_hi, S.Xg_lo, A, max_rows, stat, sms, st);
 }
 
 }  // namespace lkh

@@ -33,6 +33,7 @@ def _torch():
 class IterRecord:
     changed: int
     flagged: int
+    candidate: int
     active: int
     work: int
     sse: float
@@ -255,6 +256,7 @@ class DeviceLloyd:
                 recs.append(IterRecord(
                     changed=int(stats[t, nat.STAT["changed_global"]]),
                     flagged=int(stats[t, nat.STAT["flagged"]]),
+                    candidate=int(stats[t, nat.STAT["candidate"]]),
                     active=int(stats[t, nat.STAT["active"]]),
                     work=int(stats[t, nat.STAT["work"]]),
                     sse=float(sse[t]),

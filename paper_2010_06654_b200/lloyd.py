@@ -128,6 +128,7 @@ def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: R
         init_centroids=init_copy,
         label=label,
         extra={"device": "cuda", "recheck_rows": [r.flagged for r in out["records"]],
+               "candidate_rows": [r.candidate for r in out["records"]],
                "rescanned_rows": [r.work for r in out["records"]]},
     )
 

@@ -185,3 +185,26 @@ def test_scaled_configs_match_oracle(oracle, name, n, k, t_max, strategy):
     check_trajectory(oracle, x, init, res.assign_history, ref["history"], f"{name} {strategy}")
     assert res.converged == ref["converged"]
     assert centroid_ok(res.centroids, ref["centroids"], x), name
+
+
+@pytest.mark.parametrize("name,n,k,d_strat", [("cfg3", 6000, 300, "lloyd"), ("cfg4", 3000, 256, "hamerly"),
+                                               ("cfg5", 20000, 1000, "hamerly")])
+def test_tensor_core_and_simt_paths_agree(oracle, name, n, k, d_strat):
+    """The tcgen05 3xTF32 path and the fp32 SIMT path certify labels
+    independently; both must land on the oracle's trajectory, bit-identically."""
+    from paper_2010_06654_b200 import datasets
+    x = datasets.generate(name, n)
+    m = lk()
+    init = m.make_init(m.RunContext(seed=3), x, k, "random")
+    runs = {}
+    for kern in ("simt", "tc"):
+        if d_strat == "lloyd":
+            runs[kern] = m.run_lloyd(x, k, init=init, t_max=6, kernel=kern)
+        else:
+            runs[kern] = m.run_pruner(x, k, d_strat, init=init, t_max=6, kernel=kern)
+    ref = oracle.run_lloyd(x, k, init, 6)
+    for kern, res in runs.items():
+        check_trajectory(oracle, x, init, res.assign_history, ref["history"], f"{name} {kern}")
+    assert np.array_equal(runs["simt"].centroids, runs["tc"].centroids)
+    # the TC path must actually certify most rows itself
+    assert sum(runs["tc"].extra["recheck_rows"]) < 0.05 * n * len(runs["tc"].iterations)
