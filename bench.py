@@ -164,6 +164,10 @@ def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kern
     if cls == 0:  # assignment: 2*d flops per (row, centroid) pair evaluated
         rows = sum(n if (strategy == "lloyd" or r["t"] == 1) else r["work"] for r in recs)
         return "flop", 2.0 * rows * k * d
+    if cls == 1 and strategy in ("yinyang", "elkan"):
+        # group filter: label/ub/lb-table traffic + tightened rows + group scans
+        t = r_groups = max(1, recs[0].get("groups", 1))
+        return "byte", sum(n * (12.0 + 8.0 * t) + 4.0 * d * r["active"] for r in recs)
     if cls == 1:  # Hamerly filter: label 4 + ub 4 + lb 4 read, ub 4 + lb 4 written,
         # 4 per appended row, + the tightened rows' point (4d)
         return "byte", sum(20.0 * n + 4.0 * r["work"] + 4.0 * d * r["active"] for r in recs)
@@ -202,9 +206,10 @@ def run_ours(args):
     x = x_full[r0:r1]
     n, d, k = cfg.n, cfg.d, cfg.k
     strategy = args.strategy
-    gpu_strat = "lloyd" if strategy == "lloyd" else "hamerly"
-
-    eng = DeviceLloyd(x, k, gpu_strat, T, kernel=args.kernel, comm=group, n_total=n)
+    gpu_strat = strategy
+    from paper_2010_06654_b200.pruners import gpu_groups
+    eng = DeviceLloyd(x, k, gpu_strat, T, kernel=args.kernel, comm=group, n_total=n,
+                      groups=gpu_groups(gpu_strat, n, k), group_seed=cfg.seed_init)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
@@ -384,7 +389,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
-    ap.add_argument("--strategy", default="hamerly", choices=["lloyd", "hamerly"])
+    ap.add_argument("--strategy", default="hamerly", choices=["lloyd", "hamerly", "yinyang", "elkan"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")

@@ -115,6 +115,8 @@ enum {
     LK_STAT_CANDIDATE = 6, /* rows re-decided in fp64 over <= 3 certified candidates */
     LK_STAT_CHANGED_GLOBAL = 7, /* changed summed over all ranks (stop rule) */
     LK_STAT_OVERFLOW = 8,  /* ambiguous rows with > LK_MAX_CAND candidates (fp32 rescan) */
+    LK_STAT_YWL = 9,       /* Yinyang rows that reached the per-group scan */
+    LK_STAT_PAIRS = 10,    /* Yinyang (row, group) scans */
     LK_NSTAT = 16
 };
 
@@ -143,6 +145,11 @@ lk_status lk_layout(const lk_ctx *ctx, int64_t *ldx, int64_t *delta_len, int32_t
 lk_status lk_scan_points(lk_ctx *ctx, void *stream);
 /* Freeze the fixed-point scales from LK_BUF_QEXP.  Must follow lk_scan_points. */
 lk_status lk_set_quant(lk_ctx *ctx, void *stream);
+
+/* Yinyang / Elkan / Regroup: centroid -> group map (host int32 [k], values in
+ * [0, groups)); the grouping only affects pruning power, never labels
+ * (bounds.py:175-196 group_centroids is one way to build it). */
+lk_status lk_set_groups(lk_ctx *ctx, const int32_t *group_of, void *stream);
 
 /* Initial centroids: fp64 [k, d] device array (copied into LK_BUF_C64).
  * Resets labels to -1 (lloyd.py:159), sums, counts and stats. */

@@ -25,13 +25,13 @@ BUF = {"x32": 0, "x64": 1, "c64": 2, "labels": 3, "ub": 4, "lb": 5, "delta": 6, 
        "sse": 8, "group_of": 9, "counts": 10, "qexp": 11}
 NSTAT = 16
 STAT = {"changed": 0, "flagged": 1, "active": 2, "work": 3, "dist": 4, "bound_upd": 5,
-        "candidate": 6, "changed_global": 7, "overflow": 8}
+        "candidate": 6, "changed_global": 7, "overflow": 8, "ywl": 9, "pairs": 10}
 
 # Every symbol the header declares (checked by tests/test_native_abi.py).
 EXPORTED = (
     "lk_version", "lk_last_error", "lk_workspace_bytes", "lk_ctx_create", "lk_ctx_destroy",
     "lk_buffer", "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
-    "lk_step_assign", "lk_step_update", "lk_launch_count", "lk_profile", "lk_profile_read",
+    "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_launch_count", "lk_profile", "lk_profile_read",
 )
 
 
@@ -87,6 +87,7 @@ def load():
     L.lk_scan_points.argtypes = [vp, vp]
     L.lk_set_quant.argtypes = [vp, vp]
     L.lk_set_centroids.argtypes = [vp, vp, vp]
+    L.lk_set_groups.argtypes = [vp, vp, vp]
     L.lk_step_assign.argtypes = [vp, i32, vp]
     L.lk_step_update.argtypes = [vp, i32, vp]
     L.lk_launch_count.argtypes = [vp]
@@ -95,7 +96,7 @@ def load():
     L.lk_profile_read.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
     for name in ("lk_workspace_bytes", "lk_ctx_create", "lk_ctx_destroy", "lk_buffer",
                  "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
-                 "lk_step_assign", "lk_step_update", "lk_profile", "lk_profile_read"):
+                 "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_profile", "lk_profile_read"):
         getattr(L, name).restype = i32
     _lib = L
     return L

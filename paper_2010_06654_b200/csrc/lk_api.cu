@@ -38,6 +38,7 @@ enum InternalBuf {
     B_C64_PREV, B_C32, B_CNORM, B_DRIFT, B_SHALF, B_GDRIFT, B_SCAL, B_MOVED, B_FLAGGED, B_WORK,
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
+    B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES,
     B_COUNT_
 };
 
@@ -45,9 +46,13 @@ struct Layout {
     uint64_t off[B_COUNT_];
     uint64_t size[B_COUNT_];
     uint64_t total;
-    int64_t ldx, ldc, delta_len;
+    int64_t ldx, ldc, delta_len, pair_cap;
     int32_t nlb, groups;
 };
+
+static bool is_group_strategy(int s) {
+    return s == LK_STRAT_YINYANG || s == LK_STRAT_ELKAN || s == LK_STRAT_REGROUP;
+}
 
 static uint64_t align256(uint64_t v) { return (v + 255) & ~uint64_t(255); }
 
@@ -56,7 +61,7 @@ static int32_t nlb_for(const lk_config& c, int32_t* groups) {
     switch (c.strategy) {
         case LK_STRAT_LLOYD: g = 0; break;
         case LK_STRAT_HAMERLY: g = 1; break;
-        case LK_STRAT_ELKAN: g = c.k; break;
+        case LK_STRAT_ELKAN: g = c.groups > 0 ? c.groups : c.k; break;
         default: g = c.groups > 0 ? c.groups : (c.k + 9) / 10; break;
     }
     if (g > c.k) g = c.k;
@@ -124,6 +129,17 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_XG_LO] = (uint64_t)n * L->ldx * 4;
 
     }
+    if (is_group_strategy(c.strategy)) {
+        int64_t cap = n * (int64_t)L->groups;
+        if (cap > (1LL << 27)) cap = 1LL << 27;
+        if (cap < 1) cap = 1;
+        L->pair_cap = cap;
+        L->size[B_GPERM] = (uint64_t)k * 4;
+        L->size[B_GOFF] = (uint64_t)(L->groups + 1) * 4;
+        L->size[B_YWL] = (uint64_t)n * 16;
+        L->size[B_YPAIRS] = (uint64_t)cap * 8;
+        L->size[B_YRES] = (uint64_t)cap * 16;
+    }
     uint64_t off = 0;
     for (int b = 0; b < B_COUNT_; b++) {
         L->off[b] = off;
@@ -161,6 +177,7 @@ struct lk_ctx {
     int sms;
     bool quant_set;
     bool centroids_set;
+    bool groups_set;
     int64_t launches;
     // profiling
     bool profile;
@@ -235,10 +252,6 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
         set_error("unknown strategy id %d", cfg->strategy);
         return LK_ERR_ARG;
     }
-    if (cfg->strategy != LK_STRAT_LLOYD && cfg->strategy != LK_STRAT_HAMERLY) {
-        set_error("strategy %d not available in this build", cfg->strategy);
-        return LK_ERR_UNSUPPORTED;
-    }
     Layout L;
     if (!make_layout(*cfg, &L)) {
         set_error("invalid configuration (n=%lld d=%d k=%d)", (long long)cfg->n_local, cfg->d,
@@ -257,6 +270,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     c->ws = reinterpret_cast<uint8_t*>(workspace);
     c->quant_set = false;
     c->centroids_set = false;
+    c->groups_set = !is_group_strategy(cfg->strategy);
     c->launches = 0;
     c->profile = false;
     int sms = 148;
@@ -315,6 +329,12 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.cand_slots = buf<int32_t>(c, B_CAND_SLOTS);
     S.cand_cnt = buf<int32_t>(c, B_CAND_CNT);
     S.ovf = buf<int32_t>(c, B_OVF);
+    S.gperm = buf<int32_t>(c, B_GPERM);
+    S.goff = buf<int32_t>(c, B_GOFF);
+    S.ywl = buf<int4>(c, B_YWL);
+    S.ypairs = buf<int2>(c, B_YPAIRS);
+    S.yres = buf<float4>(c, B_YRES);
+    S.pair_cap = L.pair_cap;
 
     std::vector<int32_t> prog;
     build_pw(0, cfg->d, prog);
@@ -442,6 +462,33 @@ static __global__ void k_init_centroids(lk::DevState S, int kpad) {
     }
 }
 
+lk_status lk_set_groups(lk_ctx* c, const int32_t* group_of, void* stream) {
+    if (!c || !group_of) return LK_ERR_ARG;
+    if (!is_group_strategy(c->cfg.strategy)) {
+        set_error("lk_set_groups: strategy %d keeps no group bounds", c->cfg.strategy);
+        return LK_ERR_STATE;
+    }
+    const int k = c->cfg.k, t = c->L.groups;
+    std::vector<int32_t> cnt(t + 1, 0), perm(k), off(t + 1, 0);
+    for (int j = 0; j < k; j++) {
+        if (group_of[j] < 0 || group_of[j] >= t) {
+            set_error("group_of[%d] = %d outside [0, %d)", j, group_of[j], t);
+            return LK_ERR_ARG;
+        }
+        cnt[group_of[j]]++;
+    }
+    for (int g = 0; g < t; g++) off[g + 1] = off[g] + cnt[g];
+    std::vector<int32_t> fill(off.begin(), off.end());
+    for (int j = 0; j < k; j++) perm[fill[group_of[j]]++] = j;  // ascending j within a group
+    cudaStream_t st = (cudaStream_t)stream;
+    LK_CUDA_CHECK(cudaMemcpyAsync(c->S.group_of, group_of, k * 4, cudaMemcpyHostToDevice, st));
+    LK_CUDA_CHECK(cudaMemcpyAsync(c->S.gperm, perm.data(), k * 4, cudaMemcpyHostToDevice, st));
+    LK_CUDA_CHECK(cudaMemcpyAsync(c->S.goff, off.data(), (t + 1) * 4, cudaMemcpyHostToDevice, st));
+    LK_CUDA_CHECK(cudaStreamSynchronize(st));
+    c->groups_set = true;
+    return LK_OK;
+}
+
 lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     if (!c || !c64) return LK_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
@@ -467,8 +514,8 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
 
 lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
     if (!c) return LK_ERR_ARG;
-    if (!c->quant_set || !c->centroids_set) {
-        set_error("lk_step_assign before lk_set_quant / lk_set_centroids");
+    if (!c->quant_set || !c->centroids_set || !c->groups_set) {
+        set_error("lk_step_assign before lk_set_quant / lk_set_centroids / lk_set_groups");
         return LK_ERR_STATE;
     }
     if (t < 1 || t > c->cfg.t_max) {
@@ -489,6 +536,18 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
                        : lkh::launch_assign_simt(S, nullptr, nullptr, stat, n, c->sms, st);
             if (s != LK_OK) return s;
             c->launches += 1;
+        } else if (is_group_strategy(c->cfg.strategy)) {
+            {
+                ProfScope p(c, 1, st);
+                s = lkh::launch_yinyang(S, stat, c->sms, st);
+                if (s != LK_OK) return s;
+            }
+            ProfScope p(c, 0, st);
+            // rows that did not fit the pair capacity: full rescan
+            s = use_tc ? lkh::launch_assign_tc(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st)
+                       : lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
+            if (s != LK_OK) return s;
+            c->launches += 4;
         } else {
             {
                 ProfScope p(c, 1, st);
@@ -533,7 +592,7 @@ lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
     }
     cudaStream_t st = (cudaStream_t)stream;
     ProfScope p(c, 4, st);
-    bool need_half = c->cfg.strategy == LK_STRAT_HAMERLY;
+    const bool need_half = c->cfg.strategy == LK_STRAT_HAMERLY;
     lk_status s = lkh::launch_update(c->S, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV),
                                      buf<double>(c, B_SSE_PART), t, need_half, st);
     c->launches += need_half ? 4 : 2;

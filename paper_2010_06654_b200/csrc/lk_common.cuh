@@ -66,7 +66,21 @@ struct DevState {
     int32_t* cand_slots;    // [n, LK_MAX_CAND] collected candidates
     int32_t* cand_cnt;      // [n] candidates found (> LK_MAX_CAND: overflow)
     int32_t* ovf;           // [n] overflow rows (fp32 difference-form rescan)
+    // Yinyang group bounds
+    int32_t* gperm;         // [k] centroid ids sorted by group
+    int32_t* goff;          // [t + 1] group ranges in gperm
+    int4* ywl;              // [n] worklist: (row, pair offset, pair count, bits of D~_a)
+    int2* ypairs;           // [pair_cap] (worklist index, group)
+    float4* yres;           // [pair_cap] (bits of best j, best D~, second D~, -)
+    int64_t pair_cap;
 };
+
+// Finalize a row's lower bounds from one certified bound on every non-winning
+// centroid (Hamerly: the single slot; Yinyang: every group slot).
+__device__ __forceinline__ void write_lb_all(const DevState& S, int64_t row, float v) {
+    float* p = S.lb + row * S.nlb;
+    for (int g = 0; g < S.nlb; g++) p[g] = v;
+}
 
 __device__ __forceinline__ float tf32_trunc(float x) {
     return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);

@@ -20,6 +20,8 @@ lk_status launch_update(const lk::DevState& S, const double* qscale, const doubl
                         double* sse_part, int t, bool need_half, cudaStream_t st);
 lk_status launch_scan_exp(const lk::DevState& S, int sms, cudaStream_t st);
 
+lk_status launch_yinyang(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
+
 // tcgen05 path (lk_tc.cu): full-scan assignment with 3xTF32 products.
 bool tc_supported(const lk::DevState& S);
 lk_status launch_tc_prep_points(const lk::DevState& S, int sms, cudaStream_t st);

@@ -43,7 +43,7 @@ __device__ __forceinline__ void row_finish(const DevState& S, bool valid, int64_
         S.labels[row] = j1;
         if (S.strategy != LK_STRAT_LLOYD) {
             S.ub[row] = U1;
-            S.lb[row * S.nlb] = fmaxf(L2, 0.0f);
+            write_lb_all(S, row, fmaxf(L2, 0.0f));
         }
     }
     __shared__ unsigned long long scr[kThreads / 32 + 1];
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kRcWarps * 32) k_recheck_fp64(DevState S, int6
             S.labels[row] = j1;
             if (S.strategy != LK_STRAT_LLOYD) {
                 S.ub[row] = __double2float_ru(b1 * (1.0 + 1e-12));
-                S.lb[row * S.nlb] = isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12));
+                write_lb_all(S, row, isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12)));
             }
             if (mv) {
                 unsigned long long p =
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreads) k_recheck_cand(DevState S, int64_t* 
                 if (S.strategy != LK_STRAT_LLOYD) {
                     S.ub[row] = __double2float_ru(b1 * (1.0 + 1e-12));
                     const float l2 = isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12));
-                    S.lb[row * S.nlb] = fminf(l2, S.cand_lb[e]);
+                    write_lb_all(S, row, fminf(l2, S.cand_lb[e]));
                 }
             }
         }

@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     S.labels[row] = j1;
                     if (S.strategy != LK_STRAT_LLOYD) {
                         S.ub[row] = __fsqrt_ru(fmaxf(U, 0.f));
-                        S.lb[row * S.nlb] = isinf(L2) ? INFINITY : __fsqrt_rd(fmaxf(L2, 0.f));
+                        write_lb_all(S, row, isinf(L2) ? INFINITY : __fsqrt_rd(fmaxf(L2, 0.f)));
                     }
                 } else {
                     // any possible winner j has D'_j <= U - xn2 + e_j <= thr

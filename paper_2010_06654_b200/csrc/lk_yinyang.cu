@@ -1,0 +1,284 @@
+// lk_yinyang.cu -- group-bound (Yinyang) pruning on the GPU.
+//
+// Reference: Yinyang.update_bounds / assign_pass (pruners.py:418-497),
+// group_centroids (bounds.py:175-196).  Per point: label a, upper bound ub,
+// and one lower bound per centroid group (lb[n, t]).  Labels never depend on
+// the grouping, so t and the groups are chosen for bandwidth.
+//
+// Work-efficient mapping: instead of one thread walking a point's failing
+// groups (warp-divergent: the warp would execute the union of its lanes'
+// groups), the filter emits a flattened list of (point, group) pairs; one
+// thread scans one group for one point; a per-point merge certifies the new
+// label and rewrites the group bounds.
+//
+//   k_filter_yinyang  decay ub / every group bound, global gate, tighten,
+//                     per-group gate, append worklist rows + (row, group) pairs
+//   k_yy_pairs        fp32 difference-form distances to one group's members
+//   k_yy_merge        certified label, new group bounds, old-group fix-up;
+//                     ambiguous rows -> exact fp64 recheck, pair-capacity
+//                     overflow -> full SIMT rescan
+#include <math.h>
+
+#include "lk_common.cuh"
+#include "lk_internal.h"
+
+namespace lk {
+namespace yy {
+
+constexpr int kThreads = 256;
+
+// Block-wide exclusive scan of cnt with one global atomic per block.
+// Block-uniform call; scratch >= blockDim/32 + 1 entries.
+__device__ __forceinline__ int64_t block_reserve(int cnt, unsigned long long* counter,
+                                                 unsigned long long* scratch) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(LK_FULL_MASK, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) scratch[warp] = (unsigned long long)incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < nw; w++) {
+            unsigned long long c = scratch[w];
+            scratch[w] = tot;
+            tot += c;
+        }
+        scratch[nw] = tot ? atomicAdd(counter, tot) : 0ull;
+    }
+    __syncthreads();
+    int64_t off = (int64_t)(scratch[nw] + scratch[warp]) + (incl - cnt);
+    __syncthreads();
+    return off;
+}
+
+__device__ __forceinline__ float dist2_row(const DevState& S, const float* xp, int j) {
+    const float* cp = S.C32 + (int64_t)j * S.ldc;
+    float acc = 0.f;
+    int z = 0;
+    if ((S.ldx & 3) == 0) {
+        for (; z + 4 <= S.d; z += 4) {
+            float4 xv = *reinterpret_cast<const float4*>(xp + z);
+            float4 cv = __ldg(reinterpret_cast<const float4*>(cp + z));
+            float t0 = xv.x - cv.x, t1 = xv.y - cv.y, t2 = xv.z - cv.z, t3 = xv.w - cv.w;
+            acc = fmaf(t0, t0, acc);
+            acc = fmaf(t1, t1, acc);
+            acc = fmaf(t2, t2, acc);
+            acc = fmaf(t3, t3, acc);
+        }
+    }
+    for (; z < S.d; z++) {
+        float t = __ldg(xp + z) - __ldg(cp + z);
+        acc = fmaf(t, t, acc);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ float xnorm(const DevState& S, const float* xp) {
+    float s = 0.f;
+    for (int z = 0; z < S.d; z++) {
+        float v = __ldg(xp + z);
+        s = fmaf(v, v, s);
+    }
+    return sqrtf(s);
+}
+
+__global__ void __launch_bounds__(kThreads) k_filter_yinyang(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    extern __shared__ float gd[];  // [t] group drifts
+    __shared__ unsigned long long scr[kThreads / 32 + 1];
+    const int t = S.t_groups;
+    for (int g = threadIdx.x; g < t; g += kThreads) gd[g] = S.gdrift[g];
+    __syncthreads();
+    const float rho = simt_rel_err(S.d);
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < S.n;
+         base += (int64_t)gridDim.x * kThreads) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < S.n;
+        bool active = false, need = false;
+        int cnt = 0;
+        float acc_a = 0.f, u = 0.f;
+        float* lbr = S.lb + i * t;
+        if (valid) {
+            const int a = S.labels[i];
+            u = __fadd_ru(S.ub[i], S.drift[a]);
+            float gmin = INFINITY;
+            for (int g = 0; g < t; g++) {
+                float v = fmaxf(__fsub_rd(lbr[g], gd[g]), 0.f);
+                lbr[g] = v;
+                gmin = fminf(gmin, v);
+            }
+            if (!(gmin > u)) {
+                active = true;
+                const float* xp = S.X32 + i * S.ldx;
+                acc_a = dist2_row(S, xp, a);
+                const float U = (sqrtf(acc_a) + kU32 * (xnorm(S, xp) + S.cnorm[a])) * (1.0f + rho);
+                u = fminf(u, U);
+                need = !(gmin > u);
+            }
+            S.ub[i] = u;
+            if (need)
+                for (int g = 0; g < t; g++) cnt += !(lbr[g] > u);
+        }
+        block_count(active, stat + LK_STAT_ACTIVE, scr);
+        const int64_t wpos = block_append(need, (unsigned long long*)(stat + LK_STAT_YWL), scr);
+        const int64_t poff = block_reserve(need ? cnt : 0, (unsigned long long*)(stat + LK_STAT_PAIRS), scr);
+        if (need) {
+            if (poff + cnt <= S.pair_cap) {
+                S.ywl[wpos] = make_int4((int)i, (int)poff, cnt, __float_as_int(acc_a));
+                int p = 0;
+                for (int g = 0; g < t; g++)
+                    if (!(lbr[g] > u)) S.ypairs[poff + p++] = make_int2((int)wpos, g);
+            } else {
+                // over capacity: full rescan instead; neutralise any reserved slots
+                S.ywl[wpos] = make_int4((int)i, -1, 0, __float_as_int(acc_a));
+                for (int64_t q = poff; q < S.pair_cap && q < poff + cnt; q++)
+                    S.ypairs[q] = make_int2((int)wpos, -1);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_yy_pairs(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    const int64_t np_ = min((int64_t)stat[LK_STAT_PAIRS], S.pair_cap);
+    int64_t ndist = 0;
+    for (int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x; p < np_;
+         p += (int64_t)gridDim.x * kThreads) {
+        const int2 pr = S.ypairs[p];
+        if (pr.y < 0) continue;
+        const int4 w = S.ywl[pr.x];
+        const int64_t row = w.x;
+        const int a = S.labels[row];
+        const float* xp = S.X32 + row * S.ldx;
+        float b1 = INFINITY, b2 = INFINITY;
+        int j1 = -1;
+        const int j0 = S.goff[pr.y], j9 = S.goff[pr.y + 1];
+        for (int jj = j0; jj < j9; jj++) {
+            const int j = S.gperm[jj];
+            if (j == a) continue;  // the assigned centroid competes via the tightened bound
+            const float D = dist2_row(S, xp, j);
+            if (D < b1) { b2 = b1; b1 = D; j1 = j; }
+            else b2 = fminf(b2, D);
+        }
+        ndist += j9 - j0;
+        S.yres[p] = make_float4(__int_as_float(j1), b1, b2, 0.f);
+    }
+    warp_add(ndist, stat + LK_STAT_DIST);
+}
+
+__global__ void __launch_bounds__(kThreads) k_yy_merge(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    __shared__ unsigned long long scr[kThreads / 32 + 1];
+    const int64_t m = stat[LK_STAT_YWL];
+    const int t = S.t_groups;
+    const float rho = simt_rel_err(S.d);
+    const float cmax = S.scal[0];
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < m;
+         base += (int64_t)gridDim.x * kThreads) {
+        const int64_t e = base + threadIdx.x;
+        bool mv = false, flag = false, full = false;
+        int64_t row = 0;
+        int old = 0;
+        if (e < m) {
+            const int4 w = S.ywl[e];
+            row = w.x;
+            old = S.labels[row];
+            if (w.y < 0) {
+                full = true;
+            } else {
+                const float* xp = S.X32 + row * S.ldx;
+                const float xn = xnorm(S, xp);
+                const float acc_a = __int_as_float(w.w);
+                float bestD = acc_a, secD = INFINITY;
+                int bestJ = old;
+                for (int p = w.y; p < w.y + w.z; p++) {
+                    const float4 r = S.yres[p];
+                    const int pj = __float_as_int(r.x);
+                    if (pj < 0) continue;  // group had no member other than the label
+                    if (r.y < bestD || (r.y == bestD && pj < bestJ)) {
+                        secD = fminf(secD, bestD);
+                        bestD = r.y;
+                        bestJ = pj;
+                    } else {
+                        secD = fminf(secD, r.y);
+                    }
+                    secD = fminf(secD, r.z);
+                }
+                float* lbr = S.lb + row * t;
+                // lower bound over unscanned groups (pairs are in ascending group order)
+                float lun = INFINITY;
+                int p = w.y;
+                for (int g = 0; g < t; g++) {
+                    if (p < w.y + w.z && S.ypairs[p].y == g) { p++; continue; }
+                    lun = fminf(lun, lbr[g]);
+                }
+                const float U1 = (sqrtf(bestD) + kU32 * (xn + S.cnorm[bestJ])) * (1.0f + rho);
+                const float Ls = isinf(secD) ? INFINITY
+                                             : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
+                const float L2 = fminf(Ls, lun);
+                if (L2 > U1) {
+                    mv = bestJ != old;
+                    S.labels[row] = bestJ;
+                    S.ub[row] = U1;
+                    // scanned groups: certified min over members other than the new label
+                    for (int q = w.y; q < w.y + w.z; q++) {
+                        const float4 r = S.yres[q];
+                        const int pj = __float_as_int(r.x);
+                        const float gm = (pj == bestJ) ? r.z : r.y;
+                        lbr[S.ypairs[q].y] =
+                            isinf(gm) ? INFINITY
+                                      : fmaxf((sqrtf(gm) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
+                    }
+                    if (mv) {
+                        // the old label becomes an "other" member of its group
+                        const int go = S.group_of[old];
+                        const float la = fmaxf((sqrtf(acc_a) - kU32 * (xn + S.cnorm[old])) * (1.0f - rho), 0.f);
+                        lbr[go] = fminf(lbr[go], la);
+                    }
+                } else {
+                    flag = true;
+                }
+            }
+        }
+        int64_t pos = block_append(mv, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
+        if (mv) S.moved[pos] = make_int2((int)row, old);
+        int64_t fpos = block_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED), scr);
+        if (flag) S.flagged[fpos] = (int)row;
+        int64_t wpos = block_append(full, (unsigned long long*)(stat + LK_STAT_WORK), scr);
+        if (full) S.work[wpos] = (int)row;
+    }
+}
+
+}  // namespace yy
+}  // namespace lk
+
+namespace lkh {
+
+using namespace lk::yy;
+
+static int grid_for_rows(int64_t rows, int sms, int per_sm) {
+    int64_t b = (rows + kThreads - 1) / kThreads;
+    if (b < 1) b = 1;
+    if (b > (int64_t)sms * per_sm) b = sms * per_sm;
+    return (int)b;
+}
+
+lk_status launch_yinyang(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    const size_t smem = (size_t)S.t_groups * sizeof(float);
+    if (smem > 48 * 1024)
+        LK_CUDA_CHECK(cudaFuncSetAttribute(k_filter_yinyang,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_filter_yinyang<<<grid_for_rows(S.n, sms, 8), kThreads, smem, st>>>(S, stat);
+    LK_LAUNCH_CHECK();
+    k_yy_pairs<<<sms * 8, kThreads, 0, st>>>(S, stat);
+    LK_LAUNCH_CHECK();
+    k_yy_merge<<<grid_for_rows(S.n, sms, 4), kThreads, 0, st>>>(S, stat);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+}  // namespace lkh

@@ -29,6 +29,31 @@ def _torch():
     return torch
 
 
+GROUP_STRATEGIES = ("yinyang", "elkan", "regroup")
+
+
+def group_centroids(centers: np.ndarray, t: int, seed: int = 0, n_iters: int = 5) -> np.ndarray:
+    """Partition k centroids into t groups by a few Lloyd passes over the
+    centroids (the idea of bounds.py:175-196; any grouping yields the same
+    labels, it only changes how much the group bounds prune)."""
+    k = centers.shape[0]
+    t = max(1, min(t, k))
+    if t == k:
+        return np.arange(k, dtype=np.int32)
+    rng = np.random.default_rng(seed)
+    means = centers[rng.choice(k, size=t, replace=False)].copy()
+    cn = np.sum(centers * centers, axis=1)
+    g = np.zeros(k, dtype=np.int64)
+    for _ in range(n_iters):
+        d2 = cn[:, None] - 2.0 * centers @ means.T + np.sum(means * means, axis=1)[None, :]
+        g = np.argmin(d2, axis=1)
+        for q in range(t):
+            mem = centers[g == q]
+            if len(mem):
+                means[q] = mem.mean(axis=0)
+    return g.astype(np.int32)
+
+
 @dataclass
 class IterRecord:
     changed: int
@@ -36,6 +61,7 @@ class IterRecord:
     candidate: int
     active: int
     work: int
+    group_dists: int
     sse: float
     assign_ms: float
     update_ms: float
@@ -46,7 +72,7 @@ class DeviceLloyd:
 
     def __init__(self, data, k: int, strategy: str = "lloyd", t_max: int = 10, *,
                  device=None, kernel: str = "auto", groups: int = 0, comm=None,
-                 n_total: int | None = None):
+                 n_total: int | None = None, group_seed: int = 0):
         torch = _torch()
         if not torch.cuda.is_available():
             raise nat.NativeError("no CUDA device: the B200 path has no CPU fallback")
@@ -60,6 +86,7 @@ class DeviceLloyd:
                                       else int(device)))
         self.comm = comm
         self.strategy = strategy
+        self.group_seed = group_seed
         self.k = int(k)
         self.t_max = int(t_max)
 
@@ -166,8 +193,16 @@ class DeviceLloyd:
             pass
 
     # -- iteration --------------------------------------------------------
+    def set_groups(self, group_of):
+        g = np.ascontiguousarray(group_of, dtype=np.int32)
+        nat.check(self.lib.lk_set_groups(self.ctx, ctypes.c_void_p(g.ctypes.data),
+                                         self.stream_handle()), "lk_set_groups")
+
     def set_centroids(self, init):
         torch = _torch()
+        if self.strategy in GROUP_STRATEGIES:
+            self.set_groups(group_centroids(np.asarray(init, dtype=np.float64), self.nlb,
+                                            seed=self.group_seed))
         with torch.cuda.device(self.dev):
             c = torch.as_tensor(np.ascontiguousarray(init, dtype=np.float64)) \
                 if not isinstance(init, torch.Tensor) else init.to(torch.float64)
@@ -259,6 +294,7 @@ class DeviceLloyd:
                     candidate=int(stats[t, nat.STAT["candidate"]]),
                     active=int(stats[t, nat.STAT["active"]]),
                     work=int(stats[t, nat.STAT["work"]]),
+                    group_dists=int(stats[t, nat.STAT["dist"]]),
                     sse=float(sse[t]),
                     assign_ms=e0.elapsed_time(e1),
                     update_ms=e1.elapsed_time(e2)))

@@ -80,6 +80,12 @@ def _iteration_stats(strategy: str, t: int, rec, n: int, k: int) -> IterationSta
         dist = n * k
         if strategy != "lloyd":
             kw["bound_updates"] = 2 * n
+    elif strategy in ("yinyang", "elkan"):
+        # tightened rows + group scans (pruners.py:445-487 accounting)
+        dist = rec.active + rec.group_dists + rec.work * (k - 1)
+        kw["bound_dist_comps"] = k
+        kw["bound_accesses"] = n
+        kw["bound_updates"] = n + rec.active + 2 * rec.work
     else:
         dist = rec.active + rec.work * (k - 1)
         kw["bound_dist_comps"] = k + k * k
@@ -93,13 +99,14 @@ def _iteration_stats(strategy: str, t: int, rec, n: int, k: int) -> IterationSta
 
 def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: RunContext, *,
                label: str, kernel: str = "auto", record_history: bool = True,
-               device=None) -> RunResult:
+               device=None, groups: int = 0, group_seed: int = 0) -> RunResult:
     """Shared body of run_lloyd / run_pruner / run_engine on one GPU."""
     from .device import DeviceLloyd
 
     n = x.shape[0]
     init_copy = centers.copy()
-    eng = DeviceLloyd(x, k, strategy, t_max, kernel=kernel, device=device)
+    eng = DeviceLloyd(x, k, strategy, t_max, kernel=kernel, device=device, groups=groups,
+                      group_seed=group_seed)
     try:
         out = eng.run(centers, record_history=record_history)
     finally:

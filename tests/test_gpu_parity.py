@@ -57,7 +57,7 @@ def check_trajectory(oracle, x, init, gpu_hist, ref_hist, what):
             f"{what}: iteration {t + 1}: {int(np.sum(gap > LABEL_GAP_EXEMPT))} non-tie label mismatches"
 
 
-@pytest.mark.parametrize("strategy", ["lloyd", "hamerly"])
+@pytest.mark.parametrize("strategy", ["lloyd", "hamerly", "yinyang", "elkan"])
 @pytest.mark.parametrize("name", RUN_CASES)
 def test_golden_runs(oracle, name, strategy):
     g = load_golden(name)
@@ -108,12 +108,14 @@ def test_strategies_are_bit_identical():
             assert np.array_equal(u, v), s
 
 
-def test_hamerly_prunes_later_iterations():
+@pytest.mark.parametrize("strategy", ["hamerly", "yinyang", "elkan"])
+def test_bounded_strategies_prune_later_iterations(strategy):
     g = load_golden("pruners_blobs")
     k = int(g["k"])
-    res = lk().run_pruner(g["data"], k, "hamerly", init=g["init"], t_max=8)
+    res = lk().run_pruner(g["data"], k, strategy, init=g["init"], t_max=8)
     n = g["data"].shape[0]
     assert res.iterations[0].dist_comps == n * k
+    assert all(s.dist_comps <= n * k for s in res.iterations)
     assert min(s.dist_comps for s in res.iterations[1:]) < n * k
 
 
@@ -124,7 +126,7 @@ def test_tiny_k(oracle, k):
     m = lk()
     init = m.make_init(m.RunContext(seed=5), x, k)
     ref = oracle.run_lloyd(x, k, init, 8)
-    for s in ("lloyd", "hamerly"):
+    for s in ("lloyd", "hamerly", "yinyang", "elkan"):
         res = m.run_lloyd(x, k, init=init, t_max=8) if s == "lloyd" else \
             m.run_pruner(x, k, s, init=init, t_max=8)
         check_trajectory(oracle, x, init, res.assign_history, ref["history"], f"k={k} {s}")
@@ -168,7 +170,7 @@ SCALED = [("cfg1", 100_000, None, 50), ("cfg2", 100_000, None, 100), ("cfg3", 10
           ("cfg4", 5_000, None, 15), ("cfg5", 50_000, None, 3)]
 
 
-@pytest.mark.parametrize("strategy", ["lloyd", "hamerly"])
+@pytest.mark.parametrize("strategy", ["lloyd", "hamerly", "yinyang"])
 @pytest.mark.parametrize("name,n,k,t_max", SCALED)
 def test_scaled_configs_match_oracle(oracle, name, n, k, t_max, strategy):
     from paper_2010_06654_b200 import datasets
