@@ -256,7 +256,7 @@ def run_ours(args):
     chg = stats[:, 7]
     converged_in_window = bool(np.any(chg[W:T - 1] == 0))
     recs = [{"t": t + 1, "changed": int(stats[t, 0]), "flagged": int(stats[t, 1]),
-             "candidate": int(stats[t, 6]),
+             "candidate": int(stats[t, 6]), "ywl": int(stats[t, 9]), "pairs": int(stats[t, 10]),
              "active": int(stats[t, 2]), "work": int(stats[t, 3])} for t in range(W, T)]
 
     # profiled pass over the same iterations: per-class device time
@@ -347,7 +347,9 @@ def run_ours(args):
             "window_stats": {"changed": [r["changed"] for r in recs],
                              "rescanned": [r["work"] for r in recs],
                              "rechecked": [r["flagged"] for r in recs],
-                             "candidate_rows": [r["candidate"] for r in recs]},
+                             "candidate_rows": [r["candidate"] for r in recs],
+                             "group_rows": [r["ywl"] for r in recs],
+                             "group_scans": [r["pairs"] for r in recs]},
         }
         print(json.dumps(line))
     if ws > 1:

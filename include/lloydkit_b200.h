@@ -94,7 +94,7 @@ typedef enum {
     LK_BUF_C64 = 2,        /* double [k, d]          centroids (master copy) */
     LK_BUF_LABELS = 3,     /* int32  [n_local]       current labels */
     LK_BUF_UB = 4,         /* float  [n_local]       upper bounds */
-    LK_BUF_LB = 5,         /* float  [n_local, nlb]  lower bounds */
+    LK_BUF_LB = 5,         /* float  [nlb, n_local]  lower bounds (group-major) */
     LK_BUF_DELTA = 6,      /* int64  [delta_len]     all-reduce payload */
     LK_BUF_STATS = 7,      /* int64  [t_max, LK_NSTAT] per-iteration counters */
     LK_BUF_SSE = 8,        /* double [t_max]         per-iteration SSE */

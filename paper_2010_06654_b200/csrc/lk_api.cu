@@ -38,7 +38,7 @@ enum InternalBuf {
     B_C64_PREV, B_C32, B_CNORM, B_DRIFT, B_SHALF, B_GDRIFT, B_SCAL, B_MOVED, B_FLAGGED, B_WORK,
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
-    B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES,
+    B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN,
     B_COUNT_
 };
 
@@ -139,6 +139,9 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_YWL] = (uint64_t)n * 16;
         L->size[B_YPAIRS] = (uint64_t)cap * 8;
         L->size[B_YRES] = (uint64_t)cap * 16;
+        L->size[B_GINV] = (uint64_t)k * 4;
+        L->size[B_CG] = (uint64_t)k * L->ldc * 4;
+        L->size[B_YLUN] = (uint64_t)n * 4;
     }
     uint64_t off = 0;
     for (int b = 0; b < B_COUNT_; b++) {
@@ -334,6 +337,9 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.ywl = buf<int4>(c, B_YWL);
     S.ypairs = buf<int2>(c, B_YPAIRS);
     S.yres = buf<float4>(c, B_YRES);
+    S.ginv = buf<int32_t>(c, B_GINV);
+    S.Cg = buf<float>(c, B_CG);
+    S.ylun = buf<float>(c, B_YLUN);
     S.pair_cap = L.pair_cap;
 
     std::vector<int32_t> prog;
@@ -439,6 +445,7 @@ static __global__ void k_init_centroids(lk::DevState S, int kpad) {
         double c = z < S.d ? S.C64[(int64_t)j * S.d + z] : 0.0;
         float v = (float)c;
         S.C32[(int64_t)j * S.ldc + z] = v;
+        if (S.Cg) S.Cg[(int64_t)S.ginv[j] * S.ldc + z] = v;
         if (z < S.d) S.C64_prev[(int64_t)j * S.d + z] = c;
         cn2 = fma((double)v, (double)v, cn2);
         c2 = fma(c, c, c2);
@@ -478,12 +485,16 @@ lk_status lk_set_groups(lk_ctx* c, const int32_t* group_of, void* stream) {
         cnt[group_of[j]]++;
     }
     for (int g = 0; g < t; g++) off[g + 1] = off[g] + cnt[g];
-    std::vector<int32_t> fill(off.begin(), off.end());
-    for (int j = 0; j < k; j++) perm[fill[group_of[j]]++] = j;  // ascending j within a group
+    std::vector<int32_t> fill(off.begin(), off.end()), inv(k);
+    for (int j = 0; j < k; j++) {
+        inv[j] = fill[group_of[j]];
+        perm[fill[group_of[j]]++] = j;  // ascending j within a group
+    }
     cudaStream_t st = (cudaStream_t)stream;
     LK_CUDA_CHECK(cudaMemcpyAsync(c->S.group_of, group_of, k * 4, cudaMemcpyHostToDevice, st));
     LK_CUDA_CHECK(cudaMemcpyAsync(c->S.gperm, perm.data(), k * 4, cudaMemcpyHostToDevice, st));
     LK_CUDA_CHECK(cudaMemcpyAsync(c->S.goff, off.data(), (t + 1) * 4, cudaMemcpyHostToDevice, st));
+    LK_CUDA_CHECK(cudaMemcpyAsync(c->S.ginv, inv.data(), k * 4, cudaMemcpyHostToDevice, st));
     LK_CUDA_CHECK(cudaStreamSynchronize(st));
     c->groups_set = true;
     return LK_OK;
@@ -491,6 +502,10 @@ lk_status lk_set_groups(lk_ctx* c, const int32_t* group_of, void* stream) {
 
 lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     if (!c || !c64) return LK_ERR_ARG;
+    if (!c->groups_set) {
+        set_error("lk_set_centroids: call lk_set_groups first for group-bound strategies");
+        return LK_ERR_STATE;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     lk::DevState& S = c->S;
     const int64_t k = c->cfg.k, d = c->cfg.d;
@@ -592,7 +607,7 @@ lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
     }
     cudaStream_t st = (cudaStream_t)stream;
     ProfScope p(c, 4, st);
-    const bool need_half = c->cfg.strategy == LK_STRAT_HAMERLY;
+    const bool need_half = c->cfg.strategy != LK_STRAT_LLOYD;
     lk_status s = lkh::launch_update(c->S, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV),
                                      buf<double>(c, B_SSE_PART), t, need_half, st);
     c->launches += need_half ? 4 : 2;

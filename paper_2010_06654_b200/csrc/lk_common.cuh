@@ -37,7 +37,7 @@ struct DevState {
     int32_t* group_of;      // [k]
     int32_t* labels;        // [n]
     float* ub;              // [n]
-    float* lb;              // [n, nlb]
+    float* lb;              // [nlb, n] (group-major)
     int2* moved;            // [n] (row, old label)
     int32_t* flagged;       // [n]
     int32_t* work;          // [n]
@@ -68,7 +68,10 @@ struct DevState {
     int32_t* ovf;           // [n] overflow rows (fp32 difference-form rescan)
     // Yinyang group bounds
     int32_t* gperm;         // [k] centroid ids sorted by group
+    int32_t* ginv;          // [k] position of centroid j in gperm
     int32_t* goff;          // [t + 1] group ranges in gperm
+    float* Cg;              // [k, ldc] fp32 centroids in group order (gperm)
+    float* ylun;            // [n] per worklist row: min bound over its unscanned groups
     int4* ywl;              // [n] worklist: (row, pair offset, pair count, bits of D~_a)
     int2* ypairs;           // [pair_cap] (worklist index, group)
     float4* yres;           // [pair_cap] (bits of best j, best D~, second D~, -)
@@ -77,9 +80,10 @@ struct DevState {
 
 // Finalize a row's lower bounds from one certified bound on every non-winning
 // centroid (Hamerly: the single slot; Yinyang: every group slot).
+// The bound table is group-major, lb[g * n + row], so a warp's loads of one
+// group's bounds are coalesced.
 __device__ __forceinline__ void write_lb_all(const DevState& S, int64_t row, float v) {
-    float* p = S.lb + row * S.nlb;
-    for (int g = 0; g < S.nlb; g++) p[g] = v;
+    for (int g = 0; g < S.nlb; g++) S.lb[(int64_t)g * S.n + row] = v;
 }
 
 __device__ __forceinline__ float tf32_trunc(float x) {

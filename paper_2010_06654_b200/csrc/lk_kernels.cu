@@ -536,6 +536,7 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
         drift2 = fma(dd, dd, drift2);
         float c32 = (float)c;
         S.C32[(int64_t)j * S.ldc + z] = c32;
+        if (S.Cg) S.Cg[(int64_t)S.ginv[j] * S.ldc + z] = c32;
         cn2 = fma((double)c32, (double)c32, cn2);
         if (S.Chi) {
             float hi = tf32_trunc(c32);

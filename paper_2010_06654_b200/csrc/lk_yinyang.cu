@@ -100,17 +100,22 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang(DevState S, int64_t
         const bool valid = i < S.n;
         bool active = false, need = false;
         int cnt = 0;
-        float acc_a = 0.f, u = 0.f;
-        float* lbr = S.lb + i * t;
+        float acc_a = 0.f, u = 0.f, lun = INFINITY;
+        float* lbr = S.lb + i;  // group g at lbr[g * n]
+        const int64_t ln = S.n;
         if (valid) {
             const int a = S.labels[i];
             u = __fadd_ru(S.ub[i], S.drift[a]);
             float gmin = INFINITY;
             for (int g = 0; g < t; g++) {
-                float v = fmaxf(__fsub_rd(lbr[g], gd[g]), 0.f);
-                lbr[g] = v;
+                float v = fmaxf(__fsub_rd(lbr[g * ln], gd[g]), 0.f);
+                lbr[g * ln] = v;
                 gmin = fminf(gmin, v);
             }
+            // Hamerly's centroid-separation test holds for every bound family:
+            // d(x, c_j) >= 2 s_a - ub >= ub for all j != a when s_a > ub.
+            const float sa = S.s_half[a];
+            gmin = fmaxf(gmin, sa);
             if (!(gmin > u)) {
                 active = true;
                 const float* xp = S.X32 + i * S.ldx;
@@ -121,17 +126,22 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang(DevState S, int64_t
             }
             S.ub[i] = u;
             if (need)
-                for (int g = 0; g < t; g++) cnt += !(lbr[g] > u);
+                for (int g = 0; g < t; g++) {
+                    const float v = lbr[g * ln];
+                    if (v > u) lun = fminf(lun, v);  // this group stays unscanned
+                    else cnt++;
+                }
         }
         block_count(active, stat + LK_STAT_ACTIVE, scr);
         const int64_t wpos = block_append(need, (unsigned long long*)(stat + LK_STAT_YWL), scr);
         const int64_t poff = block_reserve(need ? cnt : 0, (unsigned long long*)(stat + LK_STAT_PAIRS), scr);
         if (need) {
+            S.ylun[wpos] = lun;
             if (poff + cnt <= S.pair_cap) {
                 S.ywl[wpos] = make_int4((int)i, (int)poff, cnt, __float_as_int(acc_a));
                 int p = 0;
                 for (int g = 0; g < t; g++)
-                    if (!(lbr[g] > u)) S.ypairs[poff + p++] = make_int2((int)wpos, g);
+                    if (!(lbr[g * ln] > u)) S.ypairs[poff + p++] = make_int2((int)wpos, g);
             } else {
                 // over capacity: full rescan instead; neutralise any reserved slots
                 S.ywl[wpos] = make_int4((int)i, -1, 0, __float_as_int(acc_a));
@@ -142,9 +152,42 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang(DevState S, int64_t
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_yy_pairs(DevState S, int64_t* stat) {
+__device__ __forceinline__ float dist2_ptr(const float* xp, const float* cp, int d, bool vec4) {
+    float acc = 0.f;
+    int z = 0;
+    if (vec4) {
+        for (; z + 4 <= d; z += 4) {
+            float4 xv = *reinterpret_cast<const float4*>(xp + z);
+            float4 cv = *reinterpret_cast<const float4*>(cp + z);
+            float t0 = xv.x - cv.x, t1 = xv.y - cv.y, t2 = xv.z - cv.z, t3 = xv.w - cv.w;
+            acc = fmaf(t0, t0, acc);
+            acc = fmaf(t1, t1, acc);
+            acc = fmaf(t2, t2, acc);
+            acc = fmaf(t3, t3, acc);
+        }
+    }
+    for (; z < d; z++) {
+        float t = xp[z] - cp[z];
+        acc = fmaf(t, t, acc);
+    }
+    return acc;
+}
+
+// One thread per (row, group) pair; the group's members are contiguous in Cg
+// (staged in shared memory when all centroids fit).
+__global__ void __launch_bounds__(kThreads) k_yy_pairs(DevState S, int64_t* stat, int staged) {
     if (*S.done) return;
+    extern __shared__ __align__(16) float csm[];
     const int64_t np_ = min((int64_t)stat[LK_STAT_PAIRS], S.pair_cap);
+    if ((int64_t)blockIdx.x * kThreads >= np_) return;
+    const float* cbase = S.Cg;
+    if (staged) {
+        const int tot = S.k * S.ldc;
+        for (int e = threadIdx.x; e < tot; e += kThreads) csm[e] = S.Cg[e];
+        __syncthreads();
+        cbase = csm;
+    }
+    const bool vec4 = (S.ldc & 3) == 0 && (S.ldx & 3) == 0;
     int64_t ndist = 0;
     for (int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x; p < np_;
          p += (int64_t)gridDim.x * kThreads) {
@@ -152,20 +195,41 @@ __global__ void __launch_bounds__(kThreads) k_yy_pairs(DevState S, int64_t* stat
         if (pr.y < 0) continue;
         const int4 w = S.ywl[pr.x];
         const int64_t row = w.x;
-        const int a = S.labels[row];
+        const int apos = S.ginv[S.labels[row]];
         const float* xp = S.X32 + row * S.ldx;
+        float xr[4];
         float b1 = INFINITY, b2 = INFINITY;
-        int j1 = -1;
+        int p1 = -1;
         const int j0 = S.goff[pr.y], j9 = S.goff[pr.y + 1];
-        for (int jj = j0; jj < j9; jj++) {
-            const int j = S.gperm[jj];
-            if (j == a) continue;  // the assigned centroid competes via the tightened bound
-            const float D = dist2_row(S, xp, j);
-            if (D < b1) { b2 = b1; b1 = D; j1 = j; }
-            else b2 = fminf(b2, D);
+        if (S.d <= 4) {
+#pragma unroll
+            for (int z = 0; z < 4; z++) xr[z] = z < S.d ? __ldg(xp + z) : 0.f;
+            for (int jj = j0; jj < j9; jj++) {
+                if (jj == apos) continue;  // the label competes via the tightened bound
+                const float* cp = cbase + (int64_t)jj * S.ldc;
+                float acc = 0.f;
+#pragma unroll
+                for (int z = 0; z < 4; z++) {
+                    if (z < S.d) {
+                        float t = xr[z] - cp[z];
+                        acc = fmaf(t, t, acc);
+                    }
+                }
+                if (acc < b1) { b2 = b1; b1 = acc; p1 = jj; }
+                else b2 = fminf(b2, acc);
+            }
+        } else {
+            for (int jj = j0; jj < j9; jj++) {
+                if (jj == apos) continue;
+                const float acc = dist2_ptr(xp, cbase + (int64_t)jj * S.ldc, S.d, vec4);
+                if (acc < b1) { b2 = b1; b1 = acc; p1 = jj; }
+                else b2 = fminf(b2, acc);
+            }
         }
-        ndist += j9 - j0;
-        S.yres[p] = make_float4(__int_as_float(j1), b1, b2, 0.f);
+        ndist += (j9 - j0) - (apos >= j0 && apos < j9 ? 1 : 0);
+        // positions ascend with centroid id inside a group, so the first
+        // strict minimum is also the lowest centroid id among equal values
+        S.yres[p] = make_float4(__int_as_float(p1 >= 0 ? S.gperm[p1] : -1), b1, b2, 0.f);
     }
     warp_add(ndist, stat + LK_STAT_DIST);
 }
@@ -208,14 +272,9 @@ __global__ void __launch_bounds__(kThreads) k_yy_merge(DevState S, int64_t* stat
                     }
                     secD = fminf(secD, r.z);
                 }
-                float* lbr = S.lb + row * t;
-                // lower bound over unscanned groups (pairs are in ascending group order)
-                float lun = INFINITY;
-                int p = w.y;
-                for (int g = 0; g < t; g++) {
-                    if (p < w.y + w.z && S.ypairs[p].y == g) { p++; continue; }
-                    lun = fminf(lun, lbr[g]);
-                }
+                float* lbr = S.lb + row;  // group g at lbr[g * n]
+                const int64_t ln = S.n;
+                const float lun = S.ylun[e];  // min bound over the unscanned groups
                 const float U1 = (sqrtf(bestD) + kU32 * (xn + S.cnorm[bestJ])) * (1.0f + rho);
                 const float Ls = isinf(secD) ? INFINITY
                                              : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
@@ -229,7 +288,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_merge(DevState S, int64_t* stat
                         const float4 r = S.yres[q];
                         const int pj = __float_as_int(r.x);
                         const float gm = (pj == bestJ) ? r.z : r.y;
-                        lbr[S.ypairs[q].y] =
+                        lbr[(int64_t)S.ypairs[q].y * ln] =
                             isinf(gm) ? INFINITY
                                       : fmaxf((sqrtf(gm) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
                     }
@@ -237,7 +296,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_merge(DevState S, int64_t* stat
                         // the old label becomes an "other" member of its group
                         const int go = S.group_of[old];
                         const float la = fmaxf((sqrtf(acc_a) - kU32 * (xn + S.cnorm[old])) * (1.0f - rho), 0.f);
-                        lbr[go] = fminf(lbr[go], la);
+                        lbr[go * ln] = fminf(lbr[go * ln], la);
                     }
                 } else {
                     flag = true;
@@ -274,7 +333,15 @@ lk_status launch_yinyang(const lk::DevState& S, int64_t* stat, int sms, cudaStre
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_filter_yinyang<<<grid_for_rows(S.n, sms, 8), kThreads, smem, st>>>(S, stat);
     LK_LAUNCH_CHECK();
-    k_yy_pairs<<<sms * 8, kThreads, 0, st>>>(S, stat);
+    const size_t csm = (size_t)S.k * S.ldc * sizeof(float);
+    const int staged = csm <= 96 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           96 * 1024));
+        attr = true;
+    }
+    k_yy_pairs<<<sms * (staged ? 2 : 8), kThreads, staged ? csm : 0, st>>>(S, stat, staged);
     LK_LAUNCH_CHECK();
     k_yy_merge<<<grid_for_rows(S.n, sms, 4), kThreads, 0, st>>>(S, stat);
     LK_LAUNCH_CHECK();

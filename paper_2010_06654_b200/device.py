@@ -138,7 +138,7 @@ class DeviceLloyd:
         self.counts = self._view("counts", torch.int64, (self.k,))
         if strategy != "lloyd":
             self.ub = self._view("ub", torch.float32, (self.n,))
-            self.lb = self._view("lb", torch.float32, (self.n, self.nlb))
+            self.lb = self._view("lb", torch.float32, (self.nlb, self.n))
         self.h2d_bytes = 0
         self._bind(src, has_x64)
 
