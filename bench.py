@@ -171,6 +171,10 @@ def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kern
     if cls == 1:  # Hamerly filter: label 4 + ub 4 + lb 4 read, ub 4 + lb 4 written,
         # 4 per appended row, + the tightened rows' point (4d)
         return "byte", sum(20.0 * n + 4.0 * r["work"] + 4.0 * d * r["active"] for r in recs)
+    if cls == 5:  # group scans: 2*d flops per (row, centroid) evaluated
+        return "flop", sum(2.0 * r.get("group_dists", 0) * d for r in recs)
+    if cls == 6:  # merge: worklist entry 16 + 8, pair results 24 per scan, bound writes
+        return "byte", sum(24.0 * r["ywl"] + 28.0 * r["pairs"] for r in recs)
     if cls == 2:  # recheck: fp64 flops 3*d per pair (sub, mul, add)
         return "flop", sum(3.0 * r["flagged"] * k * d for r in recs)
     if cls == 3:  # refine: moved rows (4d read + 8 move record + 4 label) + 2 sums rows (8d rmw)
@@ -179,7 +183,8 @@ def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kern
     return "byte", len(recs) * k * d * (8.0 * 5 + 4.0)
 
 
-CLASS_NAMES = {0: "assign", 1: "filter", 2: "recheck", 3: "refine", 4: "update"}
+CLASS_NAMES = {0: "assign", 1: "filter", 2: "recheck", 3: "refine", 4: "update", 5: "group_scan",
+               6: "group_merge"}
 
 
 def run_ours(args):
@@ -208,8 +213,9 @@ def run_ours(args):
     strategy = args.strategy
     gpu_strat = strategy
     from paper_2010_06654_b200.pruners import gpu_groups
+    n_groups = args.groups or gpu_groups(gpu_strat, n, k)
     eng = DeviceLloyd(x, k, gpu_strat, T, kernel=args.kernel, comm=group, n_total=n,
-                      groups=gpu_groups(gpu_strat, n, k), group_seed=cfg.seed_init)
+                      groups=n_groups, group_seed=cfg.seed_init, record_history=False)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
@@ -223,6 +229,14 @@ def run_ours(args):
         for t in range(1, W + 1):
             eng.step(t)
         torch.cuda.synchronize()
+        # one captured iteration replays every later one (device-side
+        # iteration index); the profiled pass runs eagerly for per-class events
+        graphs = None if (profile or args.no_graph) else eng.capture(W + 1)
+        launches_per_step = 0
+        if graphs is not None:
+            l0 = eng.launch_count()
+            eng.capture(W + 1)  # count the kernels one captured iteration holds
+            launches_per_step = eng.launch_count() - l0
         if profile:
             eng.profile(True)
         barrier()
@@ -234,13 +248,18 @@ def run_ours(args):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            eng.step(t)
+            if graphs is not None:
+                graphs[0].replay()
+                graphs[1].replay()
+            else:
+                eng.step(t)
             b.record(stream)
             evs.append((a, b))
         torch.cuda.synchronize()
         barrier()
         ms = sum(a.elapsed_time(b) for a, b in evs)
-        return ms, eng.launch_count() - launches0
+        launched = eng.launch_count() - launches0 + launches_per_step * (T - W if graphs else 0)
+        return ms, launched
 
     # untimed dry run (JIT / first-touch), then the timed trajectory
     trajectory(False)
@@ -257,11 +276,12 @@ def run_ours(args):
     converged_in_window = bool(np.any(chg[W:T - 1] == 0))
     recs = [{"t": t + 1, "changed": int(stats[t, 0]), "flagged": int(stats[t, 1]),
              "candidate": int(stats[t, 6]), "ywl": int(stats[t, 9]), "pairs": int(stats[t, 10]),
+             "group_dists": int(stats[t, 4]),
              "active": int(stats[t, 2]), "work": int(stats[t, 3])} for t in range(W, T)]
 
     # profiled pass over the same iterations: per-class device time
     _, _ = trajectory(True)
-    cls_ms = {c: eng.profile_read(c)[0] for c in range(5)}
+    cls_ms = {c: eng.profile_read(c)[0] for c in range(7)}
     eng.profile(False)
     dom = max(cls_ms, key=lambda c: cls_ms[c])
     peaks = load_peaks()
@@ -333,7 +353,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "fp32 (certified; fp64 recheck)", "data": "synthetic",
             "config": {"workload": args.workload, "n": n, "d": d, "k": k,
-                       "strategy": strategy, "kernel": args.kernel,
+                       "strategy": strategy, "kernel": args.kernel, "groups": n_groups,
                        "iterations": f"{W + 1}..{T} of one trajectory from random init",
                        "l2": "flushed (256 MB write) between timed iterations",
                        "parallelism": f"dp{ws} (row shards, int64 delta all-reduce)",
@@ -393,8 +413,10 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--strategy", default="hamerly", choices=["lloyd", "hamerly", "yinyang", "elkan"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--groups", type=int, default=0, help="Yinyang group count (0 = default)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches in the timed loop")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)  # contract: at least 3 warm-up steps
     if args.impl == "reference":

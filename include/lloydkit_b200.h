@@ -85,6 +85,7 @@ typedef struct {
     int32_t kernel;        /* lk_kernel */
     int32_t has_x64;       /* 1: an fp64 copy of X is bound (input not fp32-exact) */
     int32_t device;        /* CUDA device ordinal */
+    int64_t history_cap;   /* label-history log entries (0: no history log) */
 } lk_config;
 
 /* Named buffers inside the workspace (byte offsets via lk_buffer). */
@@ -101,7 +102,9 @@ typedef enum {
     LK_BUF_GROUP_OF = 9,   /* int32  [k]             centroid -> group */
     LK_BUF_COUNTS = 10,    /* int64  [k]             cluster sizes */
     LK_BUF_QEXP = 11,      /* int32  [d + 1]         fixed-point exponents */
-    LK_NBUF = 12
+    LK_BUF_HLOG = 12,      /* int32x2 [history_cap]  (row, new label) of every moved row */
+    LK_BUF_HLOG_OFF = 13,  /* int64  [t_max + 1]     log offset of each iteration (-1 overflow) */
+    LK_NBUF = 14
 } lk_buffer_id;
 
 /* Per-iteration counters (LK_BUF_STATS rows). */
@@ -157,7 +160,11 @@ lk_status lk_set_centroids(lk_ctx *ctx, const double *c64, void *stream);
 
 /* Iteration t (1-based): assignment (full scan or bound-filtered), exact fp64
  * recheck of ambiguous rows, changed count and member-sum deltas into
- * LK_BUF_DELTA.  Once an earlier iteration converged, kernels are no-ops. */
+ * LK_BUF_DELTA.  Once an earlier iteration converged, kernels are no-ops.
+ * The iteration index the kernels use lives on the device (advanced by
+ * lk_step_update), so the launches of any t >= 2 are identical and a CUDA
+ * graph captured from one iteration replays every later one; t only selects
+ * the first-iteration (full scan) path. */
 lk_status lk_step_assign(lk_ctx *ctx, int32_t t, void *stream);
 /* Iteration t: apply the (reduced) deltas, new centroids (empty clusters keep
  * theirs), drifts, bound tables, SSE into LK_BUF_SSE[t-1], done flag. */
@@ -166,9 +173,10 @@ lk_status lk_step_update(lk_ctx *ctx, int32_t t, void *stream);
 /* Number of kernel launches issued by this context so far. */
 int64_t lk_launch_count(const lk_ctx *ctx);
 
-/* Timing helper for bench.py: average device time (ms) of the kernels of one
- * class recorded with events since the last reset (class: 0 assign, 1 filter,
- * 2 recheck, 3 refine, 4 update).  Recording is enabled by lk_profile(ctx,1). */
+/* Timing helper for bench.py: total device time (ms) of the kernels of one
+ * class recorded with events since the last reset (class: 0 assign/rescan,
+ * 1 bound filter, 2 recheck, 3 refine, 4 update, 5 group scans, 6 group
+ * merge).  Recording is enabled by lk_profile(ctx, 1). */
 lk_status lk_profile(lk_ctx *ctx, int32_t enable);
 lk_status lk_profile_read(lk_ctx *ctx, int32_t cls, double *total_ms, int64_t *launches);
 

@@ -33,7 +33,7 @@ namespace {
 
 enum InternalBuf {
     B_X32 = 0, B_X64, B_C64, B_LABELS, B_UB, B_LB, B_DELTA, B_STATS, B_SSE, B_GROUP_OF, B_COUNTS,
-    B_QEXP,
+    B_QEXP, B_HLOG, B_HLOG_OFF, B_CUR,
     // internal
     B_C64_PREV, B_C32, B_CNORM, B_DRIFT, B_SHALF, B_GDRIFT, B_SCAL, B_MOVED, B_FLAGGED, B_WORK,
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
@@ -50,6 +50,7 @@ struct Layout {
     int32_t nlb, groups;
 };
 
+static bool is_group_strategy(int s);
 static bool is_group_strategy(int s) {
     return s == LK_STRAT_YINYANG || s == LK_STRAT_ELKAN || s == LK_STRAT_REGROUP;
 }
@@ -74,8 +75,11 @@ static bool tc_enabled(const lk_config& c) {
 }
 
 static bool make_layout(const lk_config& c, Layout* L) {
-    if (c.n_local < 0 || c.d < 1 || c.k < 1 || c.t_max < 0 || c.n_total < c.n_local) return false;
+    if (c.n_local < 0 || c.d < 1 || c.k < 1 || c.t_max < 0 || c.n_total < c.n_local ||
+        c.history_cap < 0)
+        return false;
     if (c.n_local > 0x7fffffffLL) return false;  // row ids are int32 on device
+    if (c.k > 32767) return false;                // packed (group, label position) pairs
     memset(L, 0, sizeof(*L));
     L->ldx = (c.d <= 2) ? c.d : ((c.d + 3) / 4) * 4;
     L->ldc = ((c.d + 3) / 4) * 4;
@@ -95,6 +99,9 @@ static bool make_layout(const lk_config& c, Layout* L) {
     L->size[B_GROUP_OF] = (uint64_t)k * 4;
     L->size[B_COUNTS] = (uint64_t)k * 8;
     L->size[B_QEXP] = (uint64_t)(d + 1) * 4;
+    L->size[B_HLOG] = c.history_cap > 0 ? (uint64_t)c.history_cap * 8 : 0;
+    L->size[B_HLOG_OFF] = (uint64_t)(tm + 1) * 8;
+    L->size[B_CUR] = (uint64_t)LK_NSTAT * 8;
     L->size[B_C64_PREV] = (uint64_t)k * d * 8;
     L->size[B_C32] = (uint64_t)k * L->ldc * 4;
     L->size[B_CNORM] = (uint64_t)k * 4;
@@ -141,7 +148,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_YRES] = (uint64_t)cap * 16;
         L->size[B_GINV] = (uint64_t)k * 4;
         L->size[B_CG] = (uint64_t)k * L->ldc * 4;
-        L->size[B_YLUN] = (uint64_t)n * 4;
+        L->size[B_YLUN] = (uint64_t)n * 8;
     }
     uint64_t off = 0;
     for (int b = 0; b < B_COUNT_; b++) {
@@ -316,6 +323,12 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.qsum = buf<int64_t>(c, B_QSUM);
     S.qexp = buf<int32_t>(c, B_QEXP);
     S.done = buf<int32_t>(c, B_DONE);
+    S.iter = S.done + 1;
+    S.cur = buf<int64_t>(c, B_CUR);
+    S.t_max = cfg->t_max;
+    S.hlog = buf<int2>(c, B_HLOG);
+    S.hlog_off = buf<int64_t>(c, B_HLOG_OFF);
+    S.hlog_cap = cfg->history_cap;
     S.stats = buf<int64_t>(c, B_STATS);
     S.sse = buf<double>(c, B_SSE);
     S.pw_prog = buf<int32_t>(c, B_PW_PROG);
@@ -339,7 +352,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.yres = buf<float4>(c, B_YRES);
     S.ginv = buf<int32_t>(c, B_GINV);
     S.Cg = buf<float>(c, B_CG);
-    S.ylun = buf<float>(c, B_YLUN);
+    S.ylun = buf<float2>(c, B_YLUN);
     S.pair_cap = L.pair_cap;
 
     std::vector<int32_t> prog;
@@ -352,6 +365,14 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.pw_len = (int32_t)prog.size();
     LK_CUDA_CHECK(cudaMemcpy(S.pw_prog, prog.data(), prog.size() * 4, cudaMemcpyHostToDevice));
     LK_CUDA_CHECK(cudaMemset(S.done, 0, 16));
+    // every kernel attribute is set here, never inside a (possibly captured) step
+    lk_status as = lkh::init_simt_attributes();
+    if (as == LK_OK && S.Xlo) as = lkh::init_tc_attributes();
+    if (as == LK_OK && S.Cg) as = lkh::init_yy_attributes();
+    if (as != LK_OK) {
+        delete c;
+        return as;
+    }
     *out = c;
     return LK_OK;
 }
@@ -459,6 +480,7 @@ static __global__ void k_init_centroids(lk::DevState S, int kpad) {
         cn2 += __shfl_xor_sync(LK_FULL_MASK, cn2, o);
         c2 += __shfl_xor_sync(LK_FULL_MASK, c2, o);
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *S.iter = 1;
     if (lane == 0) {
         if (S.cn2) S.cn2[j] = (float)c2;
         float cn = __double2float_ru(sqrt(cn2) * (1.0 + 1e-12));
@@ -518,6 +540,8 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     LK_CUDA_CHECK(cudaMemsetAsync(S.qsum, 0, k * 8, st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.done, 0, 16, st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.stats, 0, c->L.size[B_STATS], st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.cur, 0, c->L.size[B_CUR], st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.hlog_off, 0, c->L.size[B_HLOG_OFF], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.sse, 0, c->L.size[B_SSE], st));
     const int kpad = (int)((k + 255) / 256 * 256);
     k_init_centroids<<<(kpad + 7) / 8, 256, 0, st>>>(S, kpad);
@@ -539,7 +563,7 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
     }
     cudaStream_t st = (cudaStream_t)stream;
     lk::DevState& S = c->S;
-    int64_t* stat = S.stats + (int64_t)(t - 1) * LK_NSTAT;
+    int64_t* stat = S.cur;  // counters of the iteration in flight (copied out by the update)
     LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
     const int64_t n = c->cfg.n_local;
     const bool use_tc = lkh::tc_supported(S);
@@ -554,7 +578,17 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
         } else if (is_group_strategy(c->cfg.strategy)) {
             {
                 ProfScope p(c, 1, st);
-                s = lkh::launch_yinyang(S, stat, c->sms, st);
+                s = lkh::launch_yy_filter(S, stat, c->sms, st);
+                if (s != LK_OK) return s;
+            }
+            {
+                ProfScope p(c, 5, st);
+                s = lkh::launch_yy_pairs(S, stat, c->sms, st);
+                if (s != LK_OK) return s;
+            }
+            {
+                ProfScope p(c, 6, st);
+                s = lkh::launch_yy_merge(S, stat, c->sms, st);
                 if (s != LK_OK) return s;
             }
             ProfScope p(c, 0, st);
@@ -593,8 +627,10 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             ProfScope p(c, 3, st);
             s = lkh::launch_refine(S, stat, buf<double>(c, B_QSCALE), n, c->sms, st);
             if (s != LK_OK) return s;
+            s = lkh::launch_log_history(S, c->sms, st);
+            if (s != LK_OK) return s;
         }
-        c->launches += 2;
+        c->launches += S.hlog ? 3 : 2;
     }
     return LK_OK;
 }
@@ -609,7 +645,7 @@ lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
     ProfScope p(c, 4, st);
     const bool need_half = c->cfg.strategy != LK_STRAT_LLOYD;
     lk_status s = lkh::launch_update(c->S, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV),
-                                     buf<double>(c, B_SSE_PART), t, need_half, st);
+                                     buf<double>(c, B_SSE_PART), need_half, st);
     c->launches += need_half ? 4 : 2;
     return s;
 }

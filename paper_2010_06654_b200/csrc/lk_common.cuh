@@ -48,7 +48,13 @@ struct DevState {
     int32_t* qexp;          // [d+1] exponents (max|x_z| < 2^qexp[z]; qexp[d] for ||x||^2)
     int32_t* qshift;        // [d+1] fixed-point shifts
     int32_t* done;          // [1] set once an iteration had changed == 0
+    int32_t* iter;          // [1] current iteration (1-based), advanced by the update
+    int64_t* cur;           // [LK_NSTAT] counters of the iteration in flight
     int64_t* stats;         // [t_max, LK_NSTAT]
+    int32_t t_max;
+    int2* hlog;             // [hlog_cap] label-history log: (row, new label) of moved rows
+    int64_t* hlog_off;      // [t_max + 1] log offsets per iteration (-1: overflow)
+    int64_t hlog_cap;
     double* sse;            // [t_max]
     int32_t* pw_prog;       // numpy pairwise-sum program for the fp64 recheck
     int32_t pw_len;
@@ -71,9 +77,9 @@ struct DevState {
     int32_t* ginv;          // [k] position of centroid j in gperm
     int32_t* goff;          // [t + 1] group ranges in gperm
     float* Cg;              // [k, ldc] fp32 centroids in group order (gperm)
-    float* ylun;            // [n] per worklist row: min bound over its unscanned groups
+    float2* ylun;           // [n] per worklist row: (min bound over unscanned groups, |x|)
     int4* ywl;              // [n] worklist: (row, pair offset, pair count, bits of D~_a)
-    int2* ypairs;           // [pair_cap] (worklist index, group)
+    int2* ypairs;           // [pair_cap] (row, group | label position << 16)
     float4* yres;           // [pair_cap] (bits of best j, best D~, second D~, -)
     int64_t pair_cap;
 };

@@ -17,10 +17,16 @@ lk_status launch_filter_hamerly(const lk::DevState& S, int64_t* stat, int sms, c
 lk_status launch_refine(const lk::DevState& S, int64_t* stat, const double* qscale,
                         int64_t max_rows, int sms, cudaStream_t st);
 lk_status launch_update(const lk::DevState& S, const double* qscale, const double* qinv,
-                        double* sse_part, int t, bool need_half, cudaStream_t st);
+                        double* sse_part, bool need_half, cudaStream_t st);
+lk_status launch_log_history(const lk::DevState& S, int sms, cudaStream_t st);
+lk_status init_simt_attributes();
+lk_status init_tc_attributes();
+lk_status init_yy_attributes();
 lk_status launch_scan_exp(const lk::DevState& S, int sms, cudaStream_t st);
 
-lk_status launch_yinyang(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
+lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
+lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
+lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 
 // tcgen05 path (lk_tc.cu): full-scan assignment with 3xTF32 products.
 bool tc_supported(const lk::DevState& S);

@@ -563,9 +563,9 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
 
 // Single block: SSE (fixed reduction order), max ||c||, top-2 drift, group
 // drifts, done flag.
-__global__ void __launch_bounds__(1024) k_update_global(DevState S, const double* sse_part,
-                                                        int t) {
+__global__ void __launch_bounds__(1024) k_update_global(DevState S, const double* sse_part) {
     if (*S.done) return;
+    const int t = *S.iter;
     __shared__ double ssum[1024];
     __shared__ float smax[1024], sd1[1024], sd2[1024];
     __shared__ int sarg[1024];
@@ -599,13 +599,18 @@ __global__ void __launch_bounds__(1024) k_update_global(DevState S, const double
         __syncthreads();
     }
     if (tid == 0) {
-        S.sse[t - 1] = ssum[0];
         S.scal[0] = smax[0];
         S.scal[1] = fmaxf(sd1[0], 0.f);
         S.scal[2] = fmaxf(sd2[0], 0.f);
         S.scal[3] = __int_as_float(sarg[0]);
-        int64_t changed = S.delta[(int64_t)S.k * S.d + 2 * S.k];
-        S.stats[(int64_t)(t - 1) * LK_NSTAT + LK_STAT_CHANGED_GLOBAL] = changed;
+        const int64_t changed = S.delta[(int64_t)S.k * S.d + 2 * S.k];
+        S.cur[LK_STAT_CHANGED_GLOBAL] = changed;
+        if (t >= 1 && t <= S.t_max) {
+            S.sse[t - 1] = ssum[0];
+            for (int q = 0; q < LK_NSTAT; q++) S.stats[(int64_t)(t - 1) * LK_NSTAT + q] = S.cur[q];
+        }
+        for (int q = 0; q < LK_NSTAT; q++) S.cur[q] = 0;
+        *S.iter = t + 1;
         if (changed == 0) *S.done = 1;
     }
     // group drifts (Yinyang): max drift over each group's members
@@ -683,6 +688,26 @@ __global__ void __launch_bounds__(kThreads) k_half_sep(DevState S) {
     }
 }
 
+// Label history as a log: the moved rows of iteration t with their new label
+// (iteration 1 moves every row off -1).  The host rebuilds per-iteration label
+// vectors from it (lloyd.py:140 assign_history) without copying n labels per
+// iteration.  Runs after the refine kernel, before the update.
+__global__ void k_log_history(DevState S) {
+    if (*S.done) return;
+    const int t = *S.iter;
+    if (t < 1 || t > S.t_max) return;
+    const int64_t m = S.cur[LK_STAT_CHANGED];
+    const int64_t base = S.hlog_off[t - 1];
+    const bool ok = base >= 0 && base + m <= S.hlog_cap;
+    if (blockIdx.x == 0 && threadIdx.x == 0) S.hlog_off[t] = ok ? base + m : -1;
+    if (!ok) return;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int row = S.moved[e].x;
+        S.hlog[base + e] = make_int2(row, S.labels[row]);
+    }
+}
+
 __global__ void k_fill_inf(DevState S) {
     if (*S.done) return;
     int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -743,12 +768,6 @@ static lk_status launch_reg(const DevState& S, const int32_t* rowlist, const int
     const int smem_cap = 96 * 1024;
     if ((int64_t)tile_k * DP * 4 > smem_cap) tile_k = smem_cap / (DP * 4);
     size_t smem = (size_t)tile_k * DP * 4;
-    static bool attr_set = false;
-    if (!attr_set) {
-        LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_reg<DP, RPT>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-        attr_set = true;
-    }
     int grid = grid_for(max_rows, kThreads * RPT, sms * 6);
     k_assign_reg<DP, RPT><<<grid, kThreads, smem, st>>>(S, rowlist, rowcount, stat, tile_k);
     LK_LAUNCH_CHECK();
@@ -771,13 +790,7 @@ lk_status launch_assign_simt(const DevState& S, const int32_t* rowlist, const in
 
 lk_status launch_recheck(const DevState& S, int64_t* stat, int64_t max_rows, int sms,
                          cudaStream_t st) {
-    size_t smem = (size_t)kRcWarps * S.d * sizeof(double);
-    static bool attr_set = false;
-    if (!attr_set) {
-        LK_CUDA_CHECK(cudaFuncSetAttribute(k_recheck_fp64,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = true;
-    }
+    size_t smem = (size_t)kRcWarps * S.d * sizeof(double);  // <= 48 KB for d <= 1536
     int grid = grid_for(max_rows, kRcWarps, sms * 8);
     k_recheck_fp64<<<grid, kRcWarps * 32, smem, st>>>(S, stat);
     LK_LAUNCH_CHECK();
@@ -821,11 +834,11 @@ lk_status launch_refine(const DevState& S, int64_t* stat, const double* qscale, 
 }
 
 lk_status launch_update(const DevState& S, const double* qscale, const double* qinv,
-                        double* sse_part, int t, bool need_half, cudaStream_t st) {
+                        double* sse_part, bool need_half, cudaStream_t st) {
     int grid = (S.k + (kThreads / 32) - 1) / (kThreads / 32);
     k_update_centroids<<<grid, kThreads, 0, st>>>(S, qscale, qinv, sse_part);
     LK_LAUNCH_CHECK();
-    k_update_global<<<1, 1024, 0, st>>>(S, sse_part, t);
+    k_update_global<<<1, 1024, 0, st>>>(S, sse_part);
     LK_LAUNCH_CHECK();
     if (need_half) {
         k_fill_inf<<<(S.k + kThreads - 1) / kThreads, kThreads, 0, st>>>(S);
@@ -834,6 +847,23 @@ lk_status launch_update(const DevState& S, const double* qscale, const double* q
         k_half_sep<<<g, kThreads, 0, st>>>(S);
         LK_LAUNCH_CHECK();
     }
+    return LK_OK;
+}
+
+lk_status launch_log_history(const DevState& S, int sms, cudaStream_t st) {
+    if (!S.hlog) return LK_OK;
+    k_log_history<<<sms * 2, kThreads, 0, st>>>(S);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status init_simt_attributes() {
+    const int cap = 96 * 1024;
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_reg<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_reg<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_reg<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_reg<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_reg<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
     return LK_OK;
 }
 

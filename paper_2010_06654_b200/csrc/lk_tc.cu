@@ -495,6 +495,18 @@ bool tc_supported(const DevState& S) {
     return S.Xlo != nullptr && S.d >= 8 && (S.ldx % 4) == 0 && get_encode() != nullptr;
 }
 
+lk_status init_tc_attributes() {
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kTop2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kCollect>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<256, kTop2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<256>::TOTAL));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<256, kCollect>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<256>::TOTAL));
+    return LK_OK;
+}
+
 lk_status launch_tc_prep_points(const DevState& S, int sms, cudaStream_t st) {
     if (!S.Xlo) return LK_OK;
     k_split_points<<<sms * 8, 256, 0, st>>>(S);
@@ -515,12 +527,6 @@ static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo
     A.n_ct = (S.k + BN - 1) / BN;
     A.n_kc = (S.d + KC - 1) / KC;
     const int smem = Smem<BN>::TOTAL;
-    static bool attr = false;
-    if (!attr) {
-        LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<BN, MODE>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
     int64_t tiles = (max_rows + BM - 1) / BM;
     int grid = (int)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
     k_assign_tc<BN, MODE><<<grid, kThreadsTC, smem, st>>>(mah, mal, mbh, mbl, S, A, stat);

@@ -86,7 +86,9 @@ __device__ __forceinline__ float xnorm(const DevState& S, const float* xp) {
     return sqrtf(s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_filter_yinyang(DevState S, int64_t* stat) {
+constexpr int kCh = 8;
+
+__global__ void __launch_bounds__(kThreads, 4) k_filter_yinyang(DevState S, int64_t* stat) {
     if (*S.done) return;
     extern __shared__ float gd[];  // [t] group drifts
     __shared__ unsigned long long scr[kThreads / 32 + 1];
@@ -100,17 +102,28 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang(DevState S, int64_t
         const bool valid = i < S.n;
         bool active = false, need = false;
         int cnt = 0;
-        float acc_a = 0.f, u = 0.f, lun = INFINITY;
+        float acc_a = 0.f, u = 0.f, lun = INFINITY, xn = 0.f;
+        int apos = 0;
         float* lbr = S.lb + i;  // group g at lbr[g * n]
         const int64_t ln = S.n;
         if (valid) {
             const int a = S.labels[i];
             u = __fadd_ru(S.ub[i], S.drift[a]);
             float gmin = INFINITY;
-            for (int g = 0; g < t; g++) {
-                float v = fmaxf(__fsub_rd(lbr[g * ln], gd[g]), 0.f);
-                lbr[g * ln] = v;
-                gmin = fminf(gmin, v);
+            // chunks of kCh groups: the chunk's loads are issued before its stores
+            for (int g0 = 0; g0 < t; g0 += kCh) {
+                float v[kCh];
+#pragma unroll
+                for (int q = 0; q < kCh; q++)
+                    if (g0 + q < t) v[q] = __ldcs(lbr + (int64_t)(g0 + q) * ln);
+#pragma unroll
+                for (int q = 0; q < kCh; q++) {
+                    if (g0 + q < t) {
+                        v[q] = fmaxf(__fsub_rd(v[q], gd[g0 + q]), 0.f);
+                        gmin = fminf(gmin, v[q]);
+                        __stcs(lbr + (int64_t)(g0 + q) * ln, v[q]);
+                    }
+                }
             }
             // Hamerly's centroid-separation test holds for every bound family:
             // d(x, c_j) >= 2 s_a - ub >= ub for all j != a when s_a > ub.
@@ -120,33 +133,44 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang(DevState S, int64_t
                 active = true;
                 const float* xp = S.X32 + i * S.ldx;
                 acc_a = dist2_row(S, xp, a);
-                const float U = (sqrtf(acc_a) + kU32 * (xnorm(S, xp) + S.cnorm[a])) * (1.0f + rho);
+                xn = xnorm(S, xp);
+                apos = S.ginv[a];
+                const float U = (sqrtf(acc_a) + kU32 * (xn + S.cnorm[a])) * (1.0f + rho);
                 u = fminf(u, U);
                 need = !(gmin > u);
             }
             S.ub[i] = u;
-            if (need)
-                for (int g = 0; g < t; g++) {
-                    const float v = lbr[g * ln];
-                    if (v > u) lun = fminf(lun, v);  // this group stays unscanned
-                    else cnt++;
+            if (need) {
+                for (int g0 = 0; g0 < t; g0 += kCh) {
+                    float v[kCh];
+#pragma unroll
+                    for (int q = 0; q < kCh; q++)
+                        if (g0 + q < t) v[q] = lbr[(int64_t)(g0 + q) * ln];
+#pragma unroll
+                    for (int q = 0; q < kCh; q++) {
+                        if (g0 + q < t) {
+                            if (v[q] > u) lun = fminf(lun, v[q]);  // group stays unscanned
+                            else cnt++;
+                        }
+                    }
                 }
+            }
         }
         block_count(active, stat + LK_STAT_ACTIVE, scr);
         const int64_t wpos = block_append(need, (unsigned long long*)(stat + LK_STAT_YWL), scr);
         const int64_t poff = block_reserve(need ? cnt : 0, (unsigned long long*)(stat + LK_STAT_PAIRS), scr);
         if (need) {
-            S.ylun[wpos] = lun;
+            S.ylun[wpos] = make_float2(lun, xn);
             if (poff + cnt <= S.pair_cap) {
                 S.ywl[wpos] = make_int4((int)i, (int)poff, cnt, __float_as_int(acc_a));
                 int p = 0;
                 for (int g = 0; g < t; g++)
-                    if (!(lbr[g * ln] > u)) S.ypairs[poff + p++] = make_int2((int)wpos, g);
+                    if (!(lbr[g * ln] > u)) S.ypairs[poff + p++] = make_int2((int)i, g | (apos << 16));
             } else {
                 // over capacity: full rescan instead; neutralise any reserved slots
                 S.ywl[wpos] = make_int4((int)i, -1, 0, __float_as_int(acc_a));
                 for (int64_t q = poff; q < S.pair_cap && q < poff + cnt; q++)
-                    S.ypairs[q] = make_int2((int)wpos, -1);
+                    S.ypairs[q] = make_int2((int)i, -1);
             }
         }
     }
@@ -193,14 +217,13 @@ __global__ void __launch_bounds__(kThreads) k_yy_pairs(DevState S, int64_t* stat
          p += (int64_t)gridDim.x * kThreads) {
         const int2 pr = S.ypairs[p];
         if (pr.y < 0) continue;
-        const int4 w = S.ywl[pr.x];
-        const int64_t row = w.x;
-        const int apos = S.ginv[S.labels[row]];
+        const int64_t row = pr.x;
+        const int g = pr.y & 0xFFFF, apos = pr.y >> 16;
         const float* xp = S.X32 + row * S.ldx;
         float xr[4];
         float b1 = INFINITY, b2 = INFINITY;
         int p1 = -1;
-        const int j0 = S.goff[pr.y], j9 = S.goff[pr.y + 1];
+        const int j0 = S.goff[g], j9 = S.goff[g + 1];
         if (S.d <= 4) {
 #pragma unroll
             for (int z = 0; z < 4; z++) xr[z] = z < S.d ? __ldg(xp + z) : 0.f;
@@ -254,8 +277,9 @@ __global__ void __launch_bounds__(kThreads) k_yy_merge(DevState S, int64_t* stat
             if (w.y < 0) {
                 full = true;
             } else {
-                const float* xp = S.X32 + row * S.ldx;
-                const float xn = xnorm(S, xp);
+                const float2 lx = S.ylun[e];
+                const float lun = lx.x;  // min bound over the unscanned groups
+                const float xn = lx.y;
                 const float acc_a = __int_as_float(w.w);
                 float bestD = acc_a, secD = INFINITY;
                 int bestJ = old;
@@ -274,7 +298,6 @@ __global__ void __launch_bounds__(kThreads) k_yy_merge(DevState S, int64_t* stat
                 }
                 float* lbr = S.lb + row;  // group g at lbr[g * n]
                 const int64_t ln = S.n;
-                const float lun = S.ylun[e];  // min bound over the unscanned groups
                 const float U1 = (sqrtf(bestD) + kU32 * (xn + S.cnorm[bestJ])) * (1.0f + rho);
                 const float Ls = isinf(secD) ? INFINITY
                                              : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
@@ -288,7 +311,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_merge(DevState S, int64_t* stat
                         const float4 r = S.yres[q];
                         const int pj = __float_as_int(r.x);
                         const float gm = (pj == bestJ) ? r.z : r.y;
-                        lbr[(int64_t)S.ypairs[q].y * ln] =
+                        lbr[(int64_t)(S.ypairs[q].y & 0xFFFF) * ln] =
                             isinf(gm) ? INFINITY
                                       : fmaxf((sqrtf(gm) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
                     }
@@ -326,23 +349,30 @@ static int grid_for_rows(int64_t rows, int sms, int per_sm) {
     return (int)b;
 }
 
-lk_status launch_yinyang(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
-    const size_t smem = (size_t)S.t_groups * sizeof(float);
-    if (smem > 48 * 1024)
-        LK_CUDA_CHECK(cudaFuncSetAttribute(k_filter_yinyang,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+lk_status init_yy_attributes() {
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       96 * 1024));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_filter_yinyang, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       64 * 1024));
+    return LK_OK;
+}
+
+lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    const size_t smem = (size_t)S.t_groups * sizeof(float);  // <= 64 KB (k <= 16384)
     k_filter_yinyang<<<grid_for_rows(S.n, sms, 8), kThreads, smem, st>>>(S, stat);
     LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     const size_t csm = (size_t)S.k * S.ldc * sizeof(float);
     const int staged = csm <= 96 * 1024;
-    static bool attr = false;
-    if (!attr) {
-        LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           96 * 1024));
-        attr = true;
-    }
     k_yy_pairs<<<sms * (staged ? 2 : 8), kThreads, staged ? csm : 0, st>>>(S, stat, staged);
     LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     k_yy_merge<<<grid_for_rows(S.n, sms, 4), kThreads, 0, st>>>(S, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;

@@ -16,6 +16,7 @@ summed across ranks between the assignment and the update phase.
 from __future__ import annotations
 
 import ctypes
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -67,12 +68,54 @@ class IterRecord:
     update_ms: float
 
 
+class LabelHistory(Sequence):
+    """assign_history (lloyd.py:140) rebuilt lazily from the device's moved-row
+    log: iteration 1 sets every row, iteration t applies its (row, label)
+    moves to iteration t-1's vector.  Behaves like the reference's list of
+    int64 arrays (len, indexing, iteration)."""
+
+    def __init__(self, n: int, parts):
+        self._n = n
+        self._parts = parts
+        self._cache = {}
+
+    def __len__(self):
+        return len(self._parts)
+
+    def _build(self, t: int) -> np.ndarray:
+        if t in self._cache:
+            return self._cache[t]
+        start = max((s for s in self._cache if s < t), default=-1)
+        cur = (self._cache[start].copy() if start >= 0 else np.full(self._n, -1, dtype=np.int64))
+        for s in range(start + 1, t + 1):
+            _, rows, labels = self._parts[s]
+            cur[rows] = labels
+            if s < t:
+                self._cache[s] = cur.copy()
+        self._cache[t] = cur
+        return cur
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        return self._build(i).copy()
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+
 class DeviceLloyd:
     """One GPU context over an (n, d) block of rows."""
 
     def __init__(self, data, k: int, strategy: str = "lloyd", t_max: int = 10, *,
                  device=None, kernel: str = "auto", groups: int = 0, comm=None,
-                 n_total: int | None = None, group_seed: int = 0):
+                 n_total: int | None = None, group_seed: int = 0,
+                 record_history: bool = True, history_iters: int = 4):
         torch = _torch()
         if not torch.cuda.is_available():
             raise nat.NativeError("no CUDA device: the B200 path has no CPU fallback")
@@ -107,10 +150,14 @@ class DeviceLloyd:
                 n_total = int(t.item())
         self.n_total = int(n_total)
 
+        # the history log holds the moves of history_iters iterations between
+        # drains; every iteration moves at most n rows
+        self.history_cap = self.n * history_iters if record_history and self.n else 0
         cfg = nat.LkConfig(n_local=self.n, n_total=self.n_total, d=self.d, k=self.k,
                            strategy=nat.STRAT_IDS[strategy], groups=int(groups),
                            t_max=max(1, self.t_max), kernel=nat.KERNEL_IDS[kernel],
-                           has_x64=int(has_x64), device=self.dev.index)
+                           has_x64=int(has_x64), device=self.dev.index,
+                           history_cap=self.history_cap)
         self.cfg = cfg
         nbytes = ctypes.c_uint64(0)
         nat.check(self.lib.lk_workspace_bytes(ctypes.byref(cfg), ctypes.byref(nbytes)),
@@ -136,6 +183,9 @@ class DeviceLloyd:
         self.sse_buf = self._view("sse", torch.float64, (max(1, self.t_max),))
         self.qexp = self._view("qexp", torch.int32, (self.d + 1,))
         self.counts = self._view("counts", torch.int64, (self.k,))
+        self.hlog = (self._view("hlog", torch.int32, (self.history_cap, 2))
+                     if self.history_cap else None)
+        self.hlog_off = self._view("hlog_off", torch.int64, (max(1, self.t_max) + 1,))
         if strategy != "lloyd":
             self.ub = self._view("ub", torch.float32, (self.n,))
             self.lb = self._view("lb", torch.float32, (self.nlb, self.n))
@@ -232,9 +282,32 @@ class DeviceLloyd:
                   "lk_profile_read")
         return ms.value, nl.value
 
-    def run(self, init, *, record_history: bool = True, check_every: int = 1):
+    def capture(self, t: int):
+        """CUDA graphs of one iteration t >= 2 (assign, update).  The
+        iteration index lives on the device, so the same graphs replay every
+        later iteration (single process only: NCCL stays outside)."""
+        torch = _torch()
+        if t < 2 or self.comm is not None:
+            return None
+        with torch.cuda.device(self.dev):
+            ga, gu = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ga):
+                nat.check(self.lib.lk_step_assign(self.ctx, int(t), self.stream_handle()),
+                          "lk_step_assign")
+            with torch.cuda.graph(gu):
+                nat.check(self.lib.lk_step_update(self.ctx, int(t), self.stream_handle()),
+                          "lk_step_update")
+        return ga, gu
+
+    def run(self, init, *, record_history: bool = True, check_every: int = 4,
+            use_graphs: bool = True):
         """Run up to t_max iterations from ``init``; stop after the first with
-        changed == 0 (lloyd.py:169-171).  Returns a dict of host arrays."""
+        changed == 0 (lloyd.py:169-171).  Returns a dict of host arrays.
+
+        Iterations are launched ahead of the stop test (``check_every``):
+        once an iteration reports changed == 0 the device marks the run done
+        and every later kernel returns immediately, so iterations launched
+        past convergence change nothing."""
         torch = _torch()
         self.set_centroids(init)
         T = self.t_max
@@ -243,32 +316,42 @@ class DeviceLloyd:
             res["centroids"] = np.array(init, dtype=np.float64, copy=True)
             res["labels"] = np.full(self.n, -1, dtype=np.int64)
             return res
+        record_history = record_history and self.hlog is not None
         with torch.cuda.device(self.dev):
             stream = torch.cuda.current_stream(self.dev)
-            hist = (torch.empty((T, self.n), dtype=torch.int32, pin_memory=True)
-                    if record_history else None)
             chg = torch.zeros(T, dtype=torch.int64, pin_memory=True)
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
                    torch.cuda.Event(enable_timing=True)) for _ in range(T)]
+            log_parts = []      # (iteration, rows, labels) drained from the device log
+            graphs = None
             iters = T
             converged = False
             checked = 0
             for t in range(1, T + 1):
                 e0, e1, e2 = ev[t - 1]
+                if t == 2 and use_graphs:
+                    graphs = self.capture(2)
                 e0.record(stream)
-                st = self.stream_handle()
-                nat.check(self.lib.lk_step_assign(self.ctx, t, st), "lk_step_assign")
+                if graphs is not None:
+                    graphs[0].replay()
+                else:
+                    nat.check(self.lib.lk_step_assign(self.ctx, t, self.stream_handle()),
+                              "lk_step_assign")
                 if self.comm is not None:
                     import torch.distributed as dist
                     dist.all_reduce(self.delta, group=self.comm)
                 e1.record(stream)
-                nat.check(self.lib.lk_step_update(self.ctx, t, st), "lk_step_update")
+                if graphs is not None:
+                    graphs[1].replay()
+                else:
+                    nat.check(self.lib.lk_step_update(self.ctx, t, self.stream_handle()),
+                              "lk_step_update")
                 e2.record(stream)
-                if hist is not None:
-                    hist[t - 1].copy_(self.labels, non_blocking=True)
                 chg[t - 1].copy_(self.stats[t - 1, nat.STAT["changed_global"]], non_blocking=True)
-                if t % check_every == 0 or t == T:
+                if t % check_every == 0 or t == T or t == 1:
                     stream.synchronize()
+                    if record_history:
+                        self._drain_history(checked, t, log_parts)
                     z = np.nonzero(chg[checked:t].numpy() == 0)[0]
                     if len(z):
                         iters = checked + int(z[0]) + 1
@@ -303,7 +386,21 @@ class DeviceLloyd:
             res["records"] = recs
             res["centroids"] = self.c64.to("cpu").numpy().copy()
             res["labels"] = self.labels.to("cpu").numpy().astype(np.int64)
-            if hist is not None:
-                h = hist[:iters].numpy()
-                res["history"] = [h[t].astype(np.int64) for t in range(iters)]
+            if record_history:
+                res["history"] = LabelHistory(self.n, [p for p in log_parts if p[0] < iters])
         return res
+
+    def _drain_history(self, t0: int, t1: int, parts: list):
+        """Copy the device history log of iterations t0+1..t1 to the host and
+        rewind the log (it holds at most check_every iterations of moves)."""
+        offs = self.hlog_off[t0: t1 + 1].to("cpu").numpy()
+        if np.any(offs < 0):
+            raise nat.NativeError("label-history log overflow")
+        if offs[-1] > 0:
+            log = self.hlog[: offs[-1]].to("cpu").numpy()
+        else:
+            log = np.empty((0, 2), dtype=np.int32)
+        for t in range(t0, t1):
+            seg = log[offs[t - t0]: offs[t - t0 + 1]]
+            parts.append((t, seg[:, 0].astype(np.int64), seg[:, 1].astype(np.int64)))
+        self.hlog_off[t1].zero_()

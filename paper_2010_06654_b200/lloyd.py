@@ -106,7 +106,7 @@ def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: R
     n = x.shape[0]
     init_copy = centers.copy()
     eng = DeviceLloyd(x, k, strategy, t_max, kernel=kernel, device=device, groups=groups,
-                      group_seed=group_seed)
+                      group_seed=group_seed, record_history=record_history)
     try:
         out = eng.run(centers, record_history=record_history)
     finally:
