@@ -350,11 +350,14 @@ class DeviceLloyd:
                 chg[t - 1].copy_(self.stats[t - 1, nat.STAT["changed_global"]], non_blocking=True)
                 if t % check_every == 0 or t == T or t == 1:
                     stream.synchronize()
-                    if record_history:
-                        self._drain_history(checked, t, log_parts)
                     z = np.nonzero(chg[checked:t].numpy() == 0)[0]
+                    t_end = checked + int(z[0]) + 1 if len(z) else t
+                    if record_history:
+                        # iterations launched past convergence were no-ops and
+                        # wrote no log offsets: drain only up to t_end
+                        self._drain_history(checked, t_end, log_parts)
                     if len(z):
-                        iters = checked + int(z[0]) + 1
+                        iters = t_end
                         converged = True
                         break
                     checked = t
