@@ -161,6 +161,12 @@ def cpu_sample_rate(workload: str, strategy: str, warmup: int, steps: int, budge
 def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kernel_tc: bool):
     """Algorithmic units of one kernel class summed over the timed iterations:
     ("flop", F) or ("byte", B).  Per-unit figures are listed in DESIGN.md."""
+    if cls == 7:  # tensor-core candidate pass over the ambiguous rows
+        return "flop", sum(2.0 * r["candidate"] * k * d for r in recs)
+    if cls == 9:  # fp32 rescan of candidate-overflow rows
+        return "flop", sum(2.0 * r["overflow"] * k * d for r in recs)
+    if cls == 8:  # fp64 over <= 16 candidates: 3 fp64 flops per (candidate, dim)
+        return "flop", sum(3.0 * r["candidate"] * 4 * d for r in recs)
     if cls == 0:  # assignment: 2*d flops per (row, centroid) pair evaluated
         rows = sum(n if (strategy == "lloyd" or r["t"] == 1) else r["work"] for r in recs)
         return "flop", 2.0 * rows * k * d
@@ -183,8 +189,9 @@ def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kern
     return "byte", len(recs) * k * d * (8.0 * 5 + 4.0)
 
 
-CLASS_NAMES = {0: "assign", 1: "filter", 2: "recheck", 3: "refine", 4: "update", 5: "group_scan",
-               6: "group_merge"}
+CLASS_NAMES = {0: "assign", 1: "filter", 2: "recheck_fp64", 3: "refine", 4: "update",
+               5: "group_scan", 6: "group_merge", 7: "tc_collect", 8: "cand_recheck",
+               9: "ovf_rescan"}
 
 
 def run_ours(args):
@@ -276,27 +283,34 @@ def run_ours(args):
     converged_in_window = bool(np.any(chg[W:T - 1] == 0))
     recs = [{"t": t + 1, "changed": int(stats[t, 0]), "flagged": int(stats[t, 1]),
              "candidate": int(stats[t, 6]), "ywl": int(stats[t, 9]), "pairs": int(stats[t, 10]),
-             "group_dists": int(stats[t, 4]),
+             "group_dists": int(stats[t, 4]), "overflow": int(stats[t, 8]),
              "active": int(stats[t, 2]), "work": int(stats[t, 3])} for t in range(W, T)]
 
     # profiled pass over the same iterations: per-class device time
     _, _ = trajectory(True)
-    cls_ms = {c: eng.profile_read(c)[0] for c in range(7)}
+    cls_ms = {c: eng.profile_read(c)[0] for c in range(10)}
     eng.profile(False)
     dom = max(cls_ms, key=lambda c: cls_ms[c])
     peaks = load_peaks()
     kind, units = algorithmic_work(dom, gpu_strat, x.shape[0], d, k, recs, False)
     dom_s = cls_ms[dom] / 1e3
+    uses_tc = args.kernel == "tc" or (args.kernel == "auto" and d >= 32)
     if kind == "flop":
-        if dom == 2:
-            peak, pk_src = 37.0, "nominal B200 FP64 (no measured figure)"
+        if dom in (2, 8):
+            peak, pk_src, bound = 37.0, "nominal B200 FP64 (no measured figure)", "compute-fp64"
+        elif uses_tc and dom in (0, 7):
+            peak = peaks["bf16_tflops"] / 2.0 / 3.0
+            pk_src = (f"tensor TF32 = bf16_tflops/2 ({peaks['src']} {peaks['bf16_tflops']}), "
+                      "/3 for the 3xTF32 split")
+            bound = "tensor"
         else:
             peak = N_SMS * FP32_FLOP_PER_SM_CLK * peaks["sm_max_mhz"] * 1e6 / 1e12
             pk_src = f"FP32 SIMT = {N_SMS} SMs x 256 flop/clk x sm_max_mhz ({peaks['src']} clock)"
+            bound = "compute-fp32"
         achieved = units / dom_s / 1e12 if dom_s > 0 else 0.0
-        roof = {"bound": "compute-fp32" if dom != 2 else "compute-fp64", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                "traffic": None, "kernel": CLASS_NAMES[dom], "peak_source": pk_src}
+        roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if peak else None, "traffic": None,
+                "kernel": CLASS_NAMES[dom], "peak_source": pk_src}
     else:
         achieved = units / dom_s / 1e9 if dom_s > 0 else 0.0
         peak = peaks["hbm_gbs"]

@@ -175,8 +175,10 @@ int64_t lk_launch_count(const lk_ctx *ctx);
 
 /* Timing helper for bench.py: total device time (ms) of the kernels of one
  * class recorded with events since the last reset (class: 0 assign/rescan,
- * 1 bound filter, 2 recheck, 3 refine, 4 update, 5 group scans, 6 group
- * merge).  Recording is enabled by lk_profile(ctx, 1). */
+ * 1 bound filter, 2 fp64 full recheck, 3 refine, 4 update, 5 group scans,
+ * 6 group merge, 7 tensor-core candidate collection, 8 fp64 candidate
+ * recheck, 9 fp32 rescan of candidate overflow).  Recording is enabled by
+ * lk_profile(ctx, 1). */
 lk_status lk_profile(lk_ctx *ctx, int32_t enable);
 lk_status lk_profile_read(lk_ctx *ctx, int32_t cls, double *total_ms, int64_t *launches);
 

@@ -609,17 +609,26 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             if (s != LK_OK) return s;
             c->launches += 2;
         }
-        {
-            ProfScope p(c, 2, st);
-            if (use_tc) {
+        if (use_tc) {
+            {
+                ProfScope p(c, 7, st);
                 s = lkh::launch_collect_tc(S, stat, n, c->sms, st);
                 if (s != LK_OK) return s;
+            }
+            {
+                ProfScope p(c, 8, st);
                 s = lkh::launch_recheck_cand(S, stat, n, c->sms, st);
                 if (s != LK_OK) return s;
+            }
+            {
+                ProfScope p(c, 9, st);
                 s = lkh::launch_assign_simt(S, S.ovf, stat + LK_STAT_OVERFLOW, stat, n, c->sms, st);
                 if (s != LK_OK) return s;
-                c->launches += 4;
             }
+            c->launches += 4;
+        }
+        {
+            ProfScope p(c, 2, st);
             s = lkh::launch_recheck(S, stat, n, c->sms, st);
             if (s != LK_OK) return s;
         }
