@@ -158,7 +158,8 @@ def cpu_sample_rate(workload: str, strategy: str, warmup: int, steps: int, budge
 # ---------------------------------------------------------------------------
 
 
-def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kernel_tc: bool):
+def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kernel_tc: bool,
+                     groups: int = 1):
     """Algorithmic units of one kernel class summed over the timed iterations:
     ("flop", F) or ("byte", B).  Per-unit figures are listed in DESIGN.md."""
     if cls == 7:  # tensor-core candidate pass over the ambiguous rows
@@ -172,7 +173,7 @@ def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kern
         return "flop", 2.0 * rows * k * d
     if cls == 1 and strategy in ("yinyang", "elkan"):
         # group filter: label/ub/lb-table traffic + tightened rows + group scans
-        t = r_groups = max(1, recs[0].get("groups", 1))
+        t = max(1, groups)
         return "byte", sum(n * (12.0 + 8.0 * t) + 4.0 * d * r["active"] for r in recs)
     if cls == 1:  # Hamerly filter: label 4 + ub 4 + lb 4 read, ub 4 + lb 4 written,
         # 4 per appended row, + the tightened rows' point (4d)
@@ -292,7 +293,7 @@ def run_ours(args):
     eng.profile(False)
     dom = max(cls_ms, key=lambda c: cls_ms[c])
     peaks = load_peaks()
-    kind, units = algorithmic_work(dom, gpu_strat, x.shape[0], d, k, recs, False)
+    kind, units = algorithmic_work(dom, gpu_strat, x.shape[0], d, k, recs, False, n_groups)
     dom_s = cls_ms[dom] / 1e3
     uses_tc = args.kernel == "tc" or (args.kernel == "auto" and d >= 32)
     if kind == "flop":
