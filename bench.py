@@ -384,7 +384,8 @@ def run_ours(args):
                              "rechecked": [r["flagged"] for r in recs],
                              "candidate_rows": [r["candidate"] for r in recs],
                              "group_rows": [r["ywl"] for r in recs],
-                             "group_scans": [r["pairs"] for r in recs]},
+                             "group_scans": [r["pairs"] for r in recs],
+                             "group_dists": [r["group_dists"] for r in recs]},
         }
         print(json.dumps(line))
     if ws > 1:

@@ -655,7 +655,7 @@ lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
     const bool need_half = c->cfg.strategy != LK_STRAT_LLOYD;
     lk_status s = lkh::launch_update(c->S, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV),
                                      buf<double>(c, B_SSE_PART), need_half, st);
-    c->launches += need_half ? 4 : 2;
+    c->launches += need_half ? 3 : 2;
     return s;
 }
 

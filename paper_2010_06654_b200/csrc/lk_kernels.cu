@@ -287,50 +287,55 @@ __device__ double pw_dist2(const TX* x, const double* c, const int32_t* prog, in
     return st[0];
 }
 
-__global__ void __launch_bounds__(kRcWarps * 32) k_recheck_fp64(DevState S, int64_t* stat) {
+// One block per flagged row: every thread takes k/256 centroids, so the
+// per-thread chain of dependent global loads stays short.
+__device__ __forceinline__ void merge_top2(double& b1, int& j1, double& b2, double ob1, int oj1,
+                                           double ob2) {
+    const bool mine = (b1 < ob1) || (b1 == ob1 && j1 < oj1);
+    if (mine) {
+        b2 = fmin(b2, ob1);
+    } else {
+        b2 = fmin(ob2, b1);
+        b1 = ob1;
+        j1 = oj1;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_recheck_fp64(DevState S, int64_t* stat) {
     if (*S.done) return;
-    extern __shared__ double xsh[];  // [kRcWarps][d]
+    extern __shared__ double xr[];  // [d]
+    __shared__ double rb1[kThreads / 32], rb2[kThreads / 32];
+    __shared__ int rj1[kThreads / 32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* xr = xsh + (int64_t)warp * S.d;
     const int64_t m = stat[LK_STAT_FLAGGED];
-    for (int64_t f = (int64_t)blockIdx.x * kRcWarps + warp; f < m;
-         f += (int64_t)gridDim.x * kRcWarps) {
+    for (int64_t f = blockIdx.x; f < m; f += gridDim.x) {
         const int64_t row = S.flagged[f];
-        __syncwarp();
-        for (int z = lane; z < S.d; z += 32)
+        __syncthreads();
+        for (int z = threadIdx.x; z < S.d; z += kThreads)
             xr[z] = S.X64 ? S.X64[row * S.d + z] : (double)S.X32[row * S.ldx + z];
-        __syncwarp();
+        __syncthreads();
         double b1 = INFINITY, b2 = INFINITY;
         int j1 = 0x7fffffff;
-        for (int j = lane; j < S.k; j += 32) {
+        for (int j = threadIdx.x; j < S.k; j += kThreads) {
             double dd = __dsqrt_rn(pw_dist2(xr, S.C64 + (int64_t)j * S.d, S.pw_prog, S.pw_len));
             if (dd < b1) { b2 = b1; b1 = dd; j1 = j; }
             else b2 = fmin(b2, dd);
         }
-        // warp merge of (b1, j1, b2): lexicographic (value, index) minimum
-        for (int o = 16; o > 0; o >>= 1) {
-            double ob1 = __shfl_xor_sync(LK_FULL_MASK, b1, o);
-            double ob2 = __shfl_xor_sync(LK_FULL_MASK, b2, o);
-            int oj1 = __shfl_xor_sync(LK_FULL_MASK, j1, o);
-            bool mine = (b1 < ob1) || (b1 == ob1 && j1 < oj1);
-            if (mine) {
-                b2 = fmin(b2, ob1);
-            } else {
-                b2 = fmin(ob2, b1);
-                b1 = ob1;
-                j1 = oj1;
-            }
-        }
-        int old = S.labels[row];
-        bool mv = false;
-        if (lane == 0) {
-            mv = (old != j1);
+        // lexicographic (value, index) top-2 merge: warp, then block
+        for (int o = 16; o > 0; o >>= 1)
+            merge_top2(b1, j1, b2, __shfl_xor_sync(LK_FULL_MASK, b1, o),
+                       __shfl_xor_sync(LK_FULL_MASK, j1, o), __shfl_xor_sync(LK_FULL_MASK, b2, o));
+        if (lane == 0) { rb1[warp] = b1; rj1[warp] = j1; rb2[warp] = b2; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kThreads / 32; w++) merge_top2(b1, j1, b2, rb1[w], rj1[w], rb2[w]);
+            const int old = S.labels[row];
             S.labels[row] = j1;
             if (S.strategy != LK_STRAT_LLOYD) {
                 S.ub[row] = __double2float_ru(b1 * (1.0 + 1e-12));
                 write_lb_all(S, row, isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12)));
             }
-            if (mv) {
+            if (old != j1) {
                 unsigned long long p =
                     atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), 1ull);
                 S.moved[p] = make_int2((int)row, old);
@@ -613,6 +618,8 @@ __global__ void __launch_bounds__(1024) k_update_global(DevState S, const double
         *S.iter = t + 1;
         if (changed == 0) *S.done = 1;
     }
+    // s_half is rebuilt by k_half_sep's atomicMin: start from +inf
+    for (int j = tid; j < S.k; j += blockDim.x) S.s_half[j] = INFINITY;
     // group drifts (Yinyang): max drift over each group's members
     if (S.gdrift) {
         __syncthreads();
@@ -790,9 +797,9 @@ lk_status launch_assign_simt(const DevState& S, const int32_t* rowlist, const in
 
 lk_status launch_recheck(const DevState& S, int64_t* stat, int64_t max_rows, int sms,
                          cudaStream_t st) {
-    size_t smem = (size_t)kRcWarps * S.d * sizeof(double);  // <= 48 KB for d <= 1536
-    int grid = grid_for(max_rows, kRcWarps, sms * 8);
-    k_recheck_fp64<<<grid, kRcWarps * 32, smem, st>>>(S, stat);
+    size_t smem = (size_t)S.d * sizeof(double);  // <= 48 KB for d <= 6144
+    int grid = grid_for(max_rows, 1, sms * 2);
+    k_recheck_fp64<<<grid, kThreads, smem, st>>>(S, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
@@ -841,8 +848,6 @@ lk_status launch_update(const DevState& S, const double* qscale, const double* q
     k_update_global<<<1, 1024, 0, st>>>(S, sse_part);
     LK_LAUNCH_CHECK();
     if (need_half) {
-        k_fill_inf<<<(S.k + kThreads - 1) / kThreads, kThreads, 0, st>>>(S);
-        LK_LAUNCH_CHECK();
         dim3 g((S.k + kHsT - 1) / kHsT, (S.k + kHsT - 1) / kHsT);
         k_half_sep<<<g, kThreads, 0, st>>>(S);
         LK_LAUNCH_CHECK();

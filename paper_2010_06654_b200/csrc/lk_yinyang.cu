@@ -26,6 +26,7 @@ namespace lk {
 namespace yy {
 
 constexpr int kThreads = 256;
+constexpr int kYyG = 8;  // lanes per (row, group) scan
 
 // Block-wide exclusive scan of cnt with one global atomic per block.
 // Block-uniform call; scratch >= blockDim/32 + 1 entries.
@@ -197,13 +198,18 @@ __device__ __forceinline__ float dist2_ptr(const float* xp, const float* cp, int
     return acc;
 }
 
-// One thread per (row, group) pair; the group's members are contiguous in Cg
-// (staged in shared memory when all centroids fit).
+// G lanes per (row, group) pair: the group's members are contiguous in Cg
+// (staged in shared memory when all centroids fit) and strided over the G
+// lanes; a G-lane shuffle merges the partial top-2.  Positions ascend with
+// centroid id inside a group, so (value, position) order is (value, id) order.
+template <int G>
 __global__ void __launch_bounds__(kThreads) k_yy_pairs(DevState S, int64_t* stat, int staged) {
     if (*S.done) return;
     extern __shared__ __align__(16) float csm[];
     const int64_t np_ = min((int64_t)stat[LK_STAT_PAIRS], S.pair_cap);
-    if ((int64_t)blockIdx.x * kThreads >= np_) return;
+    constexpr int kPPW = 32 / G;  // pairs per warp
+    constexpr int kWarps = kThreads / 32;
+    if ((int64_t)blockIdx.x * kWarps * kPPW >= np_) return;
     const float* cbase = S.Cg;
     if (staged) {
         const int tot = S.k * S.ldc;
@@ -211,23 +217,27 @@ __global__ void __launch_bounds__(kThreads) k_yy_pairs(DevState S, int64_t* stat
         __syncthreads();
         cbase = csm;
     }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane % G, slot = lane / G;
     const bool vec4 = (S.ldc & 3) == 0 && (S.ldx & 3) == 0;
     int64_t ndist = 0;
-    for (int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x; p < np_;
-         p += (int64_t)gridDim.x * kThreads) {
-        const int2 pr = S.ypairs[p];
-        if (pr.y < 0) continue;
+    for (int64_t pb = ((int64_t)blockIdx.x * kWarps + warp) * kPPW; pb < np_;
+         pb += (int64_t)gridDim.x * kWarps * kPPW) {
+        const int64_t p = pb + slot;
+        int2 pr = make_int2(0, -1);
+        if (p < np_) pr = S.ypairs[p];
+        const bool valid = pr.y >= 0;
         const int64_t row = pr.x;
-        const int g = pr.y & 0xFFFF, apos = pr.y >> 16;
+        const int g = valid ? (pr.y & 0xFFFF) : 0, apos = pr.y >> 16;
+        const int j0 = valid ? S.goff[g] : 0, j9 = valid ? S.goff[g + 1] : 0;
         const float* xp = S.X32 + row * S.ldx;
-        float xr[4];
         float b1 = INFINITY, b2 = INFINITY;
-        int p1 = -1;
-        const int j0 = S.goff[g], j9 = S.goff[g + 1];
+        int p1 = 0x7fffffff;
         if (S.d <= 4) {
+            float xr[4];
 #pragma unroll
-            for (int z = 0; z < 4; z++) xr[z] = z < S.d ? __ldg(xp + z) : 0.f;
-            for (int jj = j0; jj < j9; jj++) {
+            for (int z = 0; z < 4; z++) xr[z] = (valid && z < S.d) ? __ldg(xp + z) : 0.f;
+            for (int jj = j0 + sub; jj < j9; jj += G) {
                 if (jj == apos) continue;  // the label competes via the tightened bound
                 const float* cp = cbase + (int64_t)jj * S.ldc;
                 float acc = 0.f;
@@ -242,17 +252,30 @@ __global__ void __launch_bounds__(kThreads) k_yy_pairs(DevState S, int64_t* stat
                 else b2 = fminf(b2, acc);
             }
         } else {
-            for (int jj = j0; jj < j9; jj++) {
+            for (int jj = j0 + sub; jj < j9; jj += G) {
                 if (jj == apos) continue;
                 const float acc = dist2_ptr(xp, cbase + (int64_t)jj * S.ldc, S.d, vec4);
                 if (acc < b1) { b2 = b1; b1 = acc; p1 = jj; }
                 else b2 = fminf(b2, acc);
             }
         }
-        ndist += (j9 - j0) - (apos >= j0 && apos < j9 ? 1 : 0);
-        // positions ascend with centroid id inside a group, so the first
-        // strict minimum is also the lowest centroid id among equal values
-        S.yres[p] = make_float4(__int_as_float(p1 >= 0 ? S.gperm[p1] : -1), b1, b2, 0.f);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            const float ob1 = __shfl_xor_sync(LK_FULL_MASK, b1, o, G);
+            const float ob2 = __shfl_xor_sync(LK_FULL_MASK, b2, o, G);
+            const int op1 = __shfl_xor_sync(LK_FULL_MASK, p1, o, G);
+            if (ob1 < b1 || (ob1 == b1 && op1 < p1)) {
+                b2 = fminf(b1, ob2);
+                b1 = ob1;
+                p1 = op1;
+            } else {
+                b2 = fminf(b2, ob1);
+            }
+        }
+        if (valid && sub == 0) {
+            ndist += (j9 - j0) - (apos >= j0 && apos < j9 ? 1 : 0);
+            S.yres[p] = make_float4(__int_as_float(p1 < 0x7fffffff ? S.gperm[p1] : -1), b1, b2, 0.f);
+        }
     }
     warp_add(ndist, stat + LK_STAT_DIST);
 }
@@ -350,7 +373,7 @@ static int grid_for_rows(int64_t rows, int sms, int per_sm) {
 }
 
 lk_status init_yy_attributes() {
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_pairs<kYyG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        96 * 1024));
     LK_CUDA_CHECK(cudaFuncSetAttribute(k_filter_yinyang, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        64 * 1024));
@@ -367,7 +390,7 @@ lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaSt
 lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     const size_t csm = (size_t)S.k * S.ldc * sizeof(float);
     const int staged = csm <= 96 * 1024;
-    k_yy_pairs<<<sms * (staged ? 2 : 8), kThreads, staged ? csm : 0, st>>>(S, stat, staged);
+    k_yy_pairs<kYyG><<<sms * (staged ? 4 : 8), kThreads, staged ? csm : 0, st>>>(S, stat, staged);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
