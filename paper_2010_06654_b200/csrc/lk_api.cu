@@ -57,6 +57,8 @@ static bool is_group_strategy(int s) {
 
 static uint64_t align256(uint64_t v) { return (v + 255) & ~uint64_t(255); }
 
+static bool is_group_strategy(int s);
+
 static int32_t nlb_for(const lk_config& c, int32_t* groups) {
     int32_t g = 1;
     switch (c.strategy) {
@@ -66,6 +68,9 @@ static int32_t nlb_for(const lk_config& c, int32_t* groups) {
         default: g = c.groups > 0 ? c.groups : (c.k + 9) / 10; break;
     }
     if (g > c.k) g = c.k;
+    // the warp-per-row Yinyang path works on 8/16/32 group slots; extra slots
+    // are empty groups (no members, never binding)
+    if (is_group_strategy(c.strategy) && g <= 32 && c.d <= 32) g = g <= 8 ? 8 : (g <= 16 ? 16 : 32);
     *groups = g;
     return g < 1 ? 1 : g;
 }

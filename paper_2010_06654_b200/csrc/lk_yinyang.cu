@@ -177,6 +177,239 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_yinyang(DevState S, int6
     }
 }
 
+// ---------------------------------------------------------------------------
+// Specialised path for T <= 32 groups: the filter emits one worklist entry per
+// failing row with a bitmask of the groups to scan; one warp then scans those
+// groups for that row (lane g keeps group g's result), certifies the label and
+// rewrites the bounds.  No pair list, no second pass.
+
+// Block-wide: counts of two predicates appended to two worklists + a plain
+// count, with one global atomic per counter per block.  Block-uniform call.
+__device__ __forceinline__ void block_append2(bool pa, bool pb, unsigned long long* ca,
+                                              unsigned long long* cb, int64_t* cact, bool act,
+                                              unsigned long long* scr, int64_t& posa,
+                                              int64_t& posb) {
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned ma = __ballot_sync(LK_FULL_MASK, pa), mb = __ballot_sync(LK_FULL_MASK, pb),
+                   mc = __ballot_sync(LK_FULL_MASK, act);
+    if (lane_id() == 0) {
+        scr[warp] = __popc(ma);
+        scr[nw + warp] = __popc(mb);
+        scr[2 * nw + warp] = __popc(mc);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long ta = 0, tb = 0, tc = 0;
+        for (int w = 0; w < nw; w++) {
+            unsigned long long a = scr[w], b = scr[nw + w];
+            scr[w] = ta;
+            scr[nw + w] = tb;
+            ta += a;
+            tb += b;
+            tc += scr[2 * nw + w];
+        }
+        scr[3 * nw] = ta ? atomicAdd(ca, ta) : 0ull;
+        scr[3 * nw + 1] = tb ? atomicAdd(cb, tb) : 0ull;
+        if (tc) atomicAdd((unsigned long long*)cact, tc);
+    }
+    __syncthreads();
+    const unsigned lt = lanemask_lt();
+    posa = pa ? (int64_t)(scr[3 * nw] + scr[warp] + __popc(ma & lt)) : -1;
+    posb = pb ? (int64_t)(scr[3 * nw + 1] + scr[nw + warp] + __popc(mb & lt)) : -1;
+    __syncthreads();
+}
+
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    __shared__ float gd[T];
+    __shared__ unsigned long long scr[3 * (kThreads / 32) + 2];
+    if (threadIdx.x < T) gd[threadIdx.x] = S.gdrift[threadIdx.x];
+    __syncthreads();
+    const float rho = simt_rel_err(S.d);
+    const int64_t ln = S.n;
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < S.n;
+         base += (int64_t)gridDim.x * kThreads) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < S.n;
+        bool active = false, need = false;
+        unsigned mask = 0;
+        float acc_a = 0.f, u = 0.f, lun = INFINITY, xn = 0.f;
+        if (valid) {
+            const int a = S.labels[i];
+            u = __fadd_ru(S.ub[i], S.drift[a]);
+            float v[T];
+            const float* lp = S.lb + i;
+#pragma unroll
+            for (int g = 0; g < T; g++) v[g] = __ldcs(lp + g * ln);
+            float gmin = INFINITY;
+            float* sp = S.lb + i;
+#pragma unroll
+            for (int g = 0; g < T; g++) {
+                v[g] = fmaxf(__fsub_rd(v[g], gd[g]), 0.f);
+                gmin = fminf(gmin, v[g]);
+                __stcs(sp + g * ln, v[g]);
+            }
+            // Hamerly's separation test holds for every bound family
+            gmin = fmaxf(gmin, S.s_half[a]);
+            if (!(gmin > u)) {
+                active = true;
+                const float* xp = S.X32 + i * S.ldx;
+                acc_a = dist2_row(S, xp, a);
+                xn = xnorm(S, xp);
+                const float U = (sqrtf(acc_a) + kU32 * (xn + S.cnorm[a])) * (1.0f + rho);
+                u = fminf(u, U);
+                need = !(gmin > u);
+                if (need) {
+#pragma unroll
+                    for (int g = 0; g < T; g++) {
+                        if (v[g] > u) lun = fminf(lun, v[g]);
+                        else mask |= 1u << g;
+                    }
+                }
+            }
+            S.ub[i] = u;
+        }
+        int64_t wpos, unused;
+        block_append2(need, false, (unsigned long long*)(stat + LK_STAT_YWL),
+                      (unsigned long long*)(stat + LK_STAT_PAIRS), stat + LK_STAT_ACTIVE, active,
+                      scr, wpos, unused);
+        if (need) {
+            S.ywl[wpos] = make_int4((int)i, (int)mask, __float_as_int(acc_a), __float_as_int(xn));
+            S.ylun[wpos] = make_float2(lun, 0.f);
+        }
+    }
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat, int staged) {
+    if (*S.done) return;
+    extern __shared__ __align__(16) float csm[];
+    __shared__ unsigned long long scr[kThreads / 32 + 1];
+    const int64_t m = stat[LK_STAT_YWL];
+    constexpr int kWarps = kThreads / 32;
+    if ((int64_t)blockIdx.x * kWarps >= m) return;
+    const float* cbase = S.Cg;
+    if (staged) {
+        const int tot = S.k * S.ldc;
+        for (int e = threadIdx.x; e < tot; e += kThreads) csm[e] = S.Cg[e];
+        __syncthreads();
+        cbase = csm;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float rho = simt_rel_err(S.d);
+    const float cmax = S.scal[0];
+    const int64_t ln = S.n;
+    int64_t ndist = 0;
+    for (int64_t base = (int64_t)blockIdx.x * kWarps; base < m;
+         base += (int64_t)gridDim.x * kWarps) {
+        const int64_t e = base + warp;
+        const bool valid = e < m;
+        int4 w = make_int4(0, 0, 0, 0);
+        if (valid) w = S.ywl[e];
+        const int64_t row = w.x;
+        const unsigned mask = (unsigned)w.y;
+        const float acc_a = __int_as_float(w.z), xn = __int_as_float(w.w);
+        const int old = valid ? S.labels[row] : 0;
+        const int apos = valid ? S.ginv[old] : -1;
+        float xr[DP];
+        const float* xp = S.X32 + row * S.ldx;
+#pragma unroll
+        for (int z = 0; z < DP; z++) xr[z] = (valid && z < S.d) ? __ldg(xp + z) : 0.f;
+        // best over the label (tightened distance) and the scanned groups
+        float bestD = acc_a, secD = INFINITY;
+        int bestJ = old;
+        float myg1 = INFINITY, myg2 = INFINITY;  // lane g: group g's top-2
+        int myj1 = -1;
+        unsigned mm = mask;
+        while (mm) {  // warp-uniform: mask is the same on every lane
+            const int g = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const int j0 = S.goff[g], j9 = S.goff[g + 1];
+            float b1 = INFINITY, b2 = INFINITY;
+            int p1 = 0x7fffffff;
+            for (int jj = j0 + lane; jj < j9; jj += 32) {
+                if (jj == apos) continue;
+                const float* cp = cbase + (int64_t)jj * S.ldc;
+                float acc = 0.f;
+#pragma unroll
+                for (int z = 0; z < DP; z++) {
+                    // rows of Cg are zero-padded to ldc >= DP for DP <= 8
+                    if (DP <= 8 || z < S.d) {
+                        const float t = xr[z] - cp[z];
+                        acc = fmaf(t, t, acc);
+                    }
+                }
+                if (acc < b1) { b2 = b1; b1 = acc; p1 = jj; }
+                else b2 = fminf(b2, acc);
+            }
+            ndist += (lane == 0) ? (j9 - j0) - (apos >= j0 && apos < j9 ? 1 : 0) : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ob1 = __shfl_xor_sync(LK_FULL_MASK, b1, o);
+                const float ob2 = __shfl_xor_sync(LK_FULL_MASK, b2, o);
+                const int op1 = __shfl_xor_sync(LK_FULL_MASK, p1, o);
+                if (ob1 < b1 || (ob1 == b1 && op1 < p1)) {
+                    b2 = fminf(b1, ob2);
+                    b1 = ob1;
+                    p1 = op1;
+                } else {
+                    b2 = fminf(b2, ob1);
+                }
+            }
+            const int gj = p1 < 0x7fffffff ? S.gperm[p1] : -1;
+            if (lane == g) { myg1 = b1; myg2 = b2; myj1 = gj; }
+            if (gj >= 0) {
+                if (b1 < bestD || (b1 == bestD && gj < bestJ)) {
+                    secD = fminf(secD, bestD);
+                    bestD = b1;
+                    bestJ = gj;
+                } else {
+                    secD = fminf(secD, b1);
+                }
+            }
+            secD = fminf(secD, b2);
+        }
+        bool mv = false, flag = false;
+        if (valid) {
+            const float lun = S.ylun[e].x;
+            const float U1 = (sqrtf(bestD) + kU32 * (xn + S.cnorm[bestJ])) * (1.0f + rho);
+            const float Ls = isinf(secD) ? INFINITY
+                                         : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
+            const float L2 = fminf(Ls, lun);
+            if (L2 > U1) {
+                mv = bestJ != old;
+                float* lbr = S.lb + row;
+                if (lane < 32 && ((mask >> lane) & 1u)) {
+                    const float gm = (myj1 == bestJ) ? myg2 : myg1;
+                    lbr[(int64_t)lane * ln] =
+                        isinf(gm) ? INFINITY
+                                  : fmaxf((sqrtf(gm) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    S.labels[row] = bestJ;
+                    S.ub[row] = U1;
+                    if (mv) {
+                        // the old label becomes an "other" member of its group
+                        const int go = S.group_of[old];
+                        const float la =
+                            fmaxf((sqrtf(acc_a) - kU32 * (xn + S.cnorm[old])) * (1.0f - rho), 0.f);
+                        lbr[go * ln] = fminf(lbr[go * ln], la);
+                    }
+                }
+            } else {
+                flag = true;
+            }
+        }
+        int64_t pos = block_append(mv && lane == 0, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
+        if (mv && lane == 0) S.moved[pos] = make_int2((int)row, old);
+        int64_t fpos = block_append(flag && lane == 0, (unsigned long long*)(stat + LK_STAT_FLAGGED), scr);
+        if (flag && lane == 0) S.flagged[fpos] = (int)row;
+    }
+    warp_add(ndist, stat + LK_STAT_DIST);
+}
+
 __device__ __forceinline__ float dist2_ptr(const float* xp, const float* cp, int d, bool vec4) {
     float acc = 0.f;
     int z = 0;
@@ -373,6 +606,11 @@ static int grid_for_rows(int64_t rows, int sms, int per_sm) {
 }
 
 lk_status init_yy_attributes() {
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_pairs<kYyG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        96 * 1024));
     LK_CUDA_CHECK(cudaFuncSetAttribute(k_filter_yinyang, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -380,7 +618,30 @@ lk_status init_yy_attributes() {
     return LK_OK;
 }
 
+bool yy_masked(const lk::DevState& S) { return S.t_groups <= 32 && S.d <= 32; }
+
+template <int T>
+static void launch_filter_m(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    k_filter_yinyang_m<T><<<grid_for_rows(S.n, sms, 8), kThreads, 0, st>>>(S, stat);
+}
+
+template <int DP>
+static void launch_scan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    const size_t csm = (size_t)S.k * S.ldc * sizeof(float);
+    const int staged = csm <= 96 * 1024;
+    k_yy_scan<DP><<<sms * 8, kThreads, staged ? csm : 0, st>>>(S, stat, staged);
+}
+
 lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    if (yy_masked(S)) {
+        // the group count is padded (with +inf bounds) up to a template size
+        const int t = S.t_groups;
+        if (t <= 8) launch_filter_m<8>(S, stat, sms, st);
+        else if (t <= 16) launch_filter_m<16>(S, stat, sms, st);
+        else launch_filter_m<32>(S, stat, sms, st);
+        LK_LAUNCH_CHECK();
+        return LK_OK;
+    }
     const size_t smem = (size_t)S.t_groups * sizeof(float);  // <= 64 KB (k <= 16384)
     k_filter_yinyang<<<grid_for_rows(S.n, sms, 8), kThreads, smem, st>>>(S, stat);
     LK_LAUNCH_CHECK();
@@ -388,6 +649,16 @@ lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaSt
 }
 
 lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    if (yy_masked(S)) {
+        const int d = S.d;
+        if (d <= 2) launch_scan<2>(S, stat, sms, st);
+        else if (d <= 4) launch_scan<4>(S, stat, sms, st);
+        else if (d <= 8) launch_scan<8>(S, stat, sms, st);
+        else if (d <= 16) launch_scan<16>(S, stat, sms, st);
+        else launch_scan<32>(S, stat, sms, st);
+        LK_LAUNCH_CHECK();
+        return LK_OK;
+    }
     const size_t csm = (size_t)S.k * S.ldc * sizeof(float);
     const int staged = csm <= 96 * 1024;
     k_yy_pairs<kYyG><<<sms * (staged ? 4 : 8), kThreads, staged ? csm : 0, st>>>(S, stat, staged);
@@ -396,6 +667,7 @@ lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStr
 }
 
 lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    if (yy_masked(S)) return LK_OK;  // merged into k_yy_scan
     k_yy_merge<<<grid_for_rows(S.n, sms, 4), kThreads, 0, st>>>(S, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;

@@ -130,6 +130,7 @@ class DeviceLloyd:
         self.comm = comm
         self.strategy = strategy
         self.group_seed = group_seed
+        self.groups_req = int(groups)
         self.k = int(k)
         self.t_max = int(t_max)
 
@@ -251,7 +252,8 @@ class DeviceLloyd:
     def set_centroids(self, init):
         torch = _torch()
         if self.strategy in GROUP_STRATEGIES:
-            self.set_groups(group_centroids(np.asarray(init, dtype=np.float64), self.nlb,
+            t = min(self.groups_req, self.nlb) if self.groups_req > 0 else self.nlb
+            self.set_groups(group_centroids(np.asarray(init, dtype=np.float64), t,
                                             seed=self.group_seed))
         with torch.cuda.device(self.dev):
             c = torch.as_tensor(np.ascontiguousarray(init, dtype=np.float64)) \
