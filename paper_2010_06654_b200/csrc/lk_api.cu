@@ -574,7 +574,13 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
     const bool use_tc = lkh::tc_supported(S);
     lk_status s;
     if (n > 0) {
-        if (c->cfg.strategy == LK_STRAT_LLOYD || t == 1) {
+        if (t == 1 && is_group_strategy(c->cfg.strategy) && lkh::yy_masked(S) && !use_tc) {
+            // group-order full scan that also seeds exact per-group bounds
+            ProfScope p(c, 0, st);
+            s = lkh::launch_yy_seed(S, stat, c->sms, st);
+            if (s != LK_OK) return s;
+            c->launches += 1;
+        } else if (c->cfg.strategy == LK_STRAT_LLOYD || t == 1) {
             ProfScope p(c, 0, st);
             s = use_tc ? lkh::launch_assign_tc(S, nullptr, nullptr, stat, n, c->sms, st)
                        : lkh::launch_assign_simt(S, nullptr, nullptr, stat, n, c->sms, st);

@@ -24,6 +24,8 @@ lk_status init_tc_attributes();
 lk_status init_yy_attributes();
 lk_status launch_scan_exp(const lk::DevState& S, int sms, cudaStream_t st);
 
+bool yy_masked(const lk::DevState& S);
+lk_status launch_yy_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);

@@ -282,20 +282,36 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64
 }
 
 template <int DP>
-__global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat, int staged) {
+__device__ __forceinline__ float dist2_dp(const float (&xr)[DP], const float* cp, int d) {
+    float acc = 0.f;
+#pragma unroll
+    for (int z = 0; z < DP; z++) {
+        // rows of Cg are zero-padded to ldc >= DP for DP <= 8
+        if (DP <= 8 || z < d) {
+            const float t = xr[z] - cp[z];
+            acc = fmaf(t, t, acc);
+        }
+    }
+    return acc;
+}
+
+// STAGED: all centroids (group order) live in shared memory -> LDS with
+// 32-bit addressing; otherwise they are read from L2 through the read-only path.
+template <int DP, bool STAGED>
+__global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat) {
     if (*S.done) return;
     extern __shared__ __align__(16) float csm[];
     __shared__ unsigned long long scr[kThreads / 32 + 1];
     const int64_t m = stat[LK_STAT_YWL];
     constexpr int kWarps = kThreads / 32;
     if ((int64_t)blockIdx.x * kWarps >= m) return;
-    const float* cbase = S.Cg;
-    if (staged) {
+    if (STAGED) {
         const int tot = S.k * S.ldc;
         for (int e = threadIdx.x; e < tot; e += kThreads) csm[e] = S.Cg[e];
         __syncthreads();
-        cbase = csm;
     }
+    const float* __restrict__ cg = STAGED ? csm : S.Cg;
+    const int ldc = S.ldc;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float rho = simt_rel_err(S.d);
     const float cmax = S.scal[0];
@@ -316,7 +332,6 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat,
         const float* xp = S.X32 + row * S.ldx;
 #pragma unroll
         for (int z = 0; z < DP; z++) xr[z] = (valid && z < S.d) ? __ldg(xp + z) : 0.f;
-        // best over the label (tightened distance) and the scanned groups
         float bestD = acc_a, secD = INFINITY;
         int bestJ = old;
         float myg1 = INFINITY, myg2 = INFINITY;  // lane g: group g's top-2
@@ -329,17 +344,8 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat,
             float b1 = INFINITY, b2 = INFINITY;
             int p1 = 0x7fffffff;
             for (int jj = j0 + lane; jj < j9; jj += 32) {
-                if (jj == apos) continue;
-                const float* cp = cbase + (int64_t)jj * S.ldc;
-                float acc = 0.f;
-#pragma unroll
-                for (int z = 0; z < DP; z++) {
-                    // rows of Cg are zero-padded to ldc >= DP for DP <= 8
-                    if (DP <= 8 || z < S.d) {
-                        const float t = xr[z] - cp[z];
-                        acc = fmaf(t, t, acc);
-                    }
-                }
+                float acc = dist2_dp<DP>(xr, cg + jj * ldc, S.d);
+                acc = (jj == apos) ? INFINITY : acc;  // the label competes via its tightened bound
                 if (acc < b1) { b2 = b1; b1 = acc; p1 = jj; }
                 else b2 = fminf(b2, acc);
             }
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat,
                     b2 = fminf(b2, ob1);
                 }
             }
-            const int gj = p1 < 0x7fffffff ? S.gperm[p1] : -1;
+            const int gj = (p1 < 0x7fffffff && !isinf(b1)) ? S.gperm[p1] : -1;
             if (lane == g) { myg1 = b1; myg2 = b2; myj1 = gj; }
             if (gj >= 0) {
                 if (b1 < bestD || (b1 == bestD && gj < bestJ)) {
@@ -380,7 +386,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat,
             if (L2 > U1) {
                 mv = bestJ != old;
                 float* lbr = S.lb + row;
-                if (lane < 32 && ((mask >> lane) & 1u)) {
+                if ((mask >> lane) & 1u) {
                     const float gm = (myj1 == bestJ) ? myg2 : myg1;
                     lbr[(int64_t)lane * ln] =
                         isinf(gm) ? INFINITY
@@ -408,6 +414,85 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat,
         if (flag && lane == 0) S.flagged[fpos] = (int)row;
     }
     warp_add(ndist, stat + LK_STAT_DIST);
+}
+
+// Iteration 1 of the group strategies (SequentialStrategy.seed +
+// Yinyang._seed_state, pruners.py:83-87 / :398-416): a full scan in group
+// order that also leaves the exact per-group minima (excluding the winner) as
+// the group bounds, so iteration 2 starts from tight bounds.
+template <int DP, bool STAGED>
+__global__ void __launch_bounds__(kThreads) k_seed_yinyang(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    extern __shared__ __align__(16) float csm[];
+    __shared__ unsigned long long scr[kThreads / 32 + 1];
+    if (STAGED) {
+        const int tot = S.k * S.ldc;
+        for (int e = threadIdx.x; e < tot; e += kThreads) csm[e] = S.Cg[e];
+        __syncthreads();
+    }
+    const float* __restrict__ cg = STAGED ? csm : S.Cg;
+    const int ldc = S.ldc, T = S.t_groups;
+    const float rho = simt_rel_err(S.d);
+    const int64_t ln = S.n;
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < S.n;
+         base += (int64_t)gridDim.x * kThreads) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < S.n;
+        float xr[DP];
+        const float* xp = S.X32 + i * S.ldx;
+        float xn2 = 0.f;
+#pragma unroll
+        for (int z = 0; z < DP; z++) {
+            xr[z] = (valid && z < S.d) ? __ldg(xp + z) : 0.f;
+            xn2 = fmaf(xr[z], xr[z], xn2);
+        }
+        const float xn = sqrtf(xn2);
+        const float cmax = S.scal[0];
+        float bestD = INFINITY, secD = INFINITY, bestg2 = INFINITY;
+        int bestP = 0, bestG = 0;
+        for (int g = 0; g < T; g++) {
+            const int j0 = S.goff[g], j9 = S.goff[g + 1];
+            float b1 = INFINITY, b2 = INFINITY;
+            int p1 = j0;
+            for (int jj = j0; jj < j9; jj++) {
+                const float acc = dist2_dp<DP>(xr, cg + jj * ldc, S.d);
+                if (acc < b1) { b2 = b1; b1 = acc; p1 = jj; }
+                else b2 = fminf(b2, acc);
+            }
+            if (valid && j9 > j0)
+                S.lb[(int64_t)g * ln + i] =
+                    fmaxf((sqrtf(b1) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
+            else if (valid)
+                S.lb[(int64_t)g * ln + i] = INFINITY;
+            if (b1 < bestD) {
+                secD = fminf(secD, bestD);
+                bestD = b1; bestP = p1; bestG = g; bestg2 = b2;
+            } else {
+                secD = fminf(secD, b1);
+            }
+            secD = fminf(secD, b2);
+        }
+        const int j1 = S.gperm[bestP];
+        const float U1 = (sqrtf(bestD) + kU32 * (xn + S.cnorm[j1])) * (1.0f + rho);
+        const float L2 = isinf(secD) ? INFINITY : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
+        const bool certain = valid && L2 > U1;
+        const bool flag = valid && !certain;
+        bool moved = false;
+        int old = 0;
+        if (certain) {
+            old = S.labels[i];
+            moved = old != j1;
+            S.labels[i] = j1;
+            S.ub[i] = U1;
+            S.lb[(int64_t)bestG * ln + i] =
+                isinf(bestg2) ? INFINITY
+                              : fmaxf((sqrtf(bestg2) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
+        }
+        int64_t pos = block_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
+        if (moved) S.moved[pos] = make_int2((int)i, old);
+        int64_t fpos = block_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED), scr);
+        if (flag) S.flagged[fpos] = (int)i;
+    }
 }
 
 __device__ __forceinline__ float dist2_ptr(const float* xp, const float* cp, int d, bool vec4) {
@@ -606,11 +691,19 @@ static int grid_for_rows(int64_t rows, int sms, int per_sm) {
 }
 
 lk_status init_yy_attributes() {
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_scan<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+#define LK_SMEM96(kern) \
+    LK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024))
+    LK_SMEM96((k_yy_scan<2, true>));
+    LK_SMEM96((k_yy_scan<4, true>));
+    LK_SMEM96((k_yy_scan<8, true>));
+    LK_SMEM96((k_yy_scan<16, true>));
+    LK_SMEM96((k_yy_scan<32, true>));
+    LK_SMEM96((k_seed_yinyang<2, true>));
+    LK_SMEM96((k_seed_yinyang<4, true>));
+    LK_SMEM96((k_seed_yinyang<8, true>));
+    LK_SMEM96((k_seed_yinyang<16, true>));
+    LK_SMEM96((k_seed_yinyang<32, true>));
+#undef LK_SMEM96
     LK_CUDA_CHECK(cudaFuncSetAttribute(k_yy_pairs<kYyG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        96 * 1024));
     LK_CUDA_CHECK(cudaFuncSetAttribute(k_filter_yinyang, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -628,8 +721,31 @@ static void launch_filter_m(const lk::DevState& S, int64_t* stat, int sms, cudaS
 template <int DP>
 static void launch_scan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     const size_t csm = (size_t)S.k * S.ldc * sizeof(float);
-    const int staged = csm <= 96 * 1024;
-    k_yy_scan<DP><<<sms * 8, kThreads, staged ? csm : 0, st>>>(S, stat, staged);
+    if (csm <= 96 * 1024)
+        k_yy_scan<DP, true><<<sms * 8, kThreads, csm, st>>>(S, stat);
+    else
+        k_yy_scan<DP, false><<<sms * 8, kThreads, 0, st>>>(S, stat);
+}
+
+template <int DP>
+static void launch_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    const size_t csm = (size_t)S.k * S.ldc * sizeof(float);
+    const int grid = grid_for_rows(S.n, sms, 6);
+    if (csm <= 96 * 1024)
+        k_seed_yinyang<DP, true><<<grid, kThreads, csm, st>>>(S, stat);
+    else
+        k_seed_yinyang<DP, false><<<grid, kThreads, 0, st>>>(S, stat);
+}
+
+lk_status launch_yy_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    const int d = S.d;
+    if (d <= 2) launch_seed<2>(S, stat, sms, st);
+    else if (d <= 4) launch_seed<4>(S, stat, sms, st);
+    else if (d <= 8) launch_seed<8>(S, stat, sms, st);
+    else if (d <= 16) launch_seed<16>(S, stat, sms, st);
+    else launch_seed<32>(S, stat, sms, st);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
 }
 
 lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
