@@ -305,29 +305,50 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat)
     const int64_t m = stat[LK_STAT_YWL];
     constexpr int kWarps = kThreads / 32;
     if ((int64_t)blockIdx.x * kWarps >= m) return;
+    // STAGED: centroids in group order plus the small per-centroid tables
+    // (group ranges, permutation, inverse, norms, group of) live in shared
+    // memory, so a row's dependent chain touches global memory only for its
+    // own worklist entry, label and coordinates.
+    const int k = S.k, T = S.t_groups;
+    float* s_cn = csm + k * S.ldc;
+    int* s_goff = reinterpret_cast<int*>(s_cn + k);
+    int* s_gperm = s_goff + T + 1;
+    int* s_ginv = s_gperm + k;
+    int* s_gof = s_ginv + k;
     if (STAGED) {
-        const int tot = S.k * S.ldc;
+        const int tot = k * S.ldc;
         for (int e = threadIdx.x; e < tot; e += kThreads) csm[e] = S.Cg[e];
+        for (int e = threadIdx.x; e < k; e += kThreads) {
+            s_cn[e] = S.cnorm[e];
+            s_gperm[e] = S.gperm[e];
+            s_ginv[e] = S.ginv[e];
+            s_gof[e] = S.group_of[e];
+        }
+        for (int e = threadIdx.x; e <= T; e += kThreads) s_goff[e] = S.goff[e];
         __syncthreads();
     }
     const float* __restrict__ cg = STAGED ? csm : S.Cg;
+    const float* __restrict__ cnm = STAGED ? s_cn : S.cnorm;
+    const int* __restrict__ goff = STAGED ? s_goff : S.goff;
+    const int* __restrict__ gperm = STAGED ? s_gperm : S.gperm;
+    const int* __restrict__ ginv = STAGED ? s_ginv : S.ginv;
+    const int* __restrict__ gof = STAGED ? s_gof : S.group_of;
     const int ldc = S.ldc;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float rho = simt_rel_err(S.d);
     const float cmax = S.scal[0];
     const int64_t ln = S.n;
     int64_t ndist = 0;
-    for (int64_t base = (int64_t)blockIdx.x * kWarps; base < m;
-         base += (int64_t)gridDim.x * kWarps) {
-        const int64_t e = base + warp;
-        const bool valid = e < m;
-        int4 w = make_int4(0, 0, 0, 0);
-        if (valid) w = S.ywl[e];
+    // warps pull rows independently (dynamic: rows differ in scanned groups)
+    for (int64_t e0 = (int64_t)blockIdx.x * kWarps + warp; e0 < m; e0 += (int64_t)gridDim.x * kWarps) {
+        const int64_t e = e0;
+        const bool valid = true;
+        const int4 w = S.ywl[e];
         const int64_t row = w.x;
         const unsigned mask = (unsigned)w.y;
         const float acc_a = __int_as_float(w.z), xn = __int_as_float(w.w);
         const int old = valid ? S.labels[row] : 0;
-        const int apos = valid ? S.ginv[old] : -1;
+        const int apos = valid ? ginv[old] : -1;
         float xr[DP];
         const float* xp = S.X32 + row * S.ldx;
 #pragma unroll
@@ -340,7 +361,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat)
         while (mm) {  // warp-uniform: mask is the same on every lane
             const int g = __ffs(mm) - 1;
             mm &= mm - 1;
-            const int j0 = S.goff[g], j9 = S.goff[g + 1];
+            const int j0 = goff[g], j9 = goff[g + 1];
             float b1 = INFINITY, b2 = INFINITY;
             int p1 = 0x7fffffff;
             for (int jj = j0 + lane; jj < j9; jj += 32) {
@@ -363,7 +384,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat)
                     b2 = fminf(b2, ob1);
                 }
             }
-            const int gj = (p1 < 0x7fffffff && !isinf(b1)) ? S.gperm[p1] : -1;
+            const int gj = (p1 < 0x7fffffff && !isinf(b1)) ? gperm[p1] : -1;
             if (lane == g) { myg1 = b1; myg2 = b2; myj1 = gj; }
             if (gj >= 0) {
                 if (b1 < bestD || (b1 == bestD && gj < bestJ)) {
@@ -379,7 +400,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat)
         bool mv = false, flag = false;
         if (valid) {
             const float lun = S.ylun[e].x;
-            const float U1 = (sqrtf(bestD) + kU32 * (xn + S.cnorm[bestJ])) * (1.0f + rho);
+            const float U1 = (sqrtf(bestD) + kU32 * (xn + cnm[bestJ])) * (1.0f + rho);
             const float Ls = isinf(secD) ? INFINITY
                                          : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
             const float L2 = fminf(Ls, lun);
@@ -398,9 +419,9 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat)
                     S.ub[row] = U1;
                     if (mv) {
                         // the old label becomes an "other" member of its group
-                        const int go = S.group_of[old];
+                        const int go = gof[old];
                         const float la =
-                            fmaxf((sqrtf(acc_a) - kU32 * (xn + S.cnorm[old])) * (1.0f - rho), 0.f);
+                            fmaxf((sqrtf(acc_a) - kU32 * (xn + cnm[old])) * (1.0f - rho), 0.f);
                         lbr[go * ln] = fminf(lbr[go * ln], la);
                     }
                 }
@@ -408,10 +429,16 @@ __global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat)
                 flag = true;
             }
         }
-        int64_t pos = block_append(mv && lane == 0, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
-        if (mv && lane == 0) S.moved[pos] = make_int2((int)row, old);
-        int64_t fpos = block_append(flag && lane == 0, (unsigned long long*)(stat + LK_STAT_FLAGGED), scr);
-        if (flag && lane == 0) S.flagged[fpos] = (int)row;
+        // rows differ in how many groups they scan: no block-wide barrier here,
+        // one atomic per moved / flagged row instead (both are a small minority)
+        if (lane == 0 && mv) {
+            const unsigned long long pos = atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), 1ull);
+            S.moved[pos] = make_int2((int)row, old);
+        }
+        if (lane == 0 && flag) {
+            const unsigned long long fpos = atomicAdd((unsigned long long*)(stat + LK_STAT_FLAGGED), 1ull);
+            S.flagged[fpos] = (int)row;
+        }
     }
     warp_add(ndist, stat + LK_STAT_DIST);
 }
@@ -720,7 +747,8 @@ static void launch_filter_m(const lk::DevState& S, int64_t* stat, int sms, cudaS
 
 template <int DP>
 static void launch_scan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
-    const size_t csm = (size_t)S.k * S.ldc * sizeof(float);
+    const size_t csm = (size_t)S.k * S.ldc * sizeof(float) + (size_t)S.k * 4 * 5 +
+                       (size_t)(S.t_groups + 1) * 4;
     if (csm <= 96 * 1024)
         k_yy_scan<DP, true><<<sms * 8, kThreads, csm, st>>>(S, stat);
     else
