@@ -38,7 +38,7 @@ enum InternalBuf {
     B_C64_PREV, B_C32, B_CNORM, B_DRIFT, B_SHALF, B_GDRIFT, B_SCAL, B_MOVED, B_FLAGGED, B_WORK,
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
-    B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN,
+    B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
     B_COUNT_
 };
 
@@ -154,6 +154,9 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_GINV] = (uint64_t)k * 4;
         L->size[B_CG] = (uint64_t)k * L->ldc * 4;
         L->size[B_YLUN] = (uint64_t)n * 8;
+        L->size[B_YAUX] = (uint64_t)n * 8;
+        L->size[B_YPAIRS4] = (uint64_t)cap * 16;
+        L->size[B_YBUCKET] = (uint64_t)3 * (L->groups + 1) * 8;
     }
     uint64_t off = 0;
     for (int b = 0; b < B_COUNT_; b++) {
@@ -358,6 +361,9 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.ginv = buf<int32_t>(c, B_GINV);
     S.Cg = buf<float>(c, B_CG);
     S.ylun = buf<float2>(c, B_YLUN);
+    S.yaux = buf<int2>(c, B_YAUX);
+    S.ypairs4 = buf<int4>(c, B_YPAIRS4);
+    S.ybucket = buf<int64_t>(c, B_YBUCKET);
     S.pair_cap = L.pair_cap;
 
     std::vector<int32_t> prog;
@@ -570,6 +576,7 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
     lk::DevState& S = c->S;
     int64_t* stat = S.cur;  // counters of the iteration in flight (copied out by the update)
     LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
+    if (S.ybucket) LK_CUDA_CHECK(cudaMemsetAsync(S.ybucket, 0, c->L.size[B_YBUCKET], st));
     const int64_t n = c->cfg.n_local;
     const bool use_tc = lkh::tc_supported(S);
     lk_status s;

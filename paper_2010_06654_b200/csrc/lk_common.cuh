@@ -82,6 +82,9 @@ struct DevState {
     int2* ypairs;           // [pair_cap] (row, group | label position << 16)
     float4* yres;           // [pair_cap] (bits of best j, best D~, second D~, -)
     int64_t pair_cap;
+    int2* yaux;             // [n] per worklist row: (first result slot or -1, label position)
+    int4* ypairs4;          // [pair_cap] group-sorted scans: (row, group, result slot, label pos)
+    int64_t* ybucket;       // [3 (t + 1)] bucket counts | offsets (+ total) | fills
 };
 
 // Finalize a row's lower bounds from one certified bound on every non-winning

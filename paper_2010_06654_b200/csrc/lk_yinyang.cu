@@ -223,8 +223,13 @@ template <int T>
 __global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64_t* stat) {
     if (*S.done) return;
     __shared__ float gd[T];
+    __shared__ int bcnt[T];
     __shared__ unsigned long long scr[3 * (kThreads / 32) + 2];
-    if (threadIdx.x < T) gd[threadIdx.x] = S.gdrift[threadIdx.x];
+    __shared__ unsigned long long rsc[kThreads / 32 + 1];
+    if (threadIdx.x < T) {
+        gd[threadIdx.x] = S.gdrift[threadIdx.x];
+        bcnt[threadIdx.x] = 0;
+    }
     __syncthreads();
     const float rho = simt_rel_err(S.d);
     const int64_t ln = S.n;
@@ -234,6 +239,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64
         const bool valid = i < S.n;
         bool active = false, need = false;
         unsigned mask = 0;
+        int apos = 0;
         float acc_a = 0.f, u = 0.f, lun = INFINITY, xn = 0.f;
         if (valid) {
             const int a = S.labels[i];
@@ -257,6 +263,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64
                 const float* xp = S.X32 + i * S.ldx;
                 acc_a = dist2_row(S, xp, a);
                 xn = xnorm(S, xp);
+                apos = S.ginv[a];
                 const float U = (sqrtf(acc_a) + kU32 * (xn + S.cnorm[a])) * (1.0f + rho);
                 u = fminf(u, U);
                 need = !(gmin > u);
@@ -274,11 +281,24 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64
         block_append2(need, false, (unsigned long long*)(stat + LK_STAT_YWL),
                       (unsigned long long*)(stat + LK_STAT_PAIRS), stat + LK_STAT_ACTIVE, active,
                       scr, wpos, unused);
+        // each worklist row owns a contiguous range of result slots (one per scanned group)
+        const int cnt = __popc(mask);
+        const int64_t poff = block_reserve(cnt, (unsigned long long*)(stat + LK_STAT_PAIRS), rsc);
         if (need) {
             S.ywl[wpos] = make_int4((int)i, (int)mask, __float_as_int(acc_a), __float_as_int(xn));
             S.ylun[wpos] = make_float2(lun, 0.f);
+            const bool fits = poff + cnt <= S.pair_cap;
+            S.yaux[wpos] = make_int2(fits ? (int)poff : -1, apos);
+            if (fits) {
+#pragma unroll
+                for (int g = 0; g < T; g++)
+                    if ((mask >> g) & 1u) atomicAdd(&bcnt[g], 1);
+            }
         }
     }
+    __syncthreads();
+    if (threadIdx.x < T && bcnt[threadIdx.x])
+        atomicAdd((unsigned long long*)(S.ybucket + threadIdx.x), (unsigned long long)bcnt[threadIdx.x]);
 }
 
 template <int DP>
@@ -295,152 +315,184 @@ __device__ __forceinline__ float dist2_dp(const float (&xr)[DP], const float* cp
     return acc;
 }
 
-// STAGED: all centroids (group order) live in shared memory -> LDS with
-// 32-bit addressing; otherwise they are read from L2 through the read-only path.
+// Exclusive scan of the per-group bucket counts (single small block).
+__global__ void k_yy_buckets(DevState S) {
+    if (*S.done) return;
+    if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        for (int g = 0; g < S.t_groups; g++) {
+            const int64_t c = S.ybucket[g];
+            S.ybucket[S.t_groups + 1 + g] = acc;   // bucket offset
+            S.ybucket[2 * (S.t_groups + 1) + g] = 0;  // bucket fill
+            acc += c;
+        }
+        S.ybucket[2 * S.t_groups + 1] = acc;
+    }
+}
+
+// Scatter every (row, group) scan into its group's bucket; a warp's lanes
+// agree on the bucket, so one atomic per warp and group.
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_yy_scatter(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    const int64_t m = stat[LK_STAT_YWL];
+    const int64_t* boff = S.ybucket + (T + 1);
+    unsigned long long* bfill = (unsigned long long*)(S.ybucket + 2 * (T + 1));
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < m;
+         base += (int64_t)gridDim.x * kThreads) {
+        const int64_t w = base + threadIdx.x;
+        unsigned mask = 0;
+        int4 e = make_int4(0, 0, 0, 0);
+        int2 aux = make_int2(-1, 0);
+        if (w < m) {
+            e = S.ywl[w];
+            aux = S.yaux[w];
+            mask = aux.x >= 0 ? (unsigned)e.y : 0u;
+        }
+#pragma unroll
+        for (int g = 0; g < T; g++) {
+            const bool has = (mask >> g) & 1u;
+            const unsigned bal = __ballot_sync(LK_FULL_MASK, has);
+            if (!bal) continue;
+            const int leader = __ffs(bal) - 1;
+            unsigned long long b = 0;
+            if ((int)lane_id() == leader) b = atomicAdd(bfill + g, (unsigned long long)__popc(bal));
+            b = __shfl_sync(LK_FULL_MASK, b, leader);
+            if (has) {
+                const int64_t q = boff[g] + (int64_t)b + __popc(bal & lanemask_lt());
+                const int slot = aux.x + __popc(mask & ((1u << g) - 1u));
+                if (q < S.pair_cap) S.ypairs4[q] = make_int4(e.x, g, slot, aux.y);
+            }
+        }
+    }
+}
+
+// One thread per (row, group) scan, pairs sorted by group: a warp's lanes
+// walk the same group, so the centroid reads are shared-memory broadcasts.
 template <int DP, bool STAGED>
-__global__ void __launch_bounds__(kThreads) k_yy_scan(DevState S, int64_t* stat) {
+__global__ void __launch_bounds__(kThreads) k_yy_sorted_scan(DevState S, int64_t* stat) {
     if (*S.done) return;
     extern __shared__ __align__(16) float csm[];
-    __shared__ unsigned long long scr[kThreads / 32 + 1];
-    const int64_t m = stat[LK_STAT_YWL];
-    constexpr int kWarps = kThreads / 32;
-    if ((int64_t)blockIdx.x * kWarps >= m) return;
-    // STAGED: centroids in group order plus the small per-centroid tables
-    // (group ranges, permutation, inverse, norms, group of) live in shared
-    // memory, so a row's dependent chain touches global memory only for its
-    // own worklist entry, label and coordinates.
-    const int k = S.k, T = S.t_groups;
-    float* s_cn = csm + k * S.ldc;
-    int* s_goff = reinterpret_cast<int*>(s_cn + k);
+    const int T = S.t_groups;
+    const int64_t np_ = min(S.ybucket[2 * T + 1], S.pair_cap);
+    if ((int64_t)blockIdx.x * kThreads >= np_) return;
+    const int k = S.k;
+    int* s_goff = reinterpret_cast<int*>(csm + (STAGED ? k * S.ldc : 0));
     int* s_gperm = s_goff + T + 1;
-    int* s_ginv = s_gperm + k;
-    int* s_gof = s_ginv + k;
     if (STAGED) {
         const int tot = k * S.ldc;
         for (int e = threadIdx.x; e < tot; e += kThreads) csm[e] = S.Cg[e];
-        for (int e = threadIdx.x; e < k; e += kThreads) {
-            s_cn[e] = S.cnorm[e];
-            s_gperm[e] = S.gperm[e];
-            s_ginv[e] = S.ginv[e];
-            s_gof[e] = S.group_of[e];
-        }
-        for (int e = threadIdx.x; e <= T; e += kThreads) s_goff[e] = S.goff[e];
-        __syncthreads();
     }
+    for (int e = threadIdx.x; e < k; e += kThreads) s_gperm[e] = S.gperm[e];
+    for (int e = threadIdx.x; e <= T; e += kThreads) s_goff[e] = S.goff[e];
+    __syncthreads();
     const float* __restrict__ cg = STAGED ? csm : S.Cg;
-    const float* __restrict__ cnm = STAGED ? s_cn : S.cnorm;
-    const int* __restrict__ goff = STAGED ? s_goff : S.goff;
-    const int* __restrict__ gperm = STAGED ? s_gperm : S.gperm;
-    const int* __restrict__ ginv = STAGED ? s_ginv : S.ginv;
-    const int* __restrict__ gof = STAGED ? s_gof : S.group_of;
     const int ldc = S.ldc;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const float rho = simt_rel_err(S.d);
-    const float cmax = S.scal[0];
-    const int64_t ln = S.n;
     int64_t ndist = 0;
-    // warps pull rows independently (dynamic: rows differ in scanned groups)
-    for (int64_t e0 = (int64_t)blockIdx.x * kWarps + warp; e0 < m; e0 += (int64_t)gridDim.x * kWarps) {
-        const int64_t e = e0;
-        const bool valid = true;
-        const int4 w = S.ywl[e];
-        const int64_t row = w.x;
-        const unsigned mask = (unsigned)w.y;
-        const float acc_a = __int_as_float(w.z), xn = __int_as_float(w.w);
-        const int old = valid ? S.labels[row] : 0;
-        const int apos = valid ? ginv[old] : -1;
+    for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < np_;
+         q += (int64_t)gridDim.x * kThreads) {
+        const int4 pr = S.ypairs4[q];
+        const int64_t row = pr.x;
+        const int g = pr.y, apos = pr.w;
         float xr[DP];
         const float* xp = S.X32 + row * S.ldx;
 #pragma unroll
-        for (int z = 0; z < DP; z++) xr[z] = (valid && z < S.d) ? __ldg(xp + z) : 0.f;
-        float bestD = acc_a, secD = INFINITY;
-        int bestJ = old;
-        float myg1 = INFINITY, myg2 = INFINITY;  // lane g: group g's top-2
-        int myj1 = -1;
-        unsigned mm = mask;
-        while (mm) {  // warp-uniform: mask is the same on every lane
-            const int g = __ffs(mm) - 1;
-            mm &= mm - 1;
-            const int j0 = goff[g], j9 = goff[g + 1];
-            float b1 = INFINITY, b2 = INFINITY;
-            int p1 = 0x7fffffff;
-            for (int jj = j0 + lane; jj < j9; jj += 32) {
-                float acc = dist2_dp<DP>(xr, cg + jj * ldc, S.d);
-                acc = (jj == apos) ? INFINITY : acc;  // the label competes via its tightened bound
-                if (acc < b1) { b2 = b1; b1 = acc; p1 = jj; }
-                else b2 = fminf(b2, acc);
-            }
-            ndist += (lane == 0) ? (j9 - j0) - (apos >= j0 && apos < j9 ? 1 : 0) : 0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const float ob1 = __shfl_xor_sync(LK_FULL_MASK, b1, o);
-                const float ob2 = __shfl_xor_sync(LK_FULL_MASK, b2, o);
-                const int op1 = __shfl_xor_sync(LK_FULL_MASK, p1, o);
-                if (ob1 < b1 || (ob1 == b1 && op1 < p1)) {
-                    b2 = fminf(b1, ob2);
-                    b1 = ob1;
-                    p1 = op1;
-                } else {
-                    b2 = fminf(b2, ob1);
-                }
-            }
-            const int gj = (p1 < 0x7fffffff && !isinf(b1)) ? gperm[p1] : -1;
-            if (lane == g) { myg1 = b1; myg2 = b2; myj1 = gj; }
-            if (gj >= 0) {
-                if (b1 < bestD || (b1 == bestD && gj < bestJ)) {
-                    secD = fminf(secD, bestD);
-                    bestD = b1;
-                    bestJ = gj;
-                } else {
-                    secD = fminf(secD, b1);
-                }
-            }
-            secD = fminf(secD, b2);
+        for (int z = 0; z < DP; z++) xr[z] = z < S.d ? __ldg(xp + z) : 0.f;
+        const int j0 = s_goff[g], j9 = s_goff[g + 1];
+        float b1 = INFINITY, b2 = INFINITY;
+        int p1 = -1;
+        for (int jj = j0; jj < j9; jj++) {
+            float acc = dist2_dp<DP>(xr, cg + jj * ldc, S.d);
+            acc = (jj == apos) ? INFINITY : acc;  // the label competes via its tightened bound
+            if (acc < b1) { b2 = b1; b1 = acc; p1 = jj; }
+            else b2 = fminf(b2, acc);
         }
-        bool mv = false, flag = false;
-        if (valid) {
-            const float lun = S.ylun[e].x;
-            const float U1 = (sqrtf(bestD) + kU32 * (xn + cnm[bestJ])) * (1.0f + rho);
-            const float Ls = isinf(secD) ? INFINITY
-                                         : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
-            const float L2 = fminf(Ls, lun);
-            if (L2 > U1) {
-                mv = bestJ != old;
-                float* lbr = S.lb + row;
-                if ((mask >> lane) & 1u) {
-                    const float gm = (myj1 == bestJ) ? myg2 : myg1;
-                    lbr[(int64_t)lane * ln] =
-                        isinf(gm) ? INFINITY
-                                  : fmaxf((sqrtf(gm) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    S.labels[row] = bestJ;
-                    S.ub[row] = U1;
-                    if (mv) {
-                        // the old label becomes an "other" member of its group
-                        const int go = gof[old];
-                        const float la =
-                            fmaxf((sqrtf(acc_a) - kU32 * (xn + cnm[old])) * (1.0f - rho), 0.f);
-                        lbr[go * ln] = fminf(lbr[go * ln], la);
-                    }
-                }
-            } else {
-                flag = true;
-            }
-        }
-        // rows differ in how many groups they scan: no block-wide barrier here,
-        // one atomic per moved / flagged row instead (both are a small minority)
-        if (lane == 0 && mv) {
-            const unsigned long long pos = atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), 1ull);
-            S.moved[pos] = make_int2((int)row, old);
-        }
-        if (lane == 0 && flag) {
-            const unsigned long long fpos = atomicAdd((unsigned long long*)(stat + LK_STAT_FLAGGED), 1ull);
-            S.flagged[fpos] = (int)row;
-        }
+        ndist += (j9 - j0) - (apos >= j0 && apos < j9 ? 1 : 0);
+        S.yres[pr.z] = make_float4(__int_as_float(p1 >= 0 && !isinf(b1) ? s_gperm[p1] : -1), b1, b2, 0.f);
     }
     warp_add(ndist, stat + LK_STAT_DIST);
+}
+
+// Per worklist row: certify the label from the scanned groups' top-2, write
+// the new group bounds; ambiguous rows -> exact fp64 recheck, rows whose
+// result range did not fit -> full SIMT rescan.
+template <int T>
+__global__ void __launch_bounds__(kThreads) k_yy_merge_m(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    __shared__ unsigned long long scr[kThreads / 32 + 1];
+    const int64_t m = stat[LK_STAT_YWL];
+    const float rho = simt_rel_err(S.d);
+    const float cmax = S.scal[0];
+    const int64_t ln = S.n;
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < m;
+         base += (int64_t)gridDim.x * kThreads) {
+        const int64_t e = base + threadIdx.x;
+        bool mv = false, flag = false, full = false;
+        int64_t row = 0;
+        int old = 0;
+        if (e < m) {
+            const int4 w = S.ywl[e];
+            const int2 aux = S.yaux[e];
+            row = w.x;
+            old = S.labels[row];
+            if (aux.x < 0) {
+                full = true;
+            } else {
+                const unsigned mask = (unsigned)w.y;
+                const float acc_a = __int_as_float(w.z), xn = __int_as_float(w.w);
+                float bestD = acc_a, secD = INFINITY;
+                int bestJ = old;
+                int slot = aux.x;
+                for (unsigned mm = mask; mm; mm &= mm - 1, slot++) {
+                    const float4 r = S.yres[slot];
+                    const int pj = __float_as_int(r.x);
+                    if (pj >= 0) {
+                        if (r.y < bestD || (r.y == bestD && pj < bestJ)) {
+                            secD = fminf(secD, bestD);
+                            bestD = r.y;
+                            bestJ = pj;
+                        } else {
+                            secD = fminf(secD, r.y);
+                        }
+                    }
+                    secD = fminf(secD, r.z);
+                }
+                const float lun = S.ylun[e].x;
+                const float U1 = (sqrtf(bestD) + kU32 * (xn + S.cnorm[bestJ])) * (1.0f + rho);
+                const float Ls = isinf(secD) ? INFINITY
+                                             : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
+                if (fminf(Ls, lun) > U1) {
+                    mv = bestJ != old;
+                    S.labels[row] = bestJ;
+                    S.ub[row] = U1;
+                    float* lbr = S.lb + row;
+                    slot = aux.x;
+                    for (unsigned mm = mask; mm; mm &= mm - 1, slot++) {
+                        const int g = __ffs(mm) - 1;
+                        const float4 r = S.yres[slot];
+                        const float gm = (__float_as_int(r.x) == bestJ) ? r.z : r.y;
+                        lbr[(int64_t)g * ln] =
+                            isinf(gm) ? INFINITY
+                                      : fmaxf((sqrtf(gm) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
+                    }
+                    if (mv) {
+                        const int go = S.group_of[old];
+                        const float la =
+                            fmaxf((sqrtf(acc_a) - kU32 * (xn + S.cnorm[old])) * (1.0f - rho), 0.f);
+                        lbr[go * ln] = fminf(lbr[go * ln], la);
+                    }
+                } else {
+                    flag = true;
+                }
+            }
+        }
+        int64_t pos = block_append(mv, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
+        if (mv) S.moved[pos] = make_int2((int)row, old);
+        int64_t fpos = block_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED), scr);
+        if (flag) S.flagged[fpos] = (int)row;
+        int64_t wpos = block_append(full, (unsigned long long*)(stat + LK_STAT_WORK), scr);
+        if (full) S.work[wpos] = (int)row;
+    }
 }
 
 // Iteration 1 of the group strategies (SequentialStrategy.seed +
@@ -720,11 +772,11 @@ static int grid_for_rows(int64_t rows, int sms, int per_sm) {
 lk_status init_yy_attributes() {
 #define LK_SMEM96(kern) \
     LK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024))
-    LK_SMEM96((k_yy_scan<2, true>));
-    LK_SMEM96((k_yy_scan<4, true>));
-    LK_SMEM96((k_yy_scan<8, true>));
-    LK_SMEM96((k_yy_scan<16, true>));
-    LK_SMEM96((k_yy_scan<32, true>));
+    LK_SMEM96((k_yy_sorted_scan<2, true>));
+    LK_SMEM96((k_yy_sorted_scan<4, true>));
+    LK_SMEM96((k_yy_sorted_scan<8, true>));
+    LK_SMEM96((k_yy_sorted_scan<16, true>));
+    LK_SMEM96((k_yy_sorted_scan<32, true>));
     LK_SMEM96((k_seed_yinyang<2, true>));
     LK_SMEM96((k_seed_yinyang<4, true>));
     LK_SMEM96((k_seed_yinyang<8, true>));
@@ -746,13 +798,13 @@ static void launch_filter_m(const lk::DevState& S, int64_t* stat, int sms, cudaS
 }
 
 template <int DP>
-static void launch_scan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
-    const size_t csm = (size_t)S.k * S.ldc * sizeof(float) + (size_t)S.k * 4 * 5 +
-                       (size_t)(S.t_groups + 1) * 4;
+static void launch_sorted_scan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    const size_t tabs = (size_t)S.k * 4 + (size_t)(S.t_groups + 1) * 4;
+    const size_t csm = (size_t)S.k * S.ldc * sizeof(float) + tabs;
     if (csm <= 96 * 1024)
-        k_yy_scan<DP, true><<<sms * 8, kThreads, csm, st>>>(S, stat);
+        k_yy_sorted_scan<DP, true><<<sms * 8, kThreads, csm, st>>>(S, stat);
     else
-        k_yy_scan<DP, false><<<sms * 8, kThreads, 0, st>>>(S, stat);
+        k_yy_sorted_scan<DP, false><<<sms * 8, kThreads, tabs, st>>>(S, stat);
 }
 
 template <int DP>
@@ -794,12 +846,18 @@ lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaSt
 
 lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     if (yy_masked(S)) {
+        const int T = S.t_groups;
+        k_yy_buckets<<<1, 32, 0, st>>>(S);
+        const int g2 = grid_for_rows(S.n, sms, 4);
+        if (T <= 8) k_yy_scatter<8><<<g2, kThreads, 0, st>>>(S, stat);
+        else if (T <= 16) k_yy_scatter<16><<<g2, kThreads, 0, st>>>(S, stat);
+        else k_yy_scatter<32><<<g2, kThreads, 0, st>>>(S, stat);
         const int d = S.d;
-        if (d <= 2) launch_scan<2>(S, stat, sms, st);
-        else if (d <= 4) launch_scan<4>(S, stat, sms, st);
-        else if (d <= 8) launch_scan<8>(S, stat, sms, st);
-        else if (d <= 16) launch_scan<16>(S, stat, sms, st);
-        else launch_scan<32>(S, stat, sms, st);
+        if (d <= 2) launch_sorted_scan<2>(S, stat, sms, st);
+        else if (d <= 4) launch_sorted_scan<4>(S, stat, sms, st);
+        else if (d <= 8) launch_sorted_scan<8>(S, stat, sms, st);
+        else if (d <= 16) launch_sorted_scan<16>(S, stat, sms, st);
+        else launch_sorted_scan<32>(S, stat, sms, st);
         LK_LAUNCH_CHECK();
         return LK_OK;
     }
@@ -811,7 +869,14 @@ lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStr
 }
 
 lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
-    if (yy_masked(S)) return LK_OK;  // merged into k_yy_scan
+    if (yy_masked(S)) {
+        const int T = S.t_groups, g = grid_for_rows(S.n, sms, 4);
+        if (T <= 8) k_yy_merge_m<8><<<g, kThreads, 0, st>>>(S, stat);
+        else if (T <= 16) k_yy_merge_m<16><<<g, kThreads, 0, st>>>(S, stat);
+        else k_yy_merge_m<32><<<g, kThreads, 0, st>>>(S, stat);
+        LK_LAUNCH_CHECK();
+        return LK_OK;
+    }
     k_yy_merge<<<grid_for_rows(S.n, sms, 4), kThreads, 0, st>>>(S, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;
