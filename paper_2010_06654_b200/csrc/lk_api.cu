@@ -46,7 +46,7 @@ struct Layout {
     uint64_t off[B_COUNT_];
     uint64_t size[B_COUNT_];
     uint64_t total;
-    int64_t ldx, ldc, delta_len, pair_cap;
+    int64_t ldx, ldc, delta_len, pair_cap, bucket_cap;
     int32_t nlb, groups;
 };
 
@@ -155,8 +155,13 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_CG] = (uint64_t)k * L->ldc * 4;
         L->size[B_YLUN] = (uint64_t)n * 8;
         L->size[B_YAUX] = (uint64_t)n * 8;
-        L->size[B_YPAIRS4] = (uint64_t)cap * 16;
-        L->size[B_YBUCKET] = (uint64_t)3 * (L->groups + 1) * 8;
+        // group buckets: one slot per row per group (capped); overflow -> full rescan
+        int64_t bcap = n;
+        if (bcap * L->groups > (1LL << 27)) bcap = (1LL << 27) / L->groups;
+        if (bcap < 1) bcap = 1;
+        L->bucket_cap = bcap;
+        L->size[B_YPAIRS4] = (uint64_t)bcap * L->groups * 16;
+        L->size[B_YBUCKET] = (uint64_t)(L->groups + 1) * 8;
     }
     uint64_t off = 0;
     for (int b = 0; b < B_COUNT_; b++) {
@@ -364,6 +369,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.yaux = buf<int2>(c, B_YAUX);
     S.ypairs4 = buf<int4>(c, B_YPAIRS4);
     S.ybucket = buf<int64_t>(c, B_YBUCKET);
+    S.bucket_cap = L.bucket_cap;
     S.pair_cap = L.pair_cap;
 
     std::vector<int32_t> prog;

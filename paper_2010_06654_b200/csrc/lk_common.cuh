@@ -83,8 +83,9 @@ struct DevState {
     float4* yres;           // [pair_cap] (bits of best j, best D~, second D~, -)
     int64_t pair_cap;
     int2* yaux;             // [n] per worklist row: (first result slot or -1, label position)
-    int4* ypairs4;          // [pair_cap] group-sorted scans: (row, group, result slot, label pos)
-    int64_t* ybucket;       // [3 (t + 1)] bucket counts | offsets (+ total) | fills
+    int4* ypairs4;          // [t, bucket_cap] scans bucketed by group: (row, group, slot, label pos)
+    int64_t* ybucket;       // [t] bucket fill counts
+    int64_t bucket_cap;
 };
 
 // Finalize a row's lower bounds from one certified bound on every non-winning

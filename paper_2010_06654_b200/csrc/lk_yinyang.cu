@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64
     if (*S.done) return;
     __shared__ float gd[T];
     __shared__ int bcnt[T];
+    __shared__ int64_t bbase[T];
     __shared__ unsigned long long scr[3 * (kThreads / 32) + 2];
     __shared__ unsigned long long rsc[kThreads / 32 + 1];
     if (threadIdx.x < T) {
@@ -284,21 +285,40 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64
         // each worklist row owns a contiguous range of result slots (one per scanned group)
         const int cnt = __popc(mask);
         const int64_t poff = block_reserve(cnt, (unsigned long long*)(stat + LK_STAT_PAIRS), rsc);
+        const bool fits = need && poff + cnt <= S.pair_cap;
+        // per-group buckets (region g of ypairs4 holds group g's scans): shared
+        // atomics for the block-local ranks, one global atomic per group
+        int rank[T];
+#pragma unroll
+        for (int g = 0; g < T; g++) rank[g] = (fits && ((mask >> g) & 1u)) ? atomicAdd(&bcnt[g], 1) : -1;
+        __syncthreads();
+        if (threadIdx.x < T) {
+            const int c = bcnt[threadIdx.x];
+            bbase[threadIdx.x] = c ? (int64_t)atomicAdd((unsigned long long*)(S.ybucket + threadIdx.x),
+                                                         (unsigned long long)c)
+                                   : 0;
+            bcnt[threadIdx.x] = 0;
+        }
+        __syncthreads();
         if (need) {
             S.ywl[wpos] = make_int4((int)i, (int)mask, __float_as_int(acc_a), __float_as_int(xn));
             S.ylun[wpos] = make_float2(lun, 0.f);
-            const bool fits = poff + cnt <= S.pair_cap;
-            S.yaux[wpos] = make_int2(fits ? (int)poff : -1, apos);
-            if (fits) {
+            int slot = (int)poff;
+            bool lost = false;  // a bucket was full: this row gets a full rescan instead
 #pragma unroll
-                for (int g = 0; g < T; g++)
-                    if ((mask >> g) & 1u) atomicAdd(&bcnt[g], 1);
+            for (int g = 0; g < T; g++) {
+                if (rank[g] >= 0) {
+                    const int64_t q = bbase[g] + rank[g];
+                    if (q < S.bucket_cap)
+                        S.ypairs4[(int64_t)g * S.bucket_cap + q] = make_int4((int)i, g, slot, apos);
+                    else
+                        lost = true;
+                    slot++;
+                }
             }
+            S.yaux[wpos] = make_int2(fits && !lost ? (int)poff : -1, apos);
         }
     }
-    __syncthreads();
-    if (threadIdx.x < T && bcnt[threadIdx.x])
-        atomicAdd((unsigned long long*)(S.ybucket + threadIdx.x), (unsigned long long)bcnt[threadIdx.x]);
 }
 
 template <int DP>
@@ -315,58 +335,6 @@ __device__ __forceinline__ float dist2_dp(const float (&xr)[DP], const float* cp
     return acc;
 }
 
-// Exclusive scan of the per-group bucket counts (single small block).
-__global__ void k_yy_buckets(DevState S) {
-    if (*S.done) return;
-    if (threadIdx.x == 0) {
-        int64_t acc = 0;
-        for (int g = 0; g < S.t_groups; g++) {
-            const int64_t c = S.ybucket[g];
-            S.ybucket[S.t_groups + 1 + g] = acc;   // bucket offset
-            S.ybucket[2 * (S.t_groups + 1) + g] = 0;  // bucket fill
-            acc += c;
-        }
-        S.ybucket[2 * S.t_groups + 1] = acc;
-    }
-}
-
-// Scatter every (row, group) scan into its group's bucket; a warp's lanes
-// agree on the bucket, so one atomic per warp and group.
-template <int T>
-__global__ void __launch_bounds__(kThreads) k_yy_scatter(DevState S, int64_t* stat) {
-    if (*S.done) return;
-    const int64_t m = stat[LK_STAT_YWL];
-    const int64_t* boff = S.ybucket + (T + 1);
-    unsigned long long* bfill = (unsigned long long*)(S.ybucket + 2 * (T + 1));
-    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < m;
-         base += (int64_t)gridDim.x * kThreads) {
-        const int64_t w = base + threadIdx.x;
-        unsigned mask = 0;
-        int4 e = make_int4(0, 0, 0, 0);
-        int2 aux = make_int2(-1, 0);
-        if (w < m) {
-            e = S.ywl[w];
-            aux = S.yaux[w];
-            mask = aux.x >= 0 ? (unsigned)e.y : 0u;
-        }
-#pragma unroll
-        for (int g = 0; g < T; g++) {
-            const bool has = (mask >> g) & 1u;
-            const unsigned bal = __ballot_sync(LK_FULL_MASK, has);
-            if (!bal) continue;
-            const int leader = __ffs(bal) - 1;
-            unsigned long long b = 0;
-            if ((int)lane_id() == leader) b = atomicAdd(bfill + g, (unsigned long long)__popc(bal));
-            b = __shfl_sync(LK_FULL_MASK, b, leader);
-            if (has) {
-                const int64_t q = boff[g] + (int64_t)b + __popc(bal & lanemask_lt());
-                const int slot = aux.x + __popc(mask & ((1u << g) - 1u));
-                if (q < S.pair_cap) S.ypairs4[q] = make_int4(e.x, g, slot, aux.y);
-            }
-        }
-    }
-}
-
 // One thread per (row, group) scan, pairs sorted by group: a warp's lanes
 // walk the same group, so the centroid reads are shared-memory broadcasts.
 template <int DP, bool STAGED>
@@ -374,7 +342,8 @@ __global__ void __launch_bounds__(kThreads) k_yy_sorted_scan(DevState S, int64_t
     if (*S.done) return;
     extern __shared__ __align__(16) float csm[];
     const int T = S.t_groups;
-    const int64_t np_ = min(S.ybucket[2 * T + 1], S.pair_cap);
+    const int gB = blockIdx.y;  // this block's group bucket
+    const int64_t np_ = min(S.ybucket[gB], S.bucket_cap);
     if ((int64_t)blockIdx.x * kThreads >= np_) return;
     const int k = S.k;
     int* s_goff = reinterpret_cast<int*>(csm + (STAGED ? k * S.ldc : 0));
@@ -389,9 +358,10 @@ __global__ void __launch_bounds__(kThreads) k_yy_sorted_scan(DevState S, int64_t
     const float* __restrict__ cg = STAGED ? csm : S.Cg;
     const int ldc = S.ldc;
     int64_t ndist = 0;
+    const int4* __restrict__ bucket = S.ypairs4 + (int64_t)gB * S.bucket_cap;
     for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < np_;
          q += (int64_t)gridDim.x * kThreads) {
-        const int4 pr = S.ypairs4[q];
+        const int4 pr = bucket[q];
         const int64_t row = pr.x;
         const int g = pr.y, apos = pr.w;
         float xr[DP];
@@ -801,10 +771,11 @@ template <int DP>
 static void launch_sorted_scan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     const size_t tabs = (size_t)S.k * 4 + (size_t)(S.t_groups + 1) * 4;
     const size_t csm = (size_t)S.k * S.ldc * sizeof(float) + tabs;
+    const dim3 grid((unsigned)((sms * 8 + S.t_groups - 1) / S.t_groups), (unsigned)S.t_groups);
     if (csm <= 96 * 1024)
-        k_yy_sorted_scan<DP, true><<<sms * 8, kThreads, csm, st>>>(S, stat);
+        k_yy_sorted_scan<DP, true><<<grid, kThreads, csm, st>>>(S, stat);
     else
-        k_yy_sorted_scan<DP, false><<<sms * 8, kThreads, tabs, st>>>(S, stat);
+        k_yy_sorted_scan<DP, false><<<grid, kThreads, tabs, st>>>(S, stat);
 }
 
 template <int DP>
@@ -846,12 +817,6 @@ lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaSt
 
 lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     if (yy_masked(S)) {
-        const int T = S.t_groups;
-        k_yy_buckets<<<1, 32, 0, st>>>(S);
-        const int g2 = grid_for_rows(S.n, sms, 4);
-        if (T <= 8) k_yy_scatter<8><<<g2, kThreads, 0, st>>>(S, stat);
-        else if (T <= 16) k_yy_scatter<16><<<g2, kThreads, 0, st>>>(S, stat);
-        else k_yy_scatter<32><<<g2, kThreads, 0, st>>>(S, stat);
         const int d = S.d;
         if (d <= 2) launch_sorted_scan<2>(S, stat, sms, st);
         else if (d <= 4) launch_sorted_scan<4>(S, stat, sms, st);
