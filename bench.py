@@ -436,7 +436,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
-    ap.add_argument("--strategy", default="hamerly", choices=["lloyd", "hamerly", "yinyang", "elkan"])
+    ap.add_argument("--strategy", default="yinyang", choices=["lloyd", "hamerly", "yinyang", "elkan"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc"])
     ap.add_argument("--groups", type=int, default=0, help="Yinyang group count (0 = default)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -143,7 +143,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
     }
     if (is_group_strategy(c.strategy)) {
         int64_t cap = n * (int64_t)L->groups;
-        if (cap > (1LL << 27)) cap = 1LL << 27;
+        if (cap > (1LL << 30)) cap = 1LL << 30;  // result slots, <= 16 GB
         if (cap < 1) cap = 1;
         L->pair_cap = cap;
         L->size[B_GPERM] = (uint64_t)k * 4;
@@ -157,10 +157,10 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_YAUX] = (uint64_t)n * 8;
         // group buckets: one slot per row per group (capped); overflow -> full rescan
         int64_t bcap = n;
-        if (bcap * L->groups > (1LL << 27)) bcap = (1LL << 27) / L->groups;
+        if (bcap * L->groups > (1LL << 31)) bcap = (1LL << 31) / L->groups;  // <= 16 GB
         if (bcap < 1) bcap = 1;
         L->bucket_cap = bcap;
-        L->size[B_YPAIRS4] = (uint64_t)bcap * L->groups * 16;
+        L->size[B_YPAIRS4] = (uint64_t)bcap * L->groups * 8;
         L->size[B_YBUCKET] = (uint64_t)(L->groups + 1) * 8;
     }
     uint64_t off = 0;
@@ -367,7 +367,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.Cg = buf<float>(c, B_CG);
     S.ylun = buf<float2>(c, B_YLUN);
     S.yaux = buf<int2>(c, B_YAUX);
-    S.ypairs4 = buf<int4>(c, B_YPAIRS4);
+    S.ypairs2 = buf<int2>(c, B_YPAIRS4);
     S.ybucket = buf<int64_t>(c, B_YBUCKET);
     S.bucket_cap = L.bucket_cap;
     S.pair_cap = L.pair_cap;
@@ -600,23 +600,24 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             if (s != LK_OK) return s;
             c->launches += 1;
         } else if (is_group_strategy(c->cfg.strategy)) {
+            const bool full_only = use_tc && !lkh::yy_masked(S);
             {
                 ProfScope p(c, 1, st);
-                s = lkh::launch_yy_filter(S, stat, c->sms, st);
+                s = lkh::launch_yy_filter(S, stat, c->sms, st, full_only);
                 if (s != LK_OK) return s;
             }
             {
                 ProfScope p(c, 5, st);
-                s = lkh::launch_yy_pairs(S, stat, c->sms, st);
+                s = lkh::launch_yy_pairs(S, stat, c->sms, st, full_only);
                 if (s != LK_OK) return s;
             }
             {
                 ProfScope p(c, 6, st);
-                s = lkh::launch_yy_merge(S, stat, c->sms, st);
+                s = lkh::launch_yy_merge(S, stat, c->sms, st, full_only);
                 if (s != LK_OK) return s;
             }
             ProfScope p(c, 0, st);
-            // rows that did not fit the pair capacity: full rescan
+            // full rescans: capacity overflow, or every failing row when full_only
             s = use_tc ? lkh::launch_assign_tc(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st)
                        : lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
             if (s != LK_OK) return s;

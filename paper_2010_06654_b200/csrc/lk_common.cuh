@@ -83,7 +83,7 @@ struct DevState {
     float4* yres;           // [pair_cap] (bits of best j, best D~, second D~, -)
     int64_t pair_cap;
     int2* yaux;             // [n] per worklist row: (first result slot or -1, label position)
-    int4* ypairs4;          // [t, bucket_cap] scans bucketed by group: (row, group, slot, label pos)
+    int2* ypairs2;          // [t, bucket_cap] scans bucketed by group: (row, result slot)
     int64_t* ybucket;       // [t] bucket fill counts
     int64_t bucket_cap;
 };

@@ -26,9 +26,13 @@ lk_status launch_scan_exp(const lk::DevState& S, int sms, cudaStream_t st);
 
 bool yy_masked(const lk::DevState& S);
 lk_status launch_yy_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
-lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
-lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
-lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
+// full_only: every row failing the bounds is rescanned in full (tensor-core runs with d > 32)
+lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,
+                           bool full_only);
+lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,
+                          bool full_only);
+lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,
+                          bool full_only);
 
 // tcgen05 path (lk_tc.cu): full-scan assignment with 3xTF32 products.
 bool tc_supported(const lk::DevState& S);

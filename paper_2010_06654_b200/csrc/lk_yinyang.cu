@@ -89,7 +89,8 @@ __device__ __forceinline__ float xnorm(const DevState& S, const float* xp) {
 
 constexpr int kCh = 8;
 
-__global__ void __launch_bounds__(kThreads, 4) k_filter_yinyang(DevState S, int64_t* stat) {
+__global__ void __launch_bounds__(kThreads, 4) k_filter_yinyang(DevState S, int64_t* stat,
+                                                                int full_only) {
     if (*S.done) return;
     extern __shared__ float gd[];  // [t] group drifts
     __shared__ unsigned long long scr[kThreads / 32 + 1];
@@ -158,6 +159,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_yinyang(DevState S, int6
             }
         }
         block_count(active, stat + LK_STAT_ACTIVE, scr);
+        if (full_only) {
+            // high-d tensor-core runs: failing rows are rescanned in full
+            const int64_t fpos = block_append(need, (unsigned long long*)(stat + LK_STAT_WORK), scr);
+            if (need) S.work[fpos] = (int)i;
+            continue;
+        }
         const int64_t wpos = block_append(need, (unsigned long long*)(stat + LK_STAT_YWL), scr);
         const int64_t poff = block_reserve(need ? cnt : 0, (unsigned long long*)(stat + LK_STAT_PAIRS), scr);
         if (need) {
@@ -310,7 +317,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64
                 if (rank[g] >= 0) {
                     const int64_t q = bbase[g] + rank[g];
                     if (q < S.bucket_cap)
-                        S.ypairs4[(int64_t)g * S.bucket_cap + q] = make_int4((int)i, g, slot, apos);
+                        S.ypairs2[(int64_t)g * S.bucket_cap + q] = make_int2((int)i, slot);
                     else
                         lost = true;
                     slot++;
@@ -348,22 +355,27 @@ __global__ void __launch_bounds__(kThreads) k_yy_sorted_scan(DevState S, int64_t
     const int k = S.k;
     int* s_goff = reinterpret_cast<int*>(csm + (STAGED ? k * S.ldc : 0));
     int* s_gperm = s_goff + T + 1;
+    int* s_ginv = s_gperm + k;
     if (STAGED) {
         const int tot = k * S.ldc;
         for (int e = threadIdx.x; e < tot; e += kThreads) csm[e] = S.Cg[e];
     }
-    for (int e = threadIdx.x; e < k; e += kThreads) s_gperm[e] = S.gperm[e];
+    for (int e = threadIdx.x; e < k; e += kThreads) {
+        s_gperm[e] = S.gperm[e];
+        s_ginv[e] = S.ginv[e];
+    }
     for (int e = threadIdx.x; e <= T; e += kThreads) s_goff[e] = S.goff[e];
     __syncthreads();
     const float* __restrict__ cg = STAGED ? csm : S.Cg;
     const int ldc = S.ldc;
     int64_t ndist = 0;
-    const int4* __restrict__ bucket = S.ypairs4 + (int64_t)gB * S.bucket_cap;
+    const int2* __restrict__ bucket = S.ypairs2 + (int64_t)gB * S.bucket_cap;
     for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < np_;
          q += (int64_t)gridDim.x * kThreads) {
-        const int4 pr = bucket[q];
+        const int2 pr = bucket[q];
         const int64_t row = pr.x;
-        const int g = pr.y, apos = pr.w;
+        const int g = gB, apos = s_ginv[S.labels[row]];
+        const int slot = pr.y;
         float xr[DP];
         const float* xp = S.X32 + row * S.ldx;
 #pragma unroll
@@ -378,7 +390,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_sorted_scan(DevState S, int64_t
             else b2 = fminf(b2, acc);
         }
         ndist += (j9 - j0) - (apos >= j0 && apos < j9 ? 1 : 0);
-        S.yres[pr.z] = make_float4(__int_as_float(p1 >= 0 && !isinf(b1) ? s_gperm[p1] : -1), b1, b2, 0.f);
+        S.yres[slot] = make_float4(__int_as_float(p1 >= 0 && !isinf(b1) ? s_gperm[p1] : -1), b1, b2, 0.f);
     }
     warp_add(ndist, stat + LK_STAT_DIST);
 }
@@ -769,7 +781,7 @@ static void launch_filter_m(const lk::DevState& S, int64_t* stat, int sms, cudaS
 
 template <int DP>
 static void launch_sorted_scan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
-    const size_t tabs = (size_t)S.k * 4 + (size_t)(S.t_groups + 1) * 4;
+    const size_t tabs = (size_t)S.k * 8 + (size_t)(S.t_groups + 1) * 4;
     const size_t csm = (size_t)S.k * S.ldc * sizeof(float) + tabs;
     const dim3 grid((unsigned)((sms * 8 + S.t_groups - 1) / S.t_groups), (unsigned)S.t_groups);
     if (csm <= 96 * 1024)
@@ -799,8 +811,9 @@ lk_status launch_yy_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStre
     return LK_OK;
 }
 
-lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
-    if (yy_masked(S)) {
+lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,
+                           bool full_only) {
+    if (yy_masked(S) && !full_only) {
         // the group count is padded (with +inf bounds) up to a template size
         const int t = S.t_groups;
         if (t <= 8) launch_filter_m<8>(S, stat, sms, st);
@@ -810,12 +823,14 @@ lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaSt
         return LK_OK;
     }
     const size_t smem = (size_t)S.t_groups * sizeof(float);  // <= 64 KB (k <= 16384)
-    k_filter_yinyang<<<grid_for_rows(S.n, sms, 8), kThreads, smem, st>>>(S, stat);
+    k_filter_yinyang<<<grid_for_rows(S.n, sms, 8), kThreads, smem, st>>>(S, stat, full_only ? 1 : 0);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
 
-lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,
+                          bool full_only) {
+    if (full_only) return LK_OK;
     if (yy_masked(S)) {
         const int d = S.d;
         if (d <= 2) launch_sorted_scan<2>(S, stat, sms, st);
@@ -833,7 +848,9 @@ lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStr
     return LK_OK;
 }
 
-lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,
+                          bool full_only) {
+    if (full_only) return LK_OK;
     if (yy_masked(S)) {
         const int T = S.t_groups, g = grid_for_rows(S.n, sms, 4);
         if (T <= 8) k_yy_merge_m<8><<<g, kThreads, 0, st>>>(S, stat);

@@ -44,7 +44,9 @@ def gpu_groups(strategy: str, n: int, k: int) -> int:
     if strategy == "elkan":
         return k if n * k <= (1 << 26) else min(k, 64)
     if strategy == "yinyang":
-        return max(1, min(-(-k // 10), 32))
+        # ~128 centroids per group (the reference's k/10 would make the n*t
+        # table dominate an iteration's traffic at large k), at most 32 groups
+        return max(4, min(32, round(k / 128)))
     return 0
 
 
