@@ -83,6 +83,9 @@ class LabelHistory(Sequence):
         return len(self._parts)
 
     def _build(self, t: int) -> np.ndarray:
+        """Materialize iteration t from the nearest cached vector at or
+        before it; keeps the last vector plus a checkpoint every 8 iterations
+        (bounded host memory for long runs at large n)."""
         if t in self._cache:
             return self._cache[t]
         start = max((s for s in self._cache if s < t), default=-1)
@@ -90,8 +93,10 @@ class LabelHistory(Sequence):
         for s in range(start + 1, t + 1):
             _, rows, labels = self._parts[s]
             cur[rows] = labels
-            if s < t:
+            if s % 8 == 7 and s < t:
                 self._cache[s] = cur.copy()
+        for s in [s for s in self._cache if s % 8 != 7]:
+            del self._cache[s]
         self._cache[t] = cur
         return cur
 
