@@ -170,6 +170,13 @@ lk_status lk_step_assign(lk_ctx *ctx, int32_t t, void *stream);
  * theirs), drifts, bound tables, SSE into LK_BUF_SSE[t-1], done flag. */
 lk_status lk_step_update(lk_ctx *ctx, int32_t t, void *stream);
 
+/* CUDA graph of one iteration t >= 2 (lk_step_assign + lk_step_update),
+ * captured natively on the caller's stream and owned by the context; replays
+ * are valid for every later iteration because the iteration index is
+ * device-resident.  Single-process only (no collective inside). */
+lk_status lk_graph_capture(lk_ctx *ctx, int32_t t, void *stream);
+lk_status lk_graph_replay(lk_ctx *ctx, void *stream);
+
 /* Number of kernel launches issued by this context so far. */
 int64_t lk_launch_count(const lk_ctx *ctx);
 

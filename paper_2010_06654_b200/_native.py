@@ -31,7 +31,8 @@ STAT = {"changed": 0, "flagged": 1, "active": 2, "work": 3, "dist": 4, "bound_up
 EXPORTED = (
     "lk_version", "lk_last_error", "lk_workspace_bytes", "lk_ctx_create", "lk_ctx_destroy",
     "lk_buffer", "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
-    "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_launch_count", "lk_profile", "lk_profile_read",
+    "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_graph_capture", "lk_graph_replay",
+    "lk_launch_count", "lk_profile", "lk_profile_read",
 )
 
 
@@ -91,13 +92,16 @@ def load():
     L.lk_set_groups.argtypes = [vp, vp, vp]
     L.lk_step_assign.argtypes = [vp, i32, vp]
     L.lk_step_update.argtypes = [vp, i32, vp]
+    L.lk_graph_capture.argtypes = [vp, i32, vp]
+    L.lk_graph_replay.argtypes = [vp, vp]
     L.lk_launch_count.argtypes = [vp]
     L.lk_launch_count.restype = i64
     L.lk_profile.argtypes = [vp, i32]
     L.lk_profile_read.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
     for name in ("lk_workspace_bytes", "lk_ctx_create", "lk_ctx_destroy", "lk_buffer",
                  "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
-                 "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_profile", "lk_profile_read"):
+                 "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_graph_capture",
+                 "lk_graph_replay", "lk_profile", "lk_profile_read"):
         getattr(L, name).restype = i32
     _lib = L
     return L

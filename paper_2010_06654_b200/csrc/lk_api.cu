@@ -202,6 +202,9 @@ struct lk_ctx {
     bool centroids_set;
     bool groups_set;
     int64_t launches;
+    // one-iteration CUDA graph (lk_graph_capture)
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
     // profiling
     bool profile;
     struct Rec { int cls; cudaEvent_t a, b; };
@@ -396,6 +399,8 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
 
 lk_status lk_ctx_destroy(lk_ctx* c) {
     if (!c) return LK_OK;
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    if (c->graph) cudaGraphDestroy(c->graph);
     for (auto& r : c->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -682,6 +687,51 @@ lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
                                      buf<double>(c, B_SSE_PART), need_half, st);
     c->launches += need_half ? 3 : 2;
     return s;
+}
+
+lk_status lk_graph_capture(lk_ctx* c, int32_t t, void* stream) {
+    if (!c) return LK_ERR_ARG;
+    if (t < 2) {
+        set_error("lk_graph_capture: iteration 1 takes the first-iteration path; capture t >= 2");
+        return LK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->graph_exec) {
+        cudaGraphExecDestroy(c->graph_exec);
+        c->graph_exec = nullptr;
+    }
+    if (c->graph) {
+        cudaGraphDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    const bool prof = c->profile;
+    c->profile = false;  // no event records inside the graph
+    LK_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    lk_status s1 = lk_step_assign(c, t, stream);
+    lk_status s2 = s1 == LK_OK ? lk_step_update(c, t, stream) : s1;
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(st, &g);
+    c->profile = prof;
+    if (s2 != LK_OK) {
+        if (g) cudaGraphDestroy(g);
+        return s2;
+    }
+    if (e != cudaSuccess) {
+        set_error("cudaStreamEndCapture: %s", cudaGetErrorString(e));
+        return LK_ERR_CUDA;
+    }
+    c->graph = g;
+    LK_CUDA_CHECK(cudaGraphInstantiate(&c->graph_exec, g, 0));
+    return LK_OK;
+}
+
+lk_status lk_graph_replay(lk_ctx* c, void* stream) {
+    if (!c || !c->graph_exec) {
+        set_error("lk_graph_replay before lk_graph_capture");
+        return LK_ERR_STATE;
+    }
+    LK_CUDA_CHECK(cudaGraphLaunch(c->graph_exec, (cudaStream_t)stream));
+    return LK_OK;
 }
 
 int64_t lk_launch_count(const lk_ctx* c) { return c ? c->launches : 0; }

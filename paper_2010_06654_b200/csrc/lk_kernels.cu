@@ -872,7 +872,55 @@ lk_status init_simt_attributes() {
     return LK_OK;
 }
 
+// Small d: one thread per row, per-thread maxima in registers, shared then
+// global atomicMax (the warp-per-row version idles 30 of 32 lanes at d = 2).
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_scan_exp_small(DevState S) {
+    __shared__ int se[D + 1];
+    if (threadIdx.x <= D) se[threadIdx.x] = -1100;
+    __syncthreads();
+    int e[D + 1];
+#pragma unroll
+    for (int z = 0; z <= D; z++) e[z] = -1100;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < S.n;
+         i += (int64_t)gridDim.x * kThreads) {
+        double s2 = 0.0;
+#pragma unroll
+        for (int z = 0; z < D; z++) {
+            if (z < S.d) {
+                const double v = load_x(S, i, z);
+                s2 = fma(v, v, s2);
+                if (v != 0.0) {
+                    int ex;
+                    frexp(fabs(v), &ex);
+                    e[z] = max(e[z], ex);
+                }
+            }
+        }
+        if (s2 > 0.0) {
+            int ex;
+            frexp(s2 * (1.0 + 1e-9), &ex);
+            e[D] = max(e[D], ex);
+        }
+    }
+#pragma unroll
+    for (int z = 0; z < D; z++)
+        if (z < S.d) atomicMax(&se[z], e[z]);
+    atomicMax(&se[D], e[D]);
+    __syncthreads();
+    if (threadIdx.x < S.d) atomicMax(S.qexp + threadIdx.x, se[threadIdx.x]);
+    if (threadIdx.x == 0) atomicMax(S.qexp + S.d, se[D]);
+}
+
 lk_status launch_scan_exp(const DevState& S, int sms, cudaStream_t st) {
+    if (S.d <= 8) {
+        const int grid = grid_for(S.n, kThreads, sms * 4);
+        if (S.d <= 2) k_scan_exp_small<2><<<grid, kThreads, 0, st>>>(S);
+        else if (S.d <= 4) k_scan_exp_small<4><<<grid, kThreads, 0, st>>>(S);
+        else k_scan_exp_small<8><<<grid, kThreads, 0, st>>>(S);
+        LK_LAUNCH_CHECK();
+        return LK_OK;
+    }
     size_t smem = (size_t)8 * (S.d + 1) * sizeof(int);
     if (smem > 48 * 1024)
         LK_CUDA_CHECK(cudaFuncSetAttribute(k_scan_exp, cudaFuncAttributeMaxDynamicSharedMemorySize,

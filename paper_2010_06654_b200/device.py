@@ -136,6 +136,7 @@ class DeviceLloyd:
         self.strategy = strategy
         self.group_seed = group_seed
         self.groups_req = int(groups)
+        self.graph_ready = False
         self.k = int(k)
         self.t_max = int(t_max)
 
@@ -289,22 +290,32 @@ class DeviceLloyd:
                   "lk_profile_read")
         return ms.value, nl.value
 
-    def capture(self, t: int):
-        """CUDA graphs of one iteration t >= 2 (assign, update).  The
-        iteration index lives on the device, so the same graphs replay every
-        later iteration (single process only: NCCL stays outside)."""
-        torch = _torch()
+    def capture(self, t: int) -> bool:
+        """Capture one iteration t >= 2 (assign + update) as a CUDA graph owned
+        by the native context (lk_graph_capture).  The iteration index lives
+        on the device, so the graph replays every later iteration.  Single
+        process only: with a communicator the all-reduce stays outside."""
         if t < 2 or self.comm is not None:
-            return None
-        with torch.cuda.device(self.dev):
-            ga, gu = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-            with torch.cuda.graph(ga):
-                nat.check(self.lib.lk_step_assign(self.ctx, int(t), self.stream_handle()),
-                          "lk_step_assign")
-            with torch.cuda.graph(gu):
-                nat.check(self.lib.lk_step_update(self.ctx, int(t), self.stream_handle()),
-                          "lk_step_update")
-        return ga, gu
+            return False
+        nat.check(self.lib.lk_graph_capture(self.ctx, int(t), self.stream_handle()),
+                  "lk_graph_capture")
+        self.graph_ready = True
+        return True
+
+    def replay(self):
+        nat.check(self.lib.lk_graph_replay(self.ctx, self.stream_handle()), "lk_graph_replay")
+
+    def rebind(self, data):
+        """Upload new points into this context (same n, d, dtype class)."""
+        torch = _torch()
+        src = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(data))
+        if tuple(src.shape) != (self.n, self.d):
+            raise ContractError("rebind: shape mismatch")
+        has_x64 = self.x64 is not None
+        if src.dtype == torch.float64 and not has_x64:
+            if not bool(torch.equal(src.to(torch.float32).to(torch.float64), src)):
+                raise ContractError("rebind: fp64 input not fp32-exact on an fp32 context")
+        self._bind(src, has_x64)
 
     def run(self, init, *, record_history: bool = True, check_every: int = 4,
             use_graphs: bool = True):
@@ -330,27 +341,26 @@ class DeviceLloyd:
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
                    torch.cuda.Event(enable_timing=True)) for _ in range(T)]
             log_parts = []      # (iteration, rows, labels) drained from the device log
-            graphs = None
+            graphs = False
             iters = T
             converged = False
             checked = 0
             for t in range(1, T + 1):
                 e0, e1, e2 = ev[t - 1]
                 if t == 2 and use_graphs:
-                    graphs = self.capture(2)
+                    # the graph of a cached context is reused across calls
+                    graphs = self.graph_ready or self.capture(2)
                 e0.record(stream)
-                if graphs is not None:
-                    graphs[0].replay()
+                if graphs:
+                    self.replay()  # assign + update; timed as one phase
+                    e1.record(stream)
                 else:
                     nat.check(self.lib.lk_step_assign(self.ctx, t, self.stream_handle()),
                               "lk_step_assign")
-                if self.comm is not None:
-                    import torch.distributed as dist
-                    dist.all_reduce(self.delta, group=self.comm)
-                e1.record(stream)
-                if graphs is not None:
-                    graphs[1].replay()
-                else:
+                    if self.comm is not None:
+                        import torch.distributed as dist
+                        dist.all_reduce(self.delta, group=self.comm)
+                    e1.record(stream)
                     nat.check(self.lib.lk_step_update(self.ctx, t, self.stream_handle()),
                               "lk_step_update")
                 e2.record(stream)
@@ -412,5 +422,5 @@ class DeviceLloyd:
             log = np.empty((0, 2), dtype=np.int32)
         for t in range(t0, t1):
             seg = log[offs[t - t0]: offs[t - t0 + 1]]
-            parts.append((t, seg[:, 0].astype(np.int64), seg[:, 1].astype(np.int64)))
+            parts.append((t, seg[:, 0], seg[:, 1]))
         self.hlog_off[t1].zero_()

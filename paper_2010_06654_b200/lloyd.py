@@ -97,20 +97,55 @@ def _iteration_stats(strategy: str, t: int, rec, n: int, k: int) -> IterationSta
                           data_accesses=dist + n, **kw)
 
 
+# One cached device context (workspace, native context, captured iteration
+# graph) per process, reused by the next call with the same shapes -- like an
+# FFT plan.  Every call still uploads its own points and init.
+_ENGINE_CACHE: dict = {}
+
+
+def _engine(x, k, strategy, t_max, kernel, device, groups, group_seed, record_history):
+    from .device import DeviceLloyd
+    import torch
+
+    is64 = (x.dtype == np.float64) if isinstance(x, np.ndarray) else (x.dtype == torch.float64)
+    dev = torch.cuda.current_device() if device is None else device
+    key = (x.shape[0], x.shape[1], k, strategy, t_max, kernel, str(dev), groups, bool(record_history))
+    eng = _ENGINE_CACHE.get("engine")
+    if eng is not None and eng.ctx and _ENGINE_CACHE.get("key") == key and not is64 \
+            and eng.x64 is None:
+        eng.rebind(x)
+        eng.group_seed = group_seed
+        return eng
+    if eng is not None:
+        eng.close()
+        _ENGINE_CACHE.clear()
+    eng = DeviceLloyd(x, k, strategy, t_max, kernel=kernel, device=device, groups=groups,
+                      group_seed=group_seed, record_history=record_history)
+    if eng.x64 is None:
+        _ENGINE_CACHE.update(engine=eng, key=key)
+    return eng
+
+
+def release_device_cache():
+    """Free the cached device context (its HBM workspace)."""
+    eng = _ENGINE_CACHE.pop("engine", None)
+    _ENGINE_CACHE.clear()
+    if eng is not None:
+        eng.close()
+
+
 def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: RunContext, *,
                label: str, kernel: str = "auto", record_history: bool = True,
                device=None, groups: int = 0, group_seed: int = 0) -> RunResult:
     """Shared body of run_lloyd / run_pruner / run_engine on one GPU."""
-    from .device import DeviceLloyd
-
     n = x.shape[0]
     init_copy = centers.copy()
-    eng = DeviceLloyd(x, k, strategy, t_max, kernel=kernel, device=device, groups=groups,
-                      group_seed=group_seed, record_history=record_history)
+    eng = _engine(x, k, strategy, t_max, kernel, device, groups, group_seed, record_history)
     try:
         out = eng.run(centers, record_history=record_history)
     finally:
-        eng.close()
+        if _ENGINE_CACHE.get("engine") is not eng:
+            eng.close()
     stats = [_iteration_stats(strategy, t + 1, r, n, k) for t, r in enumerate(out["records"])]
     before = ctx.counters.copy()
     for s in stats:
