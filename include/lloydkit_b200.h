@@ -171,7 +171,10 @@ lk_status lk_step_assign(lk_ctx *ctx, int32_t t, void *stream);
 lk_status lk_step_update(lk_ctx *ctx, int32_t t, void *stream);
 
 /* CUDA graph of one iteration t >= 2 (lk_step_assign + lk_step_update),
- * captured natively on the caller's stream and owned by the context; replays
+ * captured natively on a context-owned stream (the caller's stream may be the
+ * legacy default stream, which cannot be captured; `stream` is unused) and
+ * owned by the context; lk_graph_replay launches it on the caller's stream;
+ * replays
  * are valid for every later iteration because the iteration index is
  * device-resident.  Single-process only (no collective inside). */
 lk_status lk_graph_capture(lk_ctx *ctx, int32_t t, void *stream);

@@ -205,6 +205,9 @@ struct lk_ctx {
     // one-iteration CUDA graph (lk_graph_capture)
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
+    // capture happens on a context-owned stream: the caller's stream may be
+    // the legacy default stream, which cannot be captured
+    cudaStream_t cap_stream = nullptr;
     // profiling
     bool profile;
     struct Rec { int cls; cudaEvent_t a, b; };
@@ -401,6 +404,7 @@ lk_status lk_ctx_destroy(lk_ctx* c) {
     if (!c) return LK_OK;
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     if (c->graph) cudaGraphDestroy(c->graph);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     for (auto& r : c->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -695,7 +699,9 @@ lk_status lk_graph_capture(lk_ctx* c, int32_t t, void* stream) {
         set_error("lk_graph_capture: iteration 1 takes the first-iteration path; capture t >= 2");
         return LK_ERR_ARG;
     }
-    cudaStream_t st = (cudaStream_t)stream;
+    (void)stream;  // nothing executes during capture; replay uses the caller's stream
+    if (!c->cap_stream) LK_CUDA_CHECK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t st = c->cap_stream;
     if (c->graph_exec) {
         cudaGraphExecDestroy(c->graph_exec);
         c->graph_exec = nullptr;
@@ -707,8 +713,8 @@ lk_status lk_graph_capture(lk_ctx* c, int32_t t, void* stream) {
     const bool prof = c->profile;
     c->profile = false;  // no event records inside the graph
     LK_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    lk_status s1 = lk_step_assign(c, t, stream);
-    lk_status s2 = s1 == LK_OK ? lk_step_update(c, t, stream) : s1;
+    lk_status s1 = lk_step_assign(c, t, (void*)st);
+    lk_status s2 = s1 == LK_OK ? lk_step_update(c, t, (void*)st) : s1;
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(st, &g);
     c->profile = prof;
