@@ -39,7 +39,7 @@ enum InternalBuf {
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
-    B_COUNT_
+    B_SELF, B_COUNT_
 };
 
 struct Layout {
@@ -70,7 +70,8 @@ static int32_t nlb_for(const lk_config& c, int32_t* groups) {
     if (g > c.k) g = c.k;
     // the warp-per-row Yinyang path works on 8/16/32 group slots; extra slots
     // are empty groups (no members, never binding)
-    if (is_group_strategy(c.strategy) && g <= 32 && c.d <= 32) g = g <= 8 ? 8 : (g <= 16 ? 16 : 32);
+    if (is_group_strategy(c.strategy) && g <= 32 && c.d <= 32)
+        g = g <= 4 ? 4 : (g <= 8 ? 8 : (g <= 16 ? 16 : 32));
     *groups = g;
     return g < 1 ? 1 : g;
 }
@@ -163,6 +164,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_YPAIRS4] = (uint64_t)bcap * L->groups * 8;
         L->size[B_YBUCKET] = (uint64_t)(L->groups + 1) * 8;
     }
+    L->size[B_SELF] = sizeof(lk::DevState);
     uint64_t off = 0;
     for (int b = 0; b < B_COUNT_; b++) {
         L->off[b] = off;
@@ -388,10 +390,13 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.pw_len = (int32_t)prog.size();
     LK_CUDA_CHECK(cudaMemcpy(S.pw_prog, prog.data(), prog.size() * 4, cudaMemcpyHostToDevice));
     LK_CUDA_CHECK(cudaMemset(S.done, 0, 16));
+    S.self = buf<lk::DevState>(c, B_SELF);
+    LK_CUDA_CHECK(cudaMemcpy((void*)S.self, &S, sizeof(S), cudaMemcpyHostToDevice));
     // every kernel attribute is set here, never inside a (possibly captured) step
     lk_status as = lkh::init_simt_attributes();
     if (as == LK_OK && S.Xlo) as = lkh::init_tc_attributes();
     if (as == LK_OK && S.Cg) as = lkh::init_yy_attributes();
+    if (as == LK_OK && S.Cg) as = lkh::init_fused_attributes();
     if (as != LK_OK) {
         delete c;
         return as;
@@ -610,6 +615,29 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             c->launches += 1;
         } else if (is_group_strategy(c->cfg.strategy)) {
             const bool full_only = use_tc && !lkh::yy_masked(S);
+            if (lkh::yy_fused_ok(S)) {
+                // one kernel: filter, group scans, certified merge, refinement
+                // deltas (lk_yy_fused.cu); then the fp64 recheck of the rows it
+                // left ambiguous, which refines the rows it moves itself
+                {
+                    ProfScope p(c, 1, st);
+                    s = lkh::launch_yy_fused(S, stat, buf<double>(c, B_QSCALE), c->sms, st);
+                    if (s != LK_OK) return s;
+                }
+                {
+                    ProfScope p(c, 2, st);
+                    s = lkh::launch_recheck(S, stat, n, c->sms, st, buf<double>(c, B_QSCALE));
+                    if (s != LK_OK) return s;
+                }
+                c->launches += 2;
+                if (S.hlog) {
+                    ProfScope p(c, 3, st);
+                    s = lkh::launch_log_history(S, c->sms, st);
+                    if (s != LK_OK) return s;
+                    c->launches += 1;
+                }
+                return LK_OK;
+            } else {
             {
                 ProfScope p(c, 1, st);
                 s = lkh::launch_yy_filter(S, stat, c->sms, st, full_only);
@@ -631,6 +659,7 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
                        : lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
             if (s != LK_OK) return s;
             c->launches += 4;
+            }
         } else {
             {
                 ProfScope p(c, 1, st);

@@ -86,6 +86,9 @@ struct DevState {
     int2* ypairs2;          // [t, bucket_cap] scans bucketed by group: (row, result slot)
     int64_t* ybucket;       // [t] bucket fill counts
     int64_t bucket_cap;
+    // a copy of this struct in device memory, for out-of-line device
+    // functions (a reference to the kernel parameter would copy it to the stack)
+    const DevState* self;
 };
 
 // Finalize a row's lower bounds from one certified bound on every non-winning

@@ -9,8 +9,9 @@ namespace lkh {
 lk_status launch_assign_simt(const lk::DevState& S, const int32_t* rowlist,
                              const int64_t* rowcount, int64_t* stat, int64_t max_rows, int sms,
                              cudaStream_t st);
+// qscale_inline: also add the refinement deltas of the rows it moves
 lk_status launch_recheck(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
-                         cudaStream_t st);
+                         cudaStream_t st, const double* qscale_inline = nullptr);
 lk_status launch_recheck_cand(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
                               cudaStream_t st);
 lk_status launch_filter_hamerly(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
@@ -25,6 +26,11 @@ lk_status init_yy_attributes();
 lk_status launch_scan_exp(const lk::DevState& S, int sms, cudaStream_t st);
 
 bool yy_masked(const lk::DevState& S);
+// one-kernel Yinyang iteration (lk_yy_fused.cu), d <= 32 and t <= 32
+bool yy_fused_ok(const lk::DevState& S);
+lk_status init_fused_attributes();
+lk_status launch_yy_fused(const lk::DevState& S, int64_t* stat, const double* qscale, int sms,
+                          cudaStream_t st);
 lk_status launch_yy_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 // full_only: every row failing the bounds is rescanned in full (tensor-core runs with d > 32)
 lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,

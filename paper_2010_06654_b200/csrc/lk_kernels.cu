@@ -19,6 +19,7 @@
 #include <math.h>
 
 #include "lk_common.cuh"
+#include "lk_exact.cuh"
 #include "lk_internal.h"
 
 namespace lk {
@@ -232,76 +233,11 @@ __global__ void __launch_bounds__(kThreads) k_assign_gen(DevState S, const int32
 
 constexpr int kRcWarps = 4;
 
-// Sum of (x_z - c_z)^2 over [start, start+len) exactly as numpy's pairwise_sum
-// leaf does it: sequential from 0 below 8 terms, else 8 strided accumulators
-// combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail in order.
-template <typename TX>
-__device__ __forceinline__ double pw_leaf(const TX* x, const double* c, int start, int len) {
-    if (len < 8) {
-        double res = 0.0;
-        for (int z = start; z < start + len; z++) {
-            double t = __dsub_rn((double)x[z], c[z]);
-            res = __dadd_rn(res, __dmul_rn(t, t));
-        }
-        return res;
-    }
-    double r[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-        double t = __dsub_rn((double)x[start + j], c[start + j]);
-        r[j] = __dmul_rn(t, t);
-    }
-    int i = 8;
-    const int main_end = len - (len % 8);
-    for (; i < main_end; i += 8) {
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-            double t = __dsub_rn((double)x[start + i + j], c[start + i + j]);
-            r[j] = __dadd_rn(r[j], __dmul_rn(t, t));
-        }
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < len; i++) {
-        double t = __dsub_rn((double)x[start + i], c[start + i]);
-        res = __dadd_rn(res, __dmul_rn(t, t));
-    }
-    return res;
-}
-
-template <typename TX>
-__device__ double pw_dist2(const TX* x, const double* c, const int32_t* prog, int plen) {
-    if (plen == 3) return pw_leaf(x, c, __ldg(prog + 1), __ldg(prog + 2));
-    double st[24];
-    int sp = 0;
-    for (int p = 0; p < plen; p += 3) {
-        int op = __ldg(prog + p);
-        if (op == 0) {
-            st[sp++] = pw_leaf(x, c, __ldg(prog + p + 1), __ldg(prog + p + 2));
-        } else {
-            double b = st[--sp];
-            double a = st[--sp];
-            st[sp++] = __dadd_rn(a, b);
-        }
-    }
-    return st[0];
-}
-
-// One block per flagged row: every thread takes k/256 centroids, so the
-// per-thread chain of dependent global loads stays short.
-__device__ __forceinline__ void merge_top2(double& b1, int& j1, double& b2, double ob1, int oj1,
-                                           double ob2) {
-    const bool mine = (b1 < ob1) || (b1 == ob1 && j1 < oj1);
-    if (mine) {
-        b2 = fmin(b2, ob1);
-    } else {
-        b2 = fmin(ob2, b1);
-        b1 = ob1;
-        j1 = oj1;
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) k_recheck_fp64(DevState S, int64_t* stat) {
+// qscale_inline != nullptr: the assignment kernel already refined its own
+// moved rows (lk_yy_fused.cu), so the rows moved here add their fixed-point
+// deltas and changed count directly.
+__global__ void __launch_bounds__(kThreads) k_recheck_fp64(DevState S, int64_t* stat,
+                                                           const double* qscale_inline) {
     if (*S.done) return;
     extern __shared__ double xr[];  // [d]
     __shared__ double rb1[kThreads / 32], rb2[kThreads / 32];
@@ -339,6 +275,10 @@ __global__ void __launch_bounds__(kThreads) k_recheck_fp64(DevState S, int64_t* 
                 unsigned long long p =
                     atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), 1ull);
                 S.moved[p] = make_int2((int)row, old);
+                if (qscale_inline) {
+                    refine_move(S, qscale_inline, row, old, j1);
+                    atomicAdd((unsigned long long*)(S.delta + (int64_t)S.k * S.d + 2 * S.k), 1ull);
+                }
             }
         }
     }
@@ -448,9 +388,6 @@ __global__ void __launch_bounds__(kThreads) k_filter_hamerly(DevState S, int64_t
 // ---------------------------------------------------------------------------
 // K4: fixed-point member-sum deltas of the moved rows
 
-__device__ __forceinline__ double load_x(const DevState& S, int64_t row, int z) {
-    return S.X64 ? S.X64[row * S.d + z] : (double)__ldg(S.X32 + row * S.ldx + z);
-}
 
 // G lanes per moved row (G = power of two >= min(d, 32)); warp-uniform loop.
 template <int G>
@@ -796,10 +733,10 @@ lk_status launch_assign_simt(const DevState& S, const int32_t* rowlist, const in
 }
 
 lk_status launch_recheck(const DevState& S, int64_t* stat, int64_t max_rows, int sms,
-                         cudaStream_t st) {
+                         cudaStream_t st, const double* qscale_inline) {
     size_t smem = (size_t)S.d * sizeof(double);  // <= 48 KB for d <= 6144
     int grid = grid_for(max_rows, 1, sms * 2);
-    k_recheck_fp64<<<grid, kThreads, smem, st>>>(S, stat);
+    k_recheck_fp64<<<grid, kThreads, smem, st>>>(S, stat, qscale_inline);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
