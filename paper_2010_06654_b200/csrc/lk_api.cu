@@ -39,7 +39,7 @@ enum InternalBuf {
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
-    B_SELF, B_COUNT_
+    B_SELF, B_DCUM, B_DGCUM, B_GLB, B_COUNT_
 };
 
 struct Layout {
@@ -163,6 +163,12 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->bucket_cap = bcap;
         L->size[B_YPAIRS4] = (uint64_t)bcap * L->groups * 8;
         L->size[B_YBUCKET] = (uint64_t)(L->groups + 1) * 8;
+        if (L->groups <= 32 && c.d <= 32) {
+            // lazy (drift-offset) bounds of the fused path
+            L->size[B_DCUM] = (uint64_t)k * 4;
+            L->size[B_DGCUM] = (uint64_t)L->groups * 4;
+            L->size[B_GLB] = (uint64_t)n * 4;
+        }
     }
     L->size[B_SELF] = sizeof(lk::DevState);
     uint64_t off = 0;
@@ -390,6 +396,10 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.pw_len = (int32_t)prog.size();
     LK_CUDA_CHECK(cudaMemcpy(S.pw_prog, prog.data(), prog.size() * 4, cudaMemcpyHostToDevice));
     LK_CUDA_CHECK(cudaMemset(S.done, 0, 16));
+    S.lazy = L.size[B_GLB] > 0 ? 1 : 0;
+    S.dcum = buf<float>(c, B_DCUM);
+    S.dgcum = buf<float>(c, B_DGCUM);
+    S.glb = buf<float>(c, B_GLB);
     S.self = buf<lk::DevState>(c, B_SELF);
     LK_CUDA_CHECK(cudaMemcpy((void*)S.self, &S, sizeof(S), cudaMemcpyHostToDevice));
     // every kernel attribute is set here, never inside a (possibly captured) step
@@ -574,6 +584,10 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     LK_CUDA_CHECK(cudaMemsetAsync(S.cur, 0, c->L.size[B_CUR], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.hlog_off, 0, c->L.size[B_HLOG_OFF], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.sse, 0, c->L.size[B_SSE], st));
+    if (S.lazy) {
+        LK_CUDA_CHECK(cudaMemsetAsync(S.dcum, 0, c->L.size[B_DCUM], st));
+        LK_CUDA_CHECK(cudaMemsetAsync(S.dgcum, 0, c->L.size[B_DGCUM], st));
+    }
     const int kpad = (int)((k + 255) / 256 * 256);
     k_init_centroids<<<(kpad + 7) / 8, 256, 0, st>>>(S, kpad);
     LK_LAUNCH_CHECK();

@@ -86,16 +86,37 @@ struct DevState {
     int2* ypairs2;          // [t, bucket_cap] scans bucketed by group: (row, result slot)
     int64_t* ybucket;       // [t] bucket fill counts
     int64_t bucket_cap;
+    // drift-offset ("lazy") bound encoding of the fused Yinyang path
+    // (lk_yy_fused.cu): bounds are stored against cumulative drifts, so a row
+    // whose bounds still prune is never rewritten
+    int32_t lazy;
+    float* dcum;            // [k] cumulative centroid drift (rounded up)
+    float* dgcum;           // [t] cumulative group drift (rounded up); scal[4] = cumulative max drift
+    float* glb;             // [n] stored global lower bound (min over the groups)
     // a copy of this struct in device memory, for out-of-line device
     // functions (a reference to the kernel parameter would copy it to the stack)
     const DevState* self;
 };
 
+// Stored form of a certified upper bound U on d(x, c_label): in the lazy
+// encoding ub_s = U - Dc[label] rounded up, so that at any later iteration
+// ub_s + Dc_now[label] (rounded up) >= U + the label's drift since (Dc only
+// grows, by rounded-up drifts).
+__device__ __forceinline__ float store_ub(const DevState& S, float U, int label) {
+    return S.lazy ? __fsub_ru(U, S.dcum[label]) : U;
+}
+
 // Finalize a row's lower bounds from one certified bound on every non-winning
 // centroid (Hamerly: the single slot; Yinyang: every group slot).
 // The bound table is group-major, lb[g * n + row], so a warp's loads of one
-// group's bounds are coalesced.
+// group's bounds are coalesced.  Lazy encoding: lb_s[g] = v + Dg[g] and
+// glb_s = v + Dm, rounded down.
 __device__ __forceinline__ void write_lb_all(const DevState& S, int64_t row, float v) {
+    if (S.lazy) {
+        for (int g = 0; g < S.nlb; g++) S.lb[(int64_t)g * S.n + row] = __fadd_rd(v, S.dgcum[g]);
+        S.glb[row] = __fadd_rd(v, S.scal[4]);
+        return;
+    }
     for (int g = 0; g < S.nlb; g++) S.lb[(int64_t)g * S.n + row] = v;
 }
 

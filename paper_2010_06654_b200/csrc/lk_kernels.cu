@@ -43,7 +43,7 @@ __device__ __forceinline__ void row_finish(const DevState& S, bool valid, int64_
         moved = (old != j1);
         S.labels[row] = j1;
         if (S.strategy != LK_STRAT_LLOYD) {
-            S.ub[row] = U1;
+            S.ub[row] = store_ub(S, U1, j1);
             write_lb_all(S, row, fmaxf(L2, 0.0f));
         }
     }
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads) k_recheck_fp64(DevState S, int64_t* 
             const int old = S.labels[row];
             S.labels[row] = j1;
             if (S.strategy != LK_STRAT_LLOYD) {
-                S.ub[row] = __double2float_ru(b1 * (1.0 + 1e-12));
+                S.ub[row] = store_ub(S, __double2float_ru(b1 * (1.0 + 1e-12)), j1);
                 write_lb_all(S, row, isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12)));
             }
             if (old != j1) {
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) k_recheck_cand(DevState S, int64_t* 
                 mv = old != j1;
                 S.labels[row] = j1;
                 if (S.strategy != LK_STRAT_LLOYD) {
-                    S.ub[row] = __double2float_ru(b1 * (1.0 + 1e-12));
+                    S.ub[row] = store_ub(S, __double2float_ru(b1 * (1.0 + 1e-12)), j1);
                     const float l2 = isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12));
                     write_lb_all(S, row, fminf(l2, S.cand_lb[e]));
                 }
@@ -497,7 +497,9 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
         if (S.cn2) S.cn2[j] = (float)c2;
         S.counts[j] = cnt;
         S.qsum[j] = qs;
-        S.drift[j] = drift2 > 0.0 ? __double2float_ru(sqrt(drift2) * (1.0 + 1e-12)) : 0.f;
+        const float dj = drift2 > 0.0 ? __double2float_ru(sqrt(drift2) * (1.0 + 1e-12)) : 0.f;
+        S.drift[j] = dj;
+        if (S.lazy) S.dcum[j] = __fadd_ru(S.dcum[j], dj);
         S.cnorm[j] = __double2float_ru(sqrt(cn2) * (1.0 + 1e-12));
         sse_part[j] = cnt > 0 ? ((double)qs * qinv[S.d] - s2 / (double)cnt) : 0.0;
     }
@@ -563,6 +565,13 @@ __global__ void __launch_bounds__(1024) k_update_global(DevState S, const double
         for (int g = tid; g < S.t_groups; g += blockDim.x) S.gdrift[g] = 0.f;
         __syncthreads();
         for (int j = tid; j < S.k; j += blockDim.x) atomic_max_pos(S.gdrift + S.group_of[j], S.drift[j]);
+        if (S.lazy) {
+            // cumulative group and global drifts of the lazy bound encoding
+            __syncthreads();
+            for (int g = tid; g < S.t_groups; g += blockDim.x)
+                S.dgcum[g] = __fadd_ru(S.dgcum[g], S.gdrift[g]);
+            if (tid == 0) S.scal[4] = __fadd_ru(S.scal[4], S.scal[1]);
+        }
     }
 }
 

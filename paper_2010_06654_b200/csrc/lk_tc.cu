@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     moved = old != j1;
                     S.labels[row] = j1;
                     if (S.strategy != LK_STRAT_LLOYD) {
-                        S.ub[row] = __fsqrt_ru(fmaxf(U, 0.f));
+                        S.ub[row] = store_ub(S, __fsqrt_ru(fmaxf(U, 0.f)), j1);
                         write_lb_all(S, row, isinf(L2) ? INFINITY : __fsqrt_rd(fmaxf(L2, 0.f)));
                     }
                 } else {

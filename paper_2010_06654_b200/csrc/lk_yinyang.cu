@@ -184,150 +184,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_yinyang(DevState S, int6
     }
 }
 
-// ---------------------------------------------------------------------------
-// Specialised path for T <= 32 groups: the filter emits one worklist entry per
-// failing row with a bitmask of the groups to scan; one warp then scans those
-// groups for that row (lane g keeps group g's result), certifies the label and
-// rewrites the bounds.  No pair list, no second pass.
-
-// Block-wide: counts of two predicates appended to two worklists + a plain
-// count, with one global atomic per counter per block.  Block-uniform call.
-__device__ __forceinline__ void block_append2(bool pa, bool pb, unsigned long long* ca,
-                                              unsigned long long* cb, int64_t* cact, bool act,
-                                              unsigned long long* scr, int64_t& posa,
-                                              int64_t& posb) {
-    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const unsigned ma = __ballot_sync(LK_FULL_MASK, pa), mb = __ballot_sync(LK_FULL_MASK, pb),
-                   mc = __ballot_sync(LK_FULL_MASK, act);
-    if (lane_id() == 0) {
-        scr[warp] = __popc(ma);
-        scr[nw + warp] = __popc(mb);
-        scr[2 * nw + warp] = __popc(mc);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long ta = 0, tb = 0, tc = 0;
-        for (int w = 0; w < nw; w++) {
-            unsigned long long a = scr[w], b = scr[nw + w];
-            scr[w] = ta;
-            scr[nw + w] = tb;
-            ta += a;
-            tb += b;
-            tc += scr[2 * nw + w];
-        }
-        scr[3 * nw] = ta ? atomicAdd(ca, ta) : 0ull;
-        scr[3 * nw + 1] = tb ? atomicAdd(cb, tb) : 0ull;
-        if (tc) atomicAdd((unsigned long long*)cact, tc);
-    }
-    __syncthreads();
-    const unsigned lt = lanemask_lt();
-    posa = pa ? (int64_t)(scr[3 * nw] + scr[warp] + __popc(ma & lt)) : -1;
-    posb = pb ? (int64_t)(scr[3 * nw + 1] + scr[nw + warp] + __popc(mb & lt)) : -1;
-    __syncthreads();
-}
-
-template <int T>
-__global__ void __launch_bounds__(kThreads) k_filter_yinyang_m(DevState S, int64_t* stat) {
-    if (*S.done) return;
-    __shared__ float gd[T];
-    __shared__ int bcnt[T];
-    __shared__ int64_t bbase[T];
-    __shared__ unsigned long long scr[3 * (kThreads / 32) + 2];
-    __shared__ unsigned long long rsc[kThreads / 32 + 1];
-    if (threadIdx.x < T) {
-        gd[threadIdx.x] = S.gdrift[threadIdx.x];
-        bcnt[threadIdx.x] = 0;
-    }
-    __syncthreads();
-    const float rho = simt_rel_err(S.d);
-    const int64_t ln = S.n;
-    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < S.n;
-         base += (int64_t)gridDim.x * kThreads) {
-        const int64_t i = base + threadIdx.x;
-        const bool valid = i < S.n;
-        bool active = false, need = false;
-        unsigned mask = 0;
-        int apos = 0;
-        float acc_a = 0.f, u = 0.f, lun = INFINITY, xn = 0.f;
-        if (valid) {
-            const int a = S.labels[i];
-            u = __fadd_ru(S.ub[i], S.drift[a]);
-            float v[T];
-            const float* lp = S.lb + i;
-#pragma unroll
-            for (int g = 0; g < T; g++) v[g] = __ldcs(lp + g * ln);
-            float gmin = INFINITY;
-            float* sp = S.lb + i;
-#pragma unroll
-            for (int g = 0; g < T; g++) {
-                v[g] = fmaxf(__fsub_rd(v[g], gd[g]), 0.f);
-                gmin = fminf(gmin, v[g]);
-                __stcs(sp + g * ln, v[g]);
-            }
-            // Hamerly's separation test holds for every bound family
-            gmin = fmaxf(gmin, S.s_half[a]);
-            if (!(gmin > u)) {
-                active = true;
-                const float* xp = S.X32 + i * S.ldx;
-                acc_a = dist2_row(S, xp, a);
-                xn = xnorm(S, xp);
-                apos = S.ginv[a];
-                const float U = (sqrtf(acc_a) + kU32 * (xn + S.cnorm[a])) * (1.0f + rho);
-                u = fminf(u, U);
-                need = !(gmin > u);
-                if (need) {
-#pragma unroll
-                    for (int g = 0; g < T; g++) {
-                        if (v[g] > u) lun = fminf(lun, v[g]);
-                        else mask |= 1u << g;
-                    }
-                }
-            }
-            S.ub[i] = u;
-        }
-        int64_t wpos, unused;
-        block_append2(need, false, (unsigned long long*)(stat + LK_STAT_YWL),
-                      (unsigned long long*)(stat + LK_STAT_PAIRS), stat + LK_STAT_ACTIVE, active,
-                      scr, wpos, unused);
-        // each worklist row owns a contiguous range of result slots (one per scanned group)
-        const int cnt = __popc(mask);
-        const int64_t poff = block_reserve(cnt, (unsigned long long*)(stat + LK_STAT_PAIRS), rsc);
-        const bool fits = need && poff + cnt <= S.pair_cap;
-        // per-group buckets (region g of ypairs4 holds group g's scans): shared
-        // atomics for the block-local ranks, one global atomic per group
-        int rank[T];
-#pragma unroll
-        for (int g = 0; g < T; g++) rank[g] = (fits && ((mask >> g) & 1u)) ? atomicAdd(&bcnt[g], 1) : -1;
-        __syncthreads();
-        if (threadIdx.x < T) {
-            const int c = bcnt[threadIdx.x];
-            bbase[threadIdx.x] = c ? (int64_t)atomicAdd((unsigned long long*)(S.ybucket + threadIdx.x),
-                                                         (unsigned long long)c)
-                                   : 0;
-            bcnt[threadIdx.x] = 0;
-        }
-        __syncthreads();
-        if (need) {
-            S.ywl[wpos] = make_int4((int)i, (int)mask, __float_as_int(acc_a), __float_as_int(xn));
-            S.ylun[wpos] = make_float2(lun, 0.f);
-            int slot = (int)poff;
-            bool lost = false;  // a bucket was full: this row gets a full rescan instead
-#pragma unroll
-            for (int g = 0; g < T; g++) {
-                if (rank[g] >= 0) {
-                    const int64_t q = bbase[g] + rank[g];
-                    if (q < S.bucket_cap)
-                        S.ypairs2[(int64_t)g * S.bucket_cap + q] = make_int2((int)i, slot);
-                    else
-                        lost = true;
-                    slot++;
-                }
-            }
-            S.yaux[wpos] = make_int2(fits && !lost ? (int)poff : -1, apos);
-        }
-    }
-}
-
 template <int DP>
 __device__ __forceinline__ float dist2_dp(const float (&xr)[DP], const float* cp, int d) {
     float acc = 0.f;
@@ -340,141 +196,6 @@ __device__ __forceinline__ float dist2_dp(const float (&xr)[DP], const float* cp
         }
     }
     return acc;
-}
-
-// One thread per (row, group) scan, pairs sorted by group: a warp's lanes
-// walk the same group, so the centroid reads are shared-memory broadcasts.
-template <int DP, bool STAGED>
-__global__ void __launch_bounds__(kThreads) k_yy_sorted_scan(DevState S, int64_t* stat) {
-    if (*S.done) return;
-    extern __shared__ __align__(16) float csm[];
-    const int T = S.t_groups;
-    const int gB = blockIdx.y;  // this block's group bucket
-    const int64_t np_ = min(S.ybucket[gB], S.bucket_cap);
-    if ((int64_t)blockIdx.x * kThreads >= np_) return;
-    const int k = S.k;
-    int* s_goff = reinterpret_cast<int*>(csm + (STAGED ? k * S.ldc : 0));
-    int* s_gperm = s_goff + T + 1;
-    int* s_ginv = s_gperm + k;
-    if (STAGED) {
-        const int tot = k * S.ldc;
-        for (int e = threadIdx.x; e < tot; e += kThreads) csm[e] = S.Cg[e];
-    }
-    for (int e = threadIdx.x; e < k; e += kThreads) {
-        s_gperm[e] = S.gperm[e];
-        s_ginv[e] = S.ginv[e];
-    }
-    for (int e = threadIdx.x; e <= T; e += kThreads) s_goff[e] = S.goff[e];
-    __syncthreads();
-    const float* __restrict__ cg = STAGED ? csm : S.Cg;
-    const int ldc = S.ldc;
-    int64_t ndist = 0;
-    const int2* __restrict__ bucket = S.ypairs2 + (int64_t)gB * S.bucket_cap;
-    for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < np_;
-         q += (int64_t)gridDim.x * kThreads) {
-        const int2 pr = bucket[q];
-        const int64_t row = pr.x;
-        const int g = gB, apos = s_ginv[S.labels[row]];
-        const int slot = pr.y;
-        float xr[DP];
-        const float* xp = S.X32 + row * S.ldx;
-#pragma unroll
-        for (int z = 0; z < DP; z++) xr[z] = z < S.d ? __ldg(xp + z) : 0.f;
-        const int j0 = s_goff[g], j9 = s_goff[g + 1];
-        float b1 = INFINITY, b2 = INFINITY;
-        int p1 = -1;
-        for (int jj = j0; jj < j9; jj++) {
-            float acc = dist2_dp<DP>(xr, cg + jj * ldc, S.d);
-            acc = (jj == apos) ? INFINITY : acc;  // the label competes via its tightened bound
-            if (acc < b1) { b2 = b1; b1 = acc; p1 = jj; }
-            else b2 = fminf(b2, acc);
-        }
-        ndist += (j9 - j0) - (apos >= j0 && apos < j9 ? 1 : 0);
-        S.yres[slot] = make_float4(__int_as_float(p1 >= 0 && !isinf(b1) ? s_gperm[p1] : -1), b1, b2, 0.f);
-    }
-    warp_add(ndist, stat + LK_STAT_DIST);
-}
-
-// Per worklist row: certify the label from the scanned groups' top-2, write
-// the new group bounds; ambiguous rows -> exact fp64 recheck, rows whose
-// result range did not fit -> full SIMT rescan.
-template <int T>
-__global__ void __launch_bounds__(kThreads) k_yy_merge_m(DevState S, int64_t* stat) {
-    if (*S.done) return;
-    __shared__ unsigned long long scr[kThreads / 32 + 1];
-    const int64_t m = stat[LK_STAT_YWL];
-    const float rho = simt_rel_err(S.d);
-    const float cmax = S.scal[0];
-    const int64_t ln = S.n;
-    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < m;
-         base += (int64_t)gridDim.x * kThreads) {
-        const int64_t e = base + threadIdx.x;
-        bool mv = false, flag = false, full = false;
-        int64_t row = 0;
-        int old = 0;
-        if (e < m) {
-            const int4 w = S.ywl[e];
-            const int2 aux = S.yaux[e];
-            row = w.x;
-            old = S.labels[row];
-            if (aux.x < 0) {
-                full = true;
-            } else {
-                const unsigned mask = (unsigned)w.y;
-                const float acc_a = __int_as_float(w.z), xn = __int_as_float(w.w);
-                float bestD = acc_a, secD = INFINITY;
-                int bestJ = old;
-                int slot = aux.x;
-                for (unsigned mm = mask; mm; mm &= mm - 1, slot++) {
-                    const float4 r = S.yres[slot];
-                    const int pj = __float_as_int(r.x);
-                    if (pj >= 0) {
-                        if (r.y < bestD || (r.y == bestD && pj < bestJ)) {
-                            secD = fminf(secD, bestD);
-                            bestD = r.y;
-                            bestJ = pj;
-                        } else {
-                            secD = fminf(secD, r.y);
-                        }
-                    }
-                    secD = fminf(secD, r.z);
-                }
-                const float lun = S.ylun[e].x;
-                const float U1 = (sqrtf(bestD) + kU32 * (xn + S.cnorm[bestJ])) * (1.0f + rho);
-                const float Ls = isinf(secD) ? INFINITY
-                                             : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
-                if (fminf(Ls, lun) > U1) {
-                    mv = bestJ != old;
-                    S.labels[row] = bestJ;
-                    S.ub[row] = U1;
-                    float* lbr = S.lb + row;
-                    slot = aux.x;
-                    for (unsigned mm = mask; mm; mm &= mm - 1, slot++) {
-                        const int g = __ffs(mm) - 1;
-                        const float4 r = S.yres[slot];
-                        const float gm = (__float_as_int(r.x) == bestJ) ? r.z : r.y;
-                        lbr[(int64_t)g * ln] =
-                            isinf(gm) ? INFINITY
-                                      : fmaxf((sqrtf(gm) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
-                    }
-                    if (mv) {
-                        const int go = S.group_of[old];
-                        const float la =
-                            fmaxf((sqrtf(acc_a) - kU32 * (xn + S.cnorm[old])) * (1.0f - rho), 0.f);
-                        lbr[go * ln] = fminf(lbr[go * ln], la);
-                    }
-                } else {
-                    flag = true;
-                }
-            }
-        }
-        int64_t pos = block_append(mv, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
-        if (mv) S.moved[pos] = make_int2((int)row, old);
-        int64_t fpos = block_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED), scr);
-        if (flag) S.flagged[fpos] = (int)row;
-        int64_t wpos = block_append(full, (unsigned long long*)(stat + LK_STAT_WORK), scr);
-        if (full) S.work[wpos] = (int)row;
-    }
 }
 
 // Iteration 1 of the group strategies (SequentialStrategy.seed +
@@ -544,10 +265,12 @@ __global__ void __launch_bounds__(kThreads) k_seed_yinyang(DevState S, int64_t* 
             old = S.labels[i];
             moved = old != j1;
             S.labels[i] = j1;
+            // iteration 1: the cumulative drifts of the lazy encoding are 0
             S.ub[i] = U1;
             S.lb[(int64_t)bestG * ln + i] =
                 isinf(bestg2) ? INFINITY
                               : fmaxf((sqrtf(bestg2) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
+            if (S.glb) S.glb[i] = fmaxf(L2, 0.f);  // bounds every non-winner: min of the groups
         }
         int64_t pos = block_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
         if (moved) S.moved[pos] = make_int2((int)i, old);
@@ -754,11 +477,6 @@ static int grid_for_rows(int64_t rows, int sms, int per_sm) {
 lk_status init_yy_attributes() {
 #define LK_SMEM96(kern) \
     LK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024))
-    LK_SMEM96((k_yy_sorted_scan<2, true>));
-    LK_SMEM96((k_yy_sorted_scan<4, true>));
-    LK_SMEM96((k_yy_sorted_scan<8, true>));
-    LK_SMEM96((k_yy_sorted_scan<16, true>));
-    LK_SMEM96((k_yy_sorted_scan<32, true>));
     LK_SMEM96((k_seed_yinyang<2, true>));
     LK_SMEM96((k_seed_yinyang<4, true>));
     LK_SMEM96((k_seed_yinyang<8, true>));
@@ -773,22 +491,6 @@ lk_status init_yy_attributes() {
 }
 
 bool yy_masked(const lk::DevState& S) { return S.t_groups <= 32 && S.d <= 32; }
-
-template <int T>
-static void launch_filter_m(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
-    k_filter_yinyang_m<T><<<grid_for_rows(S.n, sms, 8), kThreads, 0, st>>>(S, stat);
-}
-
-template <int DP>
-static void launch_sorted_scan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
-    const size_t tabs = (size_t)S.k * 8 + (size_t)(S.t_groups + 1) * 4;
-    const size_t csm = (size_t)S.k * S.ldc * sizeof(float) + tabs;
-    const dim3 grid((unsigned)((sms * 8 + S.t_groups - 1) / S.t_groups), (unsigned)S.t_groups);
-    if (csm <= 96 * 1024)
-        k_yy_sorted_scan<DP, true><<<grid, kThreads, csm, st>>>(S, stat);
-    else
-        k_yy_sorted_scan<DP, false><<<grid, kThreads, tabs, st>>>(S, stat);
-}
 
 template <int DP>
 static void launch_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
@@ -813,15 +515,6 @@ lk_status launch_yy_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStre
 
 lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,
                            bool full_only) {
-    if (yy_masked(S) && !full_only) {
-        // the group count is padded (with +inf bounds) up to a template size
-        const int t = S.t_groups;
-        if (t <= 8) launch_filter_m<8>(S, stat, sms, st);
-        else if (t <= 16) launch_filter_m<16>(S, stat, sms, st);
-        else launch_filter_m<32>(S, stat, sms, st);
-        LK_LAUNCH_CHECK();
-        return LK_OK;
-    }
     const size_t smem = (size_t)S.t_groups * sizeof(float);  // <= 64 KB (k <= 16384)
     k_filter_yinyang<<<grid_for_rows(S.n, sms, 8), kThreads, smem, st>>>(S, stat, full_only ? 1 : 0);
     LK_LAUNCH_CHECK();
@@ -831,16 +524,6 @@ lk_status launch_yy_filter(const lk::DevState& S, int64_t* stat, int sms, cudaSt
 lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,
                           bool full_only) {
     if (full_only) return LK_OK;
-    if (yy_masked(S)) {
-        const int d = S.d;
-        if (d <= 2) launch_sorted_scan<2>(S, stat, sms, st);
-        else if (d <= 4) launch_sorted_scan<4>(S, stat, sms, st);
-        else if (d <= 8) launch_sorted_scan<8>(S, stat, sms, st);
-        else if (d <= 16) launch_sorted_scan<16>(S, stat, sms, st);
-        else launch_sorted_scan<32>(S, stat, sms, st);
-        LK_LAUNCH_CHECK();
-        return LK_OK;
-    }
     const size_t csm = (size_t)S.k * S.ldc * sizeof(float);
     const int staged = csm <= 96 * 1024;
     k_yy_pairs<kYyG><<<sms * (staged ? 4 : 8), kThreads, staged ? csm : 0, st>>>(S, stat, staged);
@@ -851,14 +534,6 @@ lk_status launch_yy_pairs(const lk::DevState& S, int64_t* stat, int sms, cudaStr
 lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st,
                           bool full_only) {
     if (full_only) return LK_OK;
-    if (yy_masked(S)) {
-        const int T = S.t_groups, g = grid_for_rows(S.n, sms, 4);
-        if (T <= 8) k_yy_merge_m<8><<<g, kThreads, 0, st>>>(S, stat);
-        else if (T <= 16) k_yy_merge_m<16><<<g, kThreads, 0, st>>>(S, stat);
-        else k_yy_merge_m<32><<<g, kThreads, 0, st>>>(S, stat);
-        LK_LAUNCH_CHECK();
-        return LK_OK;
-    }
     k_yy_merge<<<grid_for_rows(S.n, sms, 4), kThreads, 0, st>>>(S, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;

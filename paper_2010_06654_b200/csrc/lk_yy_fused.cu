@@ -37,6 +37,9 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxPairs = 1536;  // pair slots of the block queue
 constexpr int kQRows = 512;      // row slots of the block queue
+// per-centroid filter info (cumulative drift, half-separation, norm, group
+// position) is read through L1 rather than staged: k * 16 B stays L1-resident
+constexpr bool kStageInfo = false;
 
 template <int DP>
 __device__ __forceinline__ float dist2(const float (&xr)[DP], const float* cp, int d) {
@@ -66,6 +69,8 @@ struct Queue {
 };
 
 struct Shared {
+    const float* dg;   // cumulative group drifts (lazy encoding offsets)
+    float dm;          // cumulative max drift
     const int* goff;
     int* bcnt;
     int* boff;
@@ -234,24 +239,30 @@ __device__ __forceinline__ void drain(const DevState& S, int64_t* stat, const do
             const float a2 = kU32 * (xn + cmax);
             const float Ls = isinf(secD) ? INFINITY : (sqrtf(secD) - a2) * (1.0f - rho);
             if (fminf(Ls, Q.lun[q]) > U1) {
+                // stored in the lazy encoding: ub - Dc[label], lb + Dg[g], glb + Dm
                 mv = bestJ != a;
                 if (mv) S.labels[i] = bestJ;
-                S.ub[i] = U1;
+                S.ub[i] = __fsub_ru(U1, S.dcum[bestJ]);
                 float* lbr = S.lb + i;
+                float gnew = Q.lun[q];  // min over the unscanned groups
                 e = poff;
                 for (unsigned mm = mask; mm; mm &= mm - 1, e++) {
                     const int g = __ffs(mm) - 1;
                     // every member but the winner (the old label included)
                     const float gm = (sh.rp1[e] == bestJ) ? sh.rb2[e] : sh.rb1[e];
-                    lbr[(int64_t)g * ln] = isinf(gm) ? INFINITY : (sqrtf(gm) - a2) * (1.0f - rho);
+                    const float lg = isinf(gm) ? INFINITY : (sqrtf(gm) - a2) * (1.0f - rho);
+                    gnew = fminf(gnew, lg);
+                    lbr[(int64_t)g * ln] = __fadd_rd(lg, sh.dg[g]);
                 }
                 if (mv) {
                     // the old label joins its group's competitors (needed when
                     // that group was not scanned; harmless otherwise)
                     const int go = S.group_of[a];
                     const float la = (sqrtf(acc_a) - kU32 * (xn + S.cnorm[a])) * (1.0f - rho);
-                    lbr[(int64_t)go * ln] = fminf(lbr[(int64_t)go * ln], la);
+                    gnew = fminf(gnew, la);
+                    lbr[(int64_t)go * ln] = fminf(lbr[(int64_t)go * ln], __fadd_rd(la, sh.dg[go]));
                 }
+                S.glb[i] = __fadd_rd(gnew, sh.dm);
             } else {
                 Q.flag[atomicAdd(sh.nflag, 1)] = q;
             }
@@ -277,7 +288,7 @@ __global__ void __launch_bounds__(kThreads) k_yy_fused(DevState S, int64_t* stat
     // dynamic: staged centroids (group order) + per-centroid info | pair list
     // | sorted order | scan results
     extern __shared__ __align__(16) float dsm[];
-    __shared__ float gd[T];
+    __shared__ float dg[T];
     __shared__ int goff[T + 1];
     __shared__ int bcnt[T];
     __shared__ int boff[T];
@@ -288,23 +299,25 @@ __global__ void __launch_bounds__(kThreads) k_yy_fused(DevState S, int64_t* stat
 
     const int k = S.k, ldc = S.ldc;
     const int sd = DP <= 4 ? DP : ldc;  // stride of the staged centroid rows
-    // staged (STAGED): centroids in group order, then per-centroid drift,
-    // half-separation, norm bound and group position, so the filter's
+    // staged (STAGED): centroids in group order, then per-centroid cumulative
+    // drift, half-separation, norm bound and group position, so the filter's
     // label-dependent loads are shared-memory reads
     float* cgs = dsm;
+    constexpr bool SI = STAGED && kStageInfo;
     float* s_drift = dsm + (STAGED ? k * sd : 0);
-    float* s_shalf = s_drift + (STAGED ? k : 0);
-    float* s_cnorm = s_shalf + (STAGED ? k : 0);
-    int* s_ginv = reinterpret_cast<int*>(s_cnorm + (STAGED ? k : 0));
-    uint32_t* ptmp = reinterpret_cast<uint32_t*>(s_ginv + (STAGED ? k : 0));
+    float* s_shalf = s_drift + (SI ? k : 0);
+    float* s_cnorm = s_shalf + (SI ? k : 0);
+    int* s_ginv = reinterpret_cast<int*>(s_cnorm + (SI ? k : 0));
+    uint32_t* ptmp = reinterpret_cast<uint32_t*>(s_ginv + (SI ? k : 0));
     uint16_t* psort = reinterpret_cast<uint16_t*>(ptmp + pcap);
     float* rb1 = reinterpret_cast<float*>(psort + ((pcap + 1) & ~1));
     float* rb2 = rb1 + pcap;
     int* rp1 = reinterpret_cast<int*>(rb2 + pcap);
-    const Shared sh{goff, bcnt, boff, ptmp, psort, rb1, rb2, rp1, &s_nflag};
+    const float dm = S.scal[4];
+    const Shared sh{dg, dm, goff, bcnt, boff, ptmp, psort, rb1, rb2, rp1, &s_nflag};
 
     if (threadIdx.x < T) {
-        gd[threadIdx.x] = S.gdrift[threadIdx.x];
+        dg[threadIdx.x] = S.dgcum[threadIdx.x];
         bcnt[threadIdx.x] = 0;
     }
     if (threadIdx.x <= T) goff[threadIdx.x] = S.goff[threadIdx.x];
@@ -317,18 +330,21 @@ __global__ void __launch_bounds__(kThreads) k_yy_fused(DevState S, int64_t* stat
             } else {
                 for (int z = 0; z < sd; z++) cgs[j * sd + z] = src[z];
             }
-            s_drift[j] = S.drift[j];
-            s_shalf[j] = S.s_half[j];
-            s_cnorm[j] = S.cnorm[j];
-            s_ginv[j] = S.ginv[j];
+            if (SI) {
+                s_drift[j] = S.dcum[j];
+                s_shalf[j] = S.s_half[j];
+                s_cnorm[j] = S.cnorm[j];
+                s_ginv[j] = S.ginv[j];
+            }
         }
     }
     __syncthreads();
     const float* __restrict__ cg = STAGED ? cgs : S.Cg;
     const int cstride = STAGED ? sd : ldc;
-    const float* __restrict__ c_drift = STAGED ? s_drift : S.drift;
-    const float* __restrict__ c_shalf = STAGED ? s_shalf : S.s_half;
-    const float* __restrict__ c_cnorm = STAGED ? s_cnorm : S.cnorm;
+    const float* __restrict__ c_dcum = SI ? s_drift : S.dcum;
+    const float* __restrict__ c_shalf = SI ? s_shalf : S.s_half;
+    const float* __restrict__ c_cnorm = SI ? s_cnorm : S.cnorm;
+    const int* __restrict__ c_ginv = SI ? s_ginv : S.ginv;
 
     const float rho = simt_rel_err(S.d);
     const float cmax = S.scal[0];
@@ -337,18 +353,17 @@ __global__ void __launch_bounds__(kThreads) k_yy_fused(DevState S, int64_t* stat
     int64_t n_dist = 0, n_active = 0, n_need = 0, n_pairs = 0;
     int q0 = 0, p0 = 0;  // queued rows / pairs (block-uniform)
 
-    // software pipeline: the label, ub and group bounds of the next chunk are
+    // software pipeline: the label, ub and global bound of the next chunk are
     // loaded while this chunk is filtered, queued and (maybe) drained
     const int64_t cstep = (int64_t)gridDim.x * kThreads;
     int a_n = 0;
-    float ub_n = 0.f, v_n[T];
+    float ub_n = 0.f, glb_n = 0.f;
     {
         const int64_t i0 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
         if (i0 < S.n) {
             a_n = S.labels[i0];
             ub_n = S.ub[i0];
-#pragma unroll
-            for (int g = 0; g < T; g++) v_n[g] = __ldcs(S.lb + i0 + g * ln);
+            glb_n = S.glb[i0];
         }
     }
     for (int64_t base = (int64_t)blockIdx.x * kThreads; base < S.n; base += cstep) {
@@ -357,41 +372,38 @@ __global__ void __launch_bounds__(kThreads) k_yy_fused(DevState S, int64_t* stat
         bool need = false;
         unsigned mask = 0;
         const int a = a_n;
-        const float ub0 = ub_n;
-        float v[T];
-#pragma unroll
-        for (int g = 0; g < T; g++) v[g] = v_n[g];
+        const float ub_s = ub_n, glb_s = glb_n;
         {
             const int64_t in = i + cstep;
             if (in < S.n) {
                 a_n = S.labels[in];
                 ub_n = S.ub[in];
-#pragma unroll
-                for (int g = 0; g < T; g++) v_n[g] = __ldcs(S.lb + in + g * ln);
+                glb_n = S.glb[in];
             }
         }
-        float acc_a = 0.f, u = 0.f, lun = INFINITY, xn = 0.f;
+        float acc_a = 0.f, lun = INFINITY, xn = 0.f;
         float xr[DP];
 #pragma unroll
         for (int z = 0; z < DP; z++) xr[z] = 0.f;
 
-        // ---- filter: decay, gates, tighten, group mask
+        // ---- filter.  Bounds are stored against cumulative drifts (lazy
+        // encoding): u = ub_s + Dc[a] bounds d(x, c_a) from above, glb_s - Dm
+        // and lb_s[g] - Dg[g] bound every other centroid (of group g) from
+        // below, all with directed rounding.  A row that passes writes nothing.
         if (valid) {
-            u = __fadd_ru(ub0, c_drift[a]);
-            float gmin = INFINITY;
-            float* sp = S.lb + i;
-#pragma unroll
-            for (int g = 0; g < T; g++) {
-                v[g] = __fsub_rd(v[g], gd[g]);  // a negative lower bound is still valid
-                gmin = fminf(gmin, v[g]);
-                __stcs(sp + g * ln, v[g]);
-            }
+            float u = __fadd_ru(ub_s, c_dcum[a]);
+            const float sa = c_shalf[a];
             // Hamerly's separation test holds for every bound family
-            gmin = fmaxf(gmin, c_shalf[a]);
-            if (!(gmin > u)) {
+            const float gate = fmaxf(__fsub_rd(glb_s, dm), sa);
+            if (!(gate > u)) {
                 n_active++;
+                // the group table, loaded alongside the point for the tighten
+                float v[T];
+                const float* lp = S.lb + i;
+#pragma unroll
+                for (int g = 0; g < T; g++) v[g] = __ldcs(lp + g * ln);
                 const float* xp = S.X32 + i * S.ldx;
-                const float* cp = STAGED ? cgs + s_ginv[a] * sd : S.C32 + (int64_t)a * ldc;
+                const float* cp = STAGED ? cgs + c_ginv[a] * sd : S.C32 + (int64_t)a * ldc;
                 float xn2 = 0.f;
 #pragma unroll
                 for (int z = 0; z < DP; z++) {
@@ -404,17 +416,29 @@ __global__ void __launch_bounds__(kThreads) k_yy_fused(DevState S, int64_t* stat
                 }
                 xn = sqrtf(xn2);
                 const float U = (sqrtf(acc_a) + kU32 * (xn + c_cnorm[a])) * (1.0f + rho);
+                const bool tight = U < u;
                 u = fminf(u, U);
-                need = !(gmin > u);
-                if (need) {
+                if (!(gate > u)) {
+                    float gmin = INFINITY;
 #pragma unroll
                     for (int g = 0; g < T; g++) {
-                        if (v[g] > u) lun = fminf(lun, v[g]);
-                        else mask |= 1u << g;
+                        v[g] = __fsub_rd(v[g], dg[g]);  // a negative lower bound is still valid
+                        gmin = fminf(gmin, v[g]);
+                    }
+                    need = !(fmaxf(gmin, sa) > u);
+                    if (need) {
+#pragma unroll
+                        for (int g = 0; g < T; g++) {
+                            if (v[g] > u) lun = fminf(lun, v[g]);
+                            else mask |= 1u << g;
+                        }
+                    } else {
+                        // the groups prune: keep their (tighter) minimum as the global bound
+                        S.glb[i] = __fadd_rd(gmin, dm);
                     }
                 }
+                if (tight && !need) S.ub[i] = __fsub_ru(u, c_dcum[a]);
             }
-            S.ub[i] = u;
         }
 
         // ---- enqueue this chunk's failing rows in chunk order, draining the
@@ -543,7 +567,7 @@ static lk_status launch_fused_dp(const lk::DevState& S, int64_t* stat, const dou
     const int pcap = pcap_env;
     const size_t pairs = (size_t)pcap * 4 + (size_t)((pcap + 1) & ~1) * 2 + (size_t)pcap * 12;
     const int sd = DP <= 4 ? DP : S.ldc;
-    const size_t cg = (size_t)S.k * sd * 4 + (size_t)S.k * 16;  // centroids + per-centroid info
+    const size_t cg = (size_t)S.k * sd * 4 + (kStageInfo ? (size_t)S.k * 16 : 0);  // centroids (+ info)
     if (cg + pairs <= 64 * 1024)
         return launch_fused_t<DP, T, true>(S, stat, qscale, sms, cg + pairs, pcap, st);
     return launch_fused_t<DP, T, false>(S, stat, qscale, sms, pairs, pcap, st);

@@ -44,9 +44,11 @@ def gpu_groups(strategy: str, n: int, k: int) -> int:
     if strategy == "elkan":
         return k if n * k <= (1 << 26) else min(k, 64)
     if strategy == "yinyang":
-        # ~128 centroids per group (the reference's k/10 would make the n*t
-        # table dominate an iteration's traffic at large k), at most 32 groups
-        return max(4, min(32, round(k / 128)))
+        # ~64 centroids per group (the reference's k/10 would make the n*t
+        # table dominate an iteration's traffic at large k), at most 32 groups;
+        # the fused path (d <= 32) reads a row's group table only when its
+        # global bound fails
+        return max(4, min(32, round(k / 64)))
     return 0
 
 
