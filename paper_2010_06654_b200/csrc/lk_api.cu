@@ -584,6 +584,7 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     LK_CUDA_CHECK(cudaMemsetAsync(S.cur, 0, c->L.size[B_CUR], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.hlog_off, 0, c->L.size[B_HLOG_OFF], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.sse, 0, c->L.size[B_SSE], st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
     if (S.lazy) {
         LK_CUDA_CHECK(cudaMemsetAsync(S.dcum, 0, c->L.size[B_DCUM], st));
         LK_CUDA_CHECK(cudaMemsetAsync(S.dgcum, 0, c->L.size[B_DGCUM], st));
@@ -609,8 +610,10 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     lk::DevState& S = c->S;
     int64_t* stat = S.cur;  // counters of the iteration in flight (copied out by the update)
-    LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
-    if (S.ybucket) LK_CUDA_CHECK(cudaMemsetAsync(S.ybucket, 0, c->L.size[B_YBUCKET], st));
+    // the delta payload is zeroed by the update that consumes it (and at
+    // lk_set_centroids); the bucket counters only by the multi-kernel path
+    if (S.ybucket && !lkh::yy_fused_ok(S))
+        LK_CUDA_CHECK(cudaMemsetAsync(S.ybucket, 0, c->L.size[B_YBUCKET], st));
     const int64_t n = c->cfg.n_local;
     const bool use_tc = lkh::tc_supported(S);
     lk_status s;
@@ -732,7 +735,7 @@ lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
     const bool need_half = c->cfg.strategy != LK_STRAT_LLOYD;
     lk_status s = lkh::launch_update(c->S, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV),
                                      buf<double>(c, B_SSE_PART), need_half, st);
-    c->launches += need_half ? 3 : 2;
+    c->launches += need_half ? 2 : 1;
     return s;
 }
 

@@ -12,7 +12,7 @@
 //       (Hamerly.update_bounds pruners.py:234-239, assign_pass :244-254).
 //   K4  k_refine_moved  fixed-point member-sum deltas of moved points
 //       (refine_full lloyd.py:78-97, incrementally as in engine.py:134-172).
-//   K5  k_update_centroids / k_update_global / k_half_sep  centroid divide with
+//   K5  k_update_centroids (+ its last block: global scalars) / k_half_sep  centroid divide with
 //       the empty-cluster rule (lloyd.py:94-96), drifts (bounds.py:31-35),
 //       s = half nearest-other distance (bounds.py:38-47), SSE (core.py:172).
 #include <float.h>
@@ -449,16 +449,87 @@ __global__ void __launch_bounds__(kThreads) k_refine_moved(DevState S, int64_t* 
 // ---------------------------------------------------------------------------
 // K5: centroid update (one warp per centroid) and global scalars
 
+// One block (the last of k_update_centroids): SSE (fixed reduction order),
+// max ||c||, top-2 drift, group drifts, done flag.
+__device__ __forceinline__ void update_global_block(const DevState& S, const double* sse_part) {
+    const int t = *S.iter;
+    __shared__ double ssum[kThreads];
+    __shared__ float smax[kThreads], sd1[kThreads], sd2[kThreads];
+    __shared__ int sarg[kThreads];
+    const int tid = threadIdx.x;
+    double acc = 0.0;
+    float cm = 0.f, d1 = -1.f, d2 = -1.f;
+    int a1 = -1;
+    for (int j = tid; j < S.k; j += blockDim.x) {
+        acc += __ldcg(sse_part + j);
+        cm = fmaxf(cm, __ldcg(S.cnorm + j));
+        float dj = __ldcg(S.drift + j);
+        if (dj > d1) { d2 = d1; d1 = dj; a1 = j; }
+        else d2 = fmaxf(d2, dj);
+    }
+    ssum[tid] = acc; smax[tid] = cm; sd1[tid] = d1; sd2[tid] = d2; sarg[tid] = a1;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (tid < s) {
+            ssum[tid] += ssum[tid + s];
+            smax[tid] = fmaxf(smax[tid], smax[tid + s]);
+            float od1 = sd1[tid + s], od2 = sd2[tid + s];
+            int oa = sarg[tid + s];
+            if (od1 > sd1[tid] || (od1 == sd1[tid] && oa >= 0 && (sarg[tid] < 0 || oa < sarg[tid]))) {
+                sd2[tid] = fmaxf(sd1[tid], od2);
+                sd1[tid] = od1;
+                sarg[tid] = oa;
+            } else {
+                sd2[tid] = fmaxf(sd2[tid], od1);
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        S.scal[0] = smax[0];
+        S.scal[1] = fmaxf(sd1[0], 0.f);
+        S.scal[2] = fmaxf(sd2[0], 0.f);
+        S.scal[3] = __int_as_float(sarg[0]);
+        const int64_t changed = __ldcg(S.delta + (int64_t)S.k * S.d + 2 * S.k);
+        S.delta[(int64_t)S.k * S.d + 2 * S.k] = 0;
+        S.cur[LK_STAT_CHANGED_GLOBAL] = changed;
+        if (t >= 1 && t <= S.t_max) {
+            S.sse[t - 1] = ssum[0];
+            for (int q = 0; q < LK_NSTAT; q++) S.stats[(int64_t)(t - 1) * LK_NSTAT + q] = S.cur[q];
+        }
+        for (int q = 0; q < LK_NSTAT; q++) S.cur[q] = 0;
+        *S.iter = t + 1;
+        if (changed == 0) *S.done = 1;
+    }
+    // s_half is rebuilt by k_half_sep's atomicMin: start from +inf
+    for (int j = tid; j < S.k; j += blockDim.x) S.s_half[j] = INFINITY;
+    // group drifts (Yinyang): max drift over each group's members
+    if (S.gdrift) {
+        __syncthreads();
+        for (int g = tid; g < S.t_groups; g += blockDim.x) S.gdrift[g] = 0.f;
+        __syncthreads();
+        for (int j = tid; j < S.k; j += blockDim.x) atomic_max_pos(S.gdrift + S.group_of[j], __ldcg(S.drift + j));
+        if (S.lazy) {
+            // cumulative group and global drifts of the lazy bound encoding
+            __syncthreads();
+            for (int g = tid; g < S.t_groups; g += blockDim.x)
+                S.dgcum[g] = __fadd_ru(S.dgcum[g], S.gdrift[g]);
+            if (tid == 0) S.scal[4] = __fadd_ru(S.scal[4], S.scal[1]);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const double* qscale,
                                                                const double* qinv,
                                                                double* sse_part) {
     if (*S.done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = blockIdx.x * (kThreads / 32) + warp;
-    if (j >= S.k) return;
-    const int64_t* dS = S.delta;
-    const int64_t* dN = S.delta + (int64_t)S.k * S.d;
-    const int64_t* dQ = dN + S.k;
+    int64_t* dS = S.delta;
+    int64_t* dN = S.delta + (int64_t)S.k * S.d;
+    int64_t* dQ = dN + S.k;
+    if (j < S.k) {
+    // (body indented one level less than its scope, to keep the diff small)
     int64_t cnt = S.counts[j] + dN[j];
     int64_t qs = S.qsum[j] + dQ[j];
     double s2 = 0.0, drift2 = 0.0, cn2 = 0.0, c2 = 0.0;
@@ -502,76 +573,26 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
         if (S.lazy) S.dcum[j] = __fadd_ru(S.dcum[j], dj);
         S.cnorm[j] = __double2float_ru(sqrt(cn2) * (1.0 + 1e-12));
         sse_part[j] = cnt > 0 ? ((double)qs * qinv[S.d] - s2 / (double)cnt) : 0.0;
+        // the delta payload is consumed: zero it for the next iteration
+        dN[j] = 0;
+        dQ[j] = 0;
     }
-}
-
-// Single block: SSE (fixed reduction order), max ||c||, top-2 drift, group
-// drifts, done flag.
-__global__ void __launch_bounds__(1024) k_update_global(DevState S, const double* sse_part) {
-    if (*S.done) return;
-    const int t = *S.iter;
-    __shared__ double ssum[1024];
-    __shared__ float smax[1024], sd1[1024], sd2[1024];
-    __shared__ int sarg[1024];
-    const int tid = threadIdx.x;
-    double acc = 0.0;
-    float cm = 0.f, d1 = -1.f, d2 = -1.f;
-    int a1 = -1;
-    for (int j = tid; j < S.k; j += blockDim.x) {
-        acc += sse_part[j];
-        cm = fmaxf(cm, S.cnorm[j]);
-        float dj = S.drift[j];
-        if (dj > d1) { d2 = d1; d1 = dj; a1 = j; }
-        else d2 = fmaxf(d2, dj);
+    for (int z = lane; z < S.d; z += 32) dS[(int64_t)j * S.d + z] = 0;
     }
-    ssum[tid] = acc; smax[tid] = cm; sd1[tid] = d1; sd2[tid] = d2; sarg[tid] = a1;
+    // the last block to finish reduces the per-centroid results (threadfence
+    // reduction: its reads see every block's writes)
+    __shared__ bool last;
     __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if (tid < s) {
-            ssum[tid] += ssum[tid + s];
-            smax[tid] = fmaxf(smax[tid], smax[tid + s]);
-            float od1 = sd1[tid + s], od2 = sd2[tid + s];
-            int oa = sarg[tid + s];
-            if (od1 > sd1[tid] || (od1 == sd1[tid] && oa >= 0 && (sarg[tid] < 0 || oa < sarg[tid]))) {
-                sd2[tid] = fmaxf(sd1[tid], od2);
-                sd1[tid] = od1;
-                sarg[tid] = oa;
-            } else {
-                sd2[tid] = fmaxf(sd2[tid], od1);
-            }
-        }
-        __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned tk = atomicAdd((unsigned*)(S.done + 2), 1u);
+        last = tk == gridDim.x - 1;
     }
-    if (tid == 0) {
-        S.scal[0] = smax[0];
-        S.scal[1] = fmaxf(sd1[0], 0.f);
-        S.scal[2] = fmaxf(sd2[0], 0.f);
-        S.scal[3] = __int_as_float(sarg[0]);
-        const int64_t changed = S.delta[(int64_t)S.k * S.d + 2 * S.k];
-        S.cur[LK_STAT_CHANGED_GLOBAL] = changed;
-        if (t >= 1 && t <= S.t_max) {
-            S.sse[t - 1] = ssum[0];
-            for (int q = 0; q < LK_NSTAT; q++) S.stats[(int64_t)(t - 1) * LK_NSTAT + q] = S.cur[q];
-        }
-        for (int q = 0; q < LK_NSTAT; q++) S.cur[q] = 0;
-        *S.iter = t + 1;
-        if (changed == 0) *S.done = 1;
-    }
-    // s_half is rebuilt by k_half_sep's atomicMin: start from +inf
-    for (int j = tid; j < S.k; j += blockDim.x) S.s_half[j] = INFINITY;
-    // group drifts (Yinyang): max drift over each group's members
-    if (S.gdrift) {
-        __syncthreads();
-        for (int g = tid; g < S.t_groups; g += blockDim.x) S.gdrift[g] = 0.f;
-        __syncthreads();
-        for (int j = tid; j < S.k; j += blockDim.x) atomic_max_pos(S.gdrift + S.group_of[j], S.drift[j]);
-        if (S.lazy) {
-            // cumulative group and global drifts of the lazy bound encoding
-            __syncthreads();
-            for (int g = tid; g < S.t_groups; g += blockDim.x)
-                S.dgcum[g] = __fadd_ru(S.dgcum[g], S.gdrift[g]);
-            if (tid == 0) S.scal[4] = __fadd_ru(S.scal[4], S.scal[1]);
-        }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        update_global_block(S, sse_part);
+        if (threadIdx.x == 0) S.done[2] = 0;
     }
 }
 
@@ -790,8 +811,6 @@ lk_status launch_update(const DevState& S, const double* qscale, const double* q
                         double* sse_part, bool need_half, cudaStream_t st) {
     int grid = (S.k + (kThreads / 32) - 1) / (kThreads / 32);
     k_update_centroids<<<grid, kThreads, 0, st>>>(S, qscale, qinv, sse_part);
-    LK_LAUNCH_CHECK();
-    k_update_global<<<1, 1024, 0, st>>>(S, sse_part);
     LK_LAUNCH_CHECK();
     if (need_half) {
         dim3 g((S.k + kHsT - 1) / kHsT, (S.k + kHsT - 1) / kHsT);

@@ -48,10 +48,11 @@ def group_centroids(centers: np.ndarray, t: int, seed: int = 0, n_iters: int = 5
     for _ in range(n_iters):
         d2 = cn[:, None] - 2.0 * centers @ means.T + np.sum(means * means, axis=1)[None, :]
         g = np.argmin(d2, axis=1)
-        for q in range(t):
-            mem = centers[g == q]
-            if len(mem):
-                means[q] = mem.mean(axis=0)
+        cnt = np.bincount(g, minlength=t)
+        sums = np.zeros_like(means)
+        np.add.at(sums, g, centers)
+        nz = cnt > 0
+        means[nz] = sums[nz] / cnt[nz, None]
     return g.astype(np.int32)
 
 
@@ -120,7 +121,7 @@ class DeviceLloyd:
     def __init__(self, data, k: int, strategy: str = "lloyd", t_max: int = 10, *,
                  device=None, kernel: str = "auto", groups: int = 0, comm=None,
                  n_total: int | None = None, group_seed: int = 0,
-                 record_history: bool = True, history_iters: int = 4):
+                 record_history: bool = True, history_iters: int = 8):
         torch = _torch()
         if not torch.cuda.is_available():
             raise nat.NativeError("no CUDA device: the B200 path has no CPU fallback")
@@ -317,7 +318,7 @@ class DeviceLloyd:
                 raise ContractError("rebind: fp64 input not fp32-exact on an fp32 context")
         self._bind(src, has_x64)
 
-    def run(self, init, *, record_history: bool = True, check_every: int = 4,
+    def run(self, init, *, record_history: bool = True, check_every: int = 8,
             use_graphs: bool = True):
         """Run up to t_max iterations from ``init``; stop after the first with
         changed == 0 (lloyd.py:169-171).  Returns a dict of host arrays.
@@ -405,7 +406,11 @@ class DeviceLloyd:
             res["converged"] = converged
             res["records"] = recs
             res["centroids"] = self.c64.to("cpu").numpy().copy()
-            res["labels"] = self.labels.to("cpu").numpy().astype(np.int64)
+            # int64 labels (lloyd.py:52) widened on the device, one pinned D2H
+            lab = torch.empty(self.n, dtype=torch.int64, pin_memory=True)
+            lab.copy_(self.labels, non_blocking=True)
+            stream.synchronize()
+            res["labels"] = lab.numpy()
             if record_history:
                 res["history"] = LabelHistory(self.n, [p for p in log_parts if p[0] < iters])
         return res
@@ -417,7 +422,12 @@ class DeviceLloyd:
         if np.any(offs < 0):
             raise nat.NativeError("label-history log overflow")
         if offs[-1] > 0:
-            log = self.hlog[: offs[-1]].to("cpu").numpy()
+            # pinned destination (torch's caching host allocator): a full-rate D2H
+            torch = _torch()
+            host = torch.empty((int(offs[-1]), 2), dtype=torch.int32, pin_memory=True)
+            host.copy_(self.hlog[: offs[-1]], non_blocking=True)
+            torch.cuda.current_stream(self.dev).synchronize()
+            log = host.numpy()
         else:
             log = np.empty((0, 2), dtype=np.int32)
         for t in range(t0, t1):

@@ -1,33 +1,45 @@
-"""Host-side phase timing of one public-API call (run_pruner) on cfg2."""
-import sys, time
-sys.path.insert(0, "/root/repo")
-import numpy as np
-import torch
-import paper_2010_06654_b200 as lk
-from paper_2010_06654_b200 import datasets, device as dv
-from paper_2010_06654_b200.pruners import gpu_groups
+"""Host-side phase timing of the public-API call (run_pruner) on a workload,
+with the cached device context warm (what bench.py's e2e measures).
 
-x = datasets.generate("cfg2")
-init = datasets.initial_centroids("cfg2", x)
+    python tools/e2e_phases.py [cfg2] [yinyang]
+"""
+import cProfile
+import pstats
+import sys
+import time
+
+sys.path.insert(0, "/root/repo")
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2010_06654_b200 as lk  # noqa: E402
+from paper_2010_06654_b200 import datasets  # noqa: E402
+from paper_2010_06654_b200.core import RunContext, init_random  # noqa: E402
+
+wl = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+strategy = sys.argv[2] if len(sys.argv) > 2 else "yinyang"
+cfg = datasets.CONFIGS[wl]
+x = datasets.generate(wl)
+init = init_random(RunContext(seed=cfg.seed_init), x, cfg.k)
 xp = torch.from_numpy(x).pin_memory()
-k = 1000
+T = 15
+
+
+def call():
+    return lk.run_pruner(xp, cfg.k, strategy, init=init, t_max=T)
+
+
+call()
 for rep in range(3):
     torch.cuda.synchronize()
-    T = {}
     t0 = time.perf_counter()
-    eng = dv.DeviceLloyd(xp, k, "yinyang", 15, groups=gpu_groups("yinyang", len(x), k), group_seed=0)
-    torch.cuda.synchronize(); T["ctor(alloc,ctx,H2D,scan,quant)"] = time.perf_counter() - t0
-    t1 = time.perf_counter()
-    out = eng.run(init)
-    torch.cuda.synchronize(); T["run"] = time.perf_counter() - t1
-    t2 = time.perf_counter()
-    h = [np.asarray(a) for a in out["history"]]
-    T["history materialize"] = time.perf_counter() - t2
-    eng.close()
-    T["total"] = time.perf_counter() - t0
-    print(rep, {a: round(b * 1e3, 2) for a, b in T.items()}, "iters", out["iterations"])
-# inside run(): profile with cProfile once
-import cProfile, pstats
-eng = dv.DeviceLloyd(xp, k, "yinyang", 15, groups=8, group_seed=0)
-pr = cProfile.Profile(); pr.enable(); out = eng.run(init); torch.cuda.synchronize(); pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
+    res = call()
+    torch.cuda.synchronize()
+    print(f"call {rep}: {1e3 * (time.perf_counter() - t0):.2f} ms, {len(res.iterations)} iterations, "
+          f"device iteration ms {[round((s.assign_nanos + s.refine_nanos) / 1e6, 3) for s in res.iterations]}")
+pr = cProfile.Profile()
+pr.enable()
+res = call()
+torch.cuda.synchronize()
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(25)
