@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "lk_common.cuh"
 #include "lk_internal.h"
@@ -157,7 +158,19 @@ __device__ __forceinline__ float tc_kappa(int d) {
     return 2.0f * (3.1f * 9.5367431640625e-07f + (float)(3 * d + 1) * 2.384185791015625e-07f * 1.01f);
 }
 
+// Split accumulators: x_hi c_hi (exact tf32 x tf32 products) accumulates
+// alone, the two cross terms in a second TMEM accumulator, summed in the
+// epilogue.  The fp32 accumulation error of the dominant term then counts d
+// additions instead of 3d + 1; the cross accumulator's is 2^-10 smaller, plus
+// one rounding of the final sum:
+//   kappa = 2 (3.1 * 2^-20 + (d + 2) * 2^-22 * 1.01 + d * 2^-31).
+__device__ __forceinline__ float tc_kappa_split(int d) {
+    return 2.0f * (3.1f * 9.5367431640625e-07f + (float)(d + 2) * 2.384185791015625e-07f * 1.01f +
+                   (float)d * 4.656612873077393e-10f);
+}
+
 // Aggregated append over the kEpiWarps epilogue warps (named barrier 1).
+// (the certifying warps are always the first kEpiWarps epilogue warps)
 __device__ __forceinline__ int64_t epi_append(bool pred, unsigned long long* counter,
                                               unsigned long long* scr, int ew) {
     unsigned msk = __ballot_sync(LK_FULL_MASK, pred);
@@ -195,13 +208,22 @@ struct TcArgs {
 constexpr int kTop2 = 0;
 constexpr int kCollect = 1;
 
-template <int BN, int MODE>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+template <bool SPLIT>
+struct TcShape {
+    static constexpr int EW = SPLIT ? 2 * kEpiWarps : kEpiWarps;  // epilogue warps
+    static constexpr int THREADS = 64 + 32 * EW;
+    static constexpr int NACC = SPLIT ? 2 : 1;                     // accumulators per tile
+};
+
+template <int BN, int MODE, bool SPLIT>
+__global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
     k_assign_tc(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                 DevState S, TcArgs A, int64_t* stat) {
     if (*S.done) return;
     using SM = Smem<BN>;
+    constexpr int EW = TcShape<SPLIT>::EW, NACC = TcShape<SPLIT>::NACC;
+    static_assert(2 * NACC * BN <= 512, "TMEM holds 512 fp32 columns");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = (uint64_t*)(smem + SM::STAGES * SM::STAGE_BYTES);
@@ -221,7 +243,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], kEpiWarps);
+            mbar_init(&tempty[b], EW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_map(&map_ahi);
@@ -232,7 +254,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(2 * BN));
+                     "r"(2 * NACC * BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -274,7 +296,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 for (int ct = 0; ct < A.n_ct; ct++) {
                     mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
-                    const uint32_t tmem_d = tmem_base + acc * BN;
+                    const uint32_t tmem_d = tmem_base + acc * NACC * BN;
+                    const uint32_t tmem_x = tmem_d + (SPLIT ? BN : 0);
                     for (int kc = 0; kc < A.n_kc; kc++) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
@@ -286,10 +309,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
                         for (int k = 0; k < KC / UK; k++) {
                             const uint64_t off = (uint64_t)((k * UK * 4) >> 4);
-                            // small terms first, then the dominant hi*hi term
-                            mma_tf32(tmem_d, dalo + off, dbhi + off, idesc, (kc | k) != 0);
-                            mma_tf32(tmem_d, dahi + off, dblo + off, idesc, 1);
-                            mma_tf32(tmem_d, dahi + off, dbhi + off, idesc, 1);
+                            if (SPLIT) {
+                                // cross terms into their own accumulator, hi*hi alone
+                                mma_tf32(tmem_x, dalo + off, dbhi + off, idesc, (kc | k) != 0);
+                                mma_tf32(tmem_x, dahi + off, dblo + off, idesc, 1);
+                                mma_tf32(tmem_d, dahi + off, dbhi + off, idesc, (kc | k) != 0);
+                            } else {
+                                // small terms first, then the dominant hi*hi term
+                                mma_tf32(tmem_d, dalo + off, dbhi + off, idesc, (kc | k) != 0);
+                                mma_tf32(tmem_d, dahi + off, dblo + off, idesc, 1);
+                                mma_tf32(tmem_d, dahi + off, dbhi + off, idesc, 1);
+                            }
                         }
                         mma_commit(&empty[stage]);
                         if (++stage == SM::STAGES) { stage = 0; phase ^= 1; }
@@ -300,13 +330,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
         }
     } else {
-        // ===== epilogue: warps 2..5, lane quarter = warp % 4 =====
+        // ===== epilogue: warps 2.., lane quarter = warp % 4 (TMEM access rule);
+        // SPLIT: two warps per quarter take alternate 32-column chunks (half h)
+        // and merge their row top-2 through shared memory; the h = 0 warps certify
         const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
         const int row_in_tile = q * 32 + lane;
-        const float kappa = tc_kappa(S.d);
+        const float kappa = SPLIT ? tc_kappa_split(S.d) : tc_kappa(S.d);
         int acc = 0;
         uint32_t acc_phase = 0;
         __shared__ unsigned long long escr[kEpiWarps + 1];
+        __shared__ float xb1[2][BM], xb2[2][BM];
+        __shared__ int xj1[2][BM];
+        int par = 0;
         for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x) {
             const int64_t r = rt * BM + row_in_tile;
             const bool valid = r < m;
@@ -317,19 +353,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             float thr = -INFINITY;
             int cnt = 0;
             int* slots = nullptr;
+            // SPLIT collect: half h fills slots [h * kHalfCand, (h + 1) * kHalfCand)
+            constexpr int kHalfCand = kMaxCand / 2;
+            const int cap = (SPLIT && MODE == kCollect) ? kHalfCand : kMaxCand;
             if (MODE == kCollect && valid) {
                 thr = A.thr[r];
-                slots = A.slots + r * kMaxCand;
+                slots = A.slots + r * kMaxCand + ((SPLIT && h) ? kHalfCand : 0);
             }
             for (int ct = 0; ct < A.n_ct; ct++) {
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
-                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * NACC * BN;
                 const int jbase = ct * BN;
 #pragma unroll 1
                 for (int c0 = 0; c0 < BN; c0 += 32) {
+                    if (SPLIT && ((c0 >> 5) & 1) != h) continue;
                     float v[32];
                     tmem_ld32(taddr + c0, v);
+                    if (SPLIT) {
+                        float vx[32];
+                        tmem_ld32(taddr + BN + c0, vx);
+#pragma unroll
+                        for (int e = 0; e < 32; e++) v[e] += vx[e];
+                    }
                     const int jb = jbase + c0;
                     // cn2 is padded with +inf beyond k (zero-filled B rows give v = 0)
                     const float4* cp = reinterpret_cast<const float4*>(S.cn2 + jb);
@@ -345,7 +391,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                                 else b2 = fminf(b2, dp);
                             } else {
                                 if (valid && dp <= thr) {
-                                    if (cnt < kMaxCand) slots[cnt] = jb + c4 * 4 + e;
+                                    if (cnt < cap) slots[cnt] = jb + c4 * 4 + e;
                                     cnt++;
                                 }
                             }
@@ -358,8 +404,45 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
             if (MODE == kCollect) {
+                if (SPLIT) {
+                    // the h = 0 warp appends the other half's slots after its own
+                    if (h == 1) xj1[par][row_in_tile] = cnt;
+                    asm volatile("bar.sync 2, %0;" ::"r"(EW * 32) : "memory");
+                    const int cur = par;
+                    par ^= 1;
+                    if (h == 1) continue;
+                    const int c1 = xj1[cur][row_in_tile];
+                    if (valid && cnt <= kHalfCand && c1 <= kHalfCand) {
+                        int* row_slots = A.slots + r * kMaxCand;
+                        for (int e = 0; e < c1; e++) row_slots[cnt + e] = row_slots[kHalfCand + e];
+                    }
+                    cnt += c1;
+                    if (cnt <= kMaxCand && (cnt - c1 > kHalfCand || c1 > kHalfCand))
+                        cnt = kMaxCand + 1;  // a half overflowed its slots
+                }
                 if (valid) A.cnt[r] = cnt;
                 continue;
+            }
+            if (SPLIT) {
+                // merge the two halves' top-2 in (value, index) order
+                if (h == 1) {
+                    xb1[par][row_in_tile] = b1;
+                    xb2[par][row_in_tile] = b2;
+                    xj1[par][row_in_tile] = j1;
+                }
+                asm volatile("bar.sync 2, %0;" ::"r"(EW * 32) : "memory");
+                const int cur = par;
+                par ^= 1;
+                if (h == 1) continue;
+                const float ob1 = xb1[cur][row_in_tile], ob2 = xb2[cur][row_in_tile];
+                const int oj1 = xj1[cur][row_in_tile];
+                if (ob1 < b1 || (ob1 == b1 && oj1 < j1)) {
+                    b2 = fminf(b1, ob2);
+                    b1 = ob1;
+                    j1 = oj1;
+                } else {
+                    b2 = fminf(b2, ob1);
+                }
             }
             // certify this row; ambiguous rows get a candidate threshold
             int64_t row = 0;
@@ -406,7 +489,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(2 * BN));
+                     "r"(2 * NACC * BN));
     }
 }
 
@@ -496,15 +579,29 @@ bool tc_supported(const DevState& S) {
 }
 
 lk_status init_tc_attributes() {
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kTop2>,
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kTop2, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kCollect>,
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kCollect, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<256, kTop2>,
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<256, kTop2, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<256>::TOTAL));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<256, kCollect>,
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<256, kCollect, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<256>::TOTAL));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kTop2, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kCollect, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
     return LK_OK;
+}
+
+// Split accumulators (tighter certification, fewer ambiguous rows) unless
+// LK_TC_SPLIT=0 (A/B knob).
+static bool tc_split() {
+    static const int v = [] {
+        const char* e = getenv("LK_TC_SPLIT");
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
 }
 
 lk_status launch_tc_prep_points(const DevState& S, int sms, cudaStream_t st) {
@@ -514,7 +611,7 @@ lk_status launch_tc_prep_points(const DevState& S, int sms, cudaStream_t st) {
     return LK_OK;
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool SPLIT>
 static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo, int64_t a_rows,
                            TcArgs A, int64_t max_rows, int64_t* stat, int sms, cudaStream_t st) {
     CUtensorMap mah, mal, mbh, mbl;
@@ -529,7 +626,8 @@ static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo
     const int smem = Smem<BN>::TOTAL;
     int64_t tiles = (max_rows + BM - 1) / BM;
     int grid = (int)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
-    k_assign_tc<BN, MODE><<<grid, kThreadsTC, smem, st>>>(mah, mal, mbh, mbl, S, A, stat);
+    k_assign_tc<BN, MODE, SPLIT><<<grid, TcShape<SPLIT>::THREADS, smem, st>>>(mah, mal, mbh, mbl, S,
+                                                                             A, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
@@ -537,8 +635,9 @@ static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo
 template <int MODE>
 static lk_status launch_mode(const DevState& S, const float* ahi, const float* alo, TcArgs A,
                              int64_t max_rows, int64_t* stat, int sms, cudaStream_t st) {
-    if (S.k <= 128) return launch_bn<128, MODE>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
-    return launch_bn<256, MODE>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
+    if (tc_split()) return launch_bn<128, MODE, true>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
+    if (S.k <= 128) return launch_bn<128, MODE, false>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
+    return launch_bn<256, MODE, false>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
 }
 
 lk_status launch_assign_tc(const DevState& S, const int32_t* rowlist, const int64_t* rowcount,
