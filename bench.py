@@ -171,6 +171,14 @@ def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kern
     if cls == 0:  # assignment: 2*d flops per (row, centroid) pair evaluated
         rows = sum(n if (strategy == "lloyd" or r["t"] == 1) else r["work"] for r in recs)
         return "flop", 2.0 * rows * k * d
+    if cls == 1 and strategy in ("yinyang", "elkan") and d <= 32 and groups <= 32:
+        # fused Yinyang kernel (lazy bounds): label + ub + global bound of every
+        # row; the group table, point and ub/glb rewrites of the rows failing
+        # the global bound; label/ub/glb + one bound per scanned group of the
+        # rows that reach the group scans
+        t = max(1, groups)
+        return "byte", sum(12.0 * n + r["active"] * (4.0 * t + 4.0 * d + 8.0)
+                           + 12.0 * r["ywl"] + 4.0 * r["pairs"] for r in recs)
     if cls == 1 and strategy in ("yinyang", "elkan"):
         # group filter: label/ub/lb-table traffic + tightened rows + group scans
         t = max(1, groups)
@@ -393,7 +401,8 @@ def run_ours(args):
                              "candidate_rows": [r["candidate"] for r in recs],
                              "group_rows": [r["ywl"] for r in recs],
                              "group_scans": [r["pairs"] for r in recs],
-                             "group_dists": [r["group_dists"] for r in recs]},
+                             "group_dists": [r["group_dists"] for r in recs],
+                             "active": [r["active"] for r in recs]},
         }
         print(json.dumps(line))
     if ws > 1:

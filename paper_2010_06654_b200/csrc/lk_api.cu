@@ -9,6 +9,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <stdlib.h>
 #include <vector>
 
 #include "lk_common.cuh"
@@ -397,6 +398,10 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     LK_CUDA_CHECK(cudaMemcpy(S.pw_prog, prog.data(), prog.size() * 4, cudaMemcpyHostToDevice));
     LK_CUDA_CHECK(cudaMemset(S.done, 0, 16));
     S.lazy = L.size[B_GLB] > 0 ? 1 : 0;
+    {
+        const char* e = getenv("LK_SGATE");  // A/B knob for the centroid-separation gate
+        S.sgate = e ? (atoi(e) != 0) : 1;
+    }
     S.dcum = buf<float>(c, B_DCUM);
     S.dgcum = buf<float>(c, B_DGCUM);
     S.glb = buf<float>(c, B_GLB);
@@ -732,7 +737,7 @@ lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
     }
     cudaStream_t st = (cudaStream_t)stream;
     ProfScope p(c, 4, st);
-    const bool need_half = c->cfg.strategy != LK_STRAT_LLOYD;
+    const bool need_half = c->cfg.strategy != LK_STRAT_LLOYD && c->S.sgate;
     lk_status s = lkh::launch_update(c->S, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV),
                                      buf<double>(c, B_SSE_PART), need_half, st);
     c->launches += need_half ? 2 : 1;

@@ -90,6 +90,7 @@ struct DevState {
     // (lk_yy_fused.cu): bounds are stored against cumulative drifts, so a row
     // whose bounds still prune is never rewritten
     int32_t lazy;
+    int32_t sgate;          // Hamerly's centroid-separation gate on (s_half maintained)
     float* dcum;            // [k] cumulative centroid drift (rounded up)
     float* dgcum;           // [t] cumulative group drift (rounded up); scal[4] = cumulative max drift
     float* glb;             // [n] stored global lower bound (min over the groups)

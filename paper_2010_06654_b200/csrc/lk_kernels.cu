@@ -502,7 +502,8 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
         if (changed == 0) *S.done = 1;
     }
     // s_half is rebuilt by k_half_sep's atomicMin: start from +inf
-    for (int j = tid; j < S.k; j += blockDim.x) S.s_half[j] = INFINITY;
+    // (gate off: s = 0 never prunes)
+    for (int j = tid; j < S.k; j += blockDim.x) S.s_half[j] = S.sgate ? INFINITY : 0.f;
     // group drifts (Yinyang): max drift over each group's members
     if (S.gdrift) {
         __syncthreads();

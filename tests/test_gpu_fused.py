@@ -1,0 +1,102 @@
+"""GPU parity of the fused Yinyang kernel (lk_yy_fused.cu, d <= 32 and
+t <= 32 groups) and its drift-offset ("lazy") bound encoding, across the
+template instances it dispatches to (d in {2, 4, 8, 16, 32} padded, group
+slots in {4, 8, 16, 32}), against the CPU oracle's Lloyd trajectory.
+
+Reference semantics: Yinyang (pruners.py:387-497) returns Lloyd's labels at
+every iteration (tests/test_pruners.py:38-49), so the oracle's run_lloyd
+trajectory is the expected output for every grouping.
+"""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from test_gpu_parity import centroid_ok, check_trajectory
+
+pytestmark = pytest.mark.gpu
+
+
+def blobs(n, d, centers, sigma, seed, dup_frac=0.0):
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-20, 20, size=(centers, d))
+    lab = rng.integers(0, centers, size=n)
+    x = (c[lab] + rng.normal(0, sigma, size=(n, d))).astype(np.float32)
+    if dup_frac:
+        m = int(n * dup_frac)
+        x[:m] = x[rng.integers(0, n, size=m)]  # exact duplicates: tie-heavy rows
+    return x
+
+
+def run_groups(x, k, init, t_max, groups):
+    from paper_2010_06654_b200.device import DeviceLloyd
+    eng = DeviceLloyd(x, k, "yinyang", t_max, groups=groups, group_seed=1)
+    try:
+        return eng.run(init)
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 8, 13, 16, 24, 32])
+@pytest.mark.parametrize("groups", [4, 8, 16, 32])
+def test_fused_dims_and_groups(oracle, d, groups):
+    n, k, t_max = 6000, 96, 12
+    x = blobs(n, d, 24, 1.5, seed=100 + d, dup_frac=0.05)
+    rng = np.random.default_rng(7 + d)
+    init = x[rng.choice(n, k, replace=False)].astype(np.float64)
+    out = run_groups(x, k, init, t_max, groups)
+    ref = oracle.run_lloyd(x, k, init, t_max)
+    check_trajectory(oracle, x, init, out["history"], ref["history"], f"d={d} t={groups}")
+    assert out["converged"] == ref["converged"]
+    assert centroid_ok(out["centroids"], ref["centroids"], x)
+
+
+def test_fused_more_groups_than_centroids(oracle):
+    """k < t: empty group slots carry +inf bounds and are never scanned."""
+    x = blobs(3000, 2, 5, 1.0, seed=5)
+    init = x[:6].astype(np.float64)
+    out = run_groups(x, 6, init, 10, 16)
+    ref = oracle.run_lloyd(x, 6, init, 10)
+    check_trajectory(oracle, x, init, out["history"], ref["history"], "k<t")
+
+
+def test_fused_multi_chunk_queue(oracle):
+    """Enough rows per block that the block-local queue fills and drains many
+    times within one launch (several chunks per persistent block)."""
+    x = blobs(400_000, 2, 300, 3.0, seed=11)
+    k = 300
+    init = x[np.random.default_rng(2).choice(len(x), k, replace=False)].astype(np.float64)
+    out = run_groups(x, k, init, 6, 16)
+    ref = oracle.run_lloyd(x, k, init, 6)
+    check_trajectory(oracle, x, init, out["history"], ref["history"], "multi-chunk")
+    assert centroid_ok(out["centroids"], ref["centroids"], x)
+
+
+SMALL_QUEUE = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
+from oracle import oracle
+from test_gpu_fused import blobs, run_groups
+from test_gpu_parity import check_trajectory
+x = blobs(60_000, 2, 120, 2.0, seed=3)
+k = 128
+init = x[np.random.default_rng(4).choice(len(x), k, replace=False)].astype(np.float64)
+out = run_groups(x, k, init, 8, 32)
+ref = oracle.run_lloyd(x, k, init, 8)
+check_trajectory(oracle, x, init, out["history"], ref["history"], "small queue")
+print("ok")
+"""
+
+
+def test_fused_tiny_pair_buffer():
+    """LK_YY_PCAP=256: a chunk's pairs overflow the block's pair buffer, so
+    rows of one chunk are queued across several drains (the enqueue loop)."""
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tests = os.path.join(repo, "tests")
+    env = dict(os.environ, LK_YY_PCAP="256")
+    r = subprocess.run([sys.executable, "-c", SMALL_QUEUE.format(repo=repo, tests=tests)],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
