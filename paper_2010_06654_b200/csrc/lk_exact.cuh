@@ -141,13 +141,34 @@ __device__ __forceinline__ void refine_move(const DevState& S, const double* qsc
     int64_t* dS = S.delta;
     int64_t* dN = S.delta + (int64_t)S.k * S.d;
     int64_t* dQ = dN + S.k;
-    for (int z = 0; z < S.d; z++) {
-        const double v = load_x(S, row, z);
-        const long long q = __double2ll_rn(v * qscale[z]);
-        if (q) {
-            atomicAdd((unsigned long long*)(dS + (int64_t)nw * S.d + z), (unsigned long long)q);
-            if (old >= 0)
-                atomicAdd((unsigned long long*)(dS + (int64_t)old * S.d + z), (unsigned long long)(-q));
+    if (DP > 0) {
+        // short rows: all loads first (independent), then the atomics
+        constexpr int P = DP > 0 ? DP : 1;
+        double v[P], sc[P];
+#pragma unroll
+        for (int z = 0; z < P; z++) {
+            v[z] = z < S.d ? load_x(S, row, z) : 0.0;
+            sc[z] = z < S.d ? __ldg(qscale + z) : 0.0;
+        }
+#pragma unroll
+        for (int z = 0; z < P; z++) {
+            const long long q = z < S.d ? __double2ll_rn(v[z] * sc[z]) : 0;
+            if (q) {
+                atomicAdd((unsigned long long*)(dS + (int64_t)nw * S.d + z), (unsigned long long)q);
+                if (old >= 0)
+                    atomicAdd((unsigned long long*)(dS + (int64_t)old * S.d + z),
+                              (unsigned long long)(-q));
+            }
+        }
+    } else {
+        for (int z = 0; z < S.d; z++) {
+            const double v = load_x(S, row, z);
+            const long long q = __double2ll_rn(v * qscale[z]);
+            if (q) {
+                atomicAdd((unsigned long long*)(dS + (int64_t)nw * S.d + z), (unsigned long long)q);
+                if (old >= 0)
+                    atomicAdd((unsigned long long*)(dS + (int64_t)old * S.d + z), (unsigned long long)(-q));
+            }
         }
     }
     const double x2 = DP > 0 ? row_norm2_refine_r<(DP > 0 ? DP : 1)>(S, row) : row_norm2_refine(S, row);

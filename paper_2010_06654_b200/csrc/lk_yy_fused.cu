@@ -281,7 +281,7 @@ __device__ __forceinline__ void drain(const DevState& S, int64_t* stat, const do
 }
 
 template <int DP, int T, bool STAGED>
-__global__ void __launch_bounds__(kThreads) k_yy_fused(DevState S, int64_t* stat,
+__global__ void __launch_bounds__(kThreads, (DP <= 4 ? 3 : 2)) k_yy_fused(DevState S, int64_t* stat,
                                                       const double* qscale, int pcap,
                                                       int lg_parts) {
     if (*S.done) return;
@@ -541,9 +541,10 @@ template <int DP, int T, bool STAGED>
 static lk_status launch_fused_t(const lk::DevState& S, int64_t* stat, const double* qscale,
                                 int sms, size_t smem, int pcap, cudaStream_t st) {
     // lanes per (row, group) scan: split the average group into parts of >= 16
+    // members, or of >= 96 member-dimensions when the rows are long
     const int gs = S.k / (S.t_groups > 0 ? S.t_groups : 1);
     int lg = 0;
-    while (lg < 5 && gs / (2 << lg) >= 16) lg++;
+    while (lg < 5 && (gs / (2 << lg) >= 16 || gs * DP / (2 << lg) >= 96)) lg++;
     auto kern = k_yy_fused<DP, T, STAGED>;
     int occ = 0;
     LK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
