@@ -164,8 +164,9 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->bucket_cap = bcap;
         L->size[B_YPAIRS4] = (uint64_t)bcap * L->groups * 8;
         L->size[B_YBUCKET] = (uint64_t)(L->groups + 1) * 8;
-        if (L->groups <= 32 && c.d <= 32) {
-            // lazy (drift-offset) bounds of the fused path
+        if (L->groups <= 32 && c.d <= 32 && !tc_enabled(c)) {
+            // lazy (drift-offset) bounds of the fused path (SIMT group scans;
+            // tensor-core runs rescan failing rows in full instead)
             L->size[B_DCUM] = (uint64_t)k * 4;
             L->size[B_DGCUM] = (uint64_t)L->groups * 4;
             L->size[B_GLB] = (uint64_t)n * 4;
@@ -636,7 +637,8 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             if (s != LK_OK) return s;
             c->launches += 1;
         } else if (is_group_strategy(c->cfg.strategy)) {
-            const bool full_only = use_tc && !lkh::yy_masked(S);
+            // tensor-core runs: every row failing the bounds is rescanned in full
+            const bool full_only = use_tc;
             if (lkh::yy_fused_ok(S)) {
                 // one kernel: filter, group scans, certified merge, refinement
                 // deltas (lk_yy_fused.cu); then the fp64 recheck of the rows it

@@ -361,7 +361,12 @@ __global__ void __launch_bounds__(kThreads) k_filter_hamerly(DevState S, int64_t
             float u = __fadd_ru(S.ub[i], S.drift[a]);
             float l = fmaxf(__fsub_rd(S.lb[i], a == amax ? dmax2 : dmax1), 0.f);
             float gate = fmaxf(l, S.s_half[a]);
-            if (!(gate > u)) {
+            if (!(gate > u) && S.Xlo != nullptr && S.d >= 32) {
+                // long rows on the tensor cores: skip the 2d-load tighten, the
+                // full rescan decides the row anyway
+                active = true;
+                need = true;
+            } else if (!(gate > u)) {
                 active = true;
                 const float* xp = S.X32 + i * S.ldx;
                 const float* cp = S.C32 + (int64_t)a * S.ldc;

@@ -131,7 +131,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_yinyang(DevState S, int6
             // d(x, c_j) >= 2 s_a - ub >= ub for all j != a when s_a > ub.
             const float sa = S.s_half[a];
             gmin = fmaxf(gmin, sa);
-            if (!(gmin > u)) {
+            if (!(gmin > u) && full_only && S.d >= 32) {
+                // long rows on the tensor cores: a tighten costs 2d loads per
+                // row, the full rescan decides the row anyway
+                active = true;
+                need = true;
+            } else if (!(gmin > u)) {
                 active = true;
                 const float* xp = S.X32 + i * S.ldx;
                 acc_a = dist2_row(S, xp, a);
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_yinyang(DevState S, int6
                 need = !(gmin > u);
             }
             S.ub[i] = u;
-            if (need) {
+            if (need && !full_only) {
                 for (int g0 = 0; g0 < t; g0 += kCh) {
                     float v[kCh];
 #pragma unroll

@@ -585,7 +585,9 @@ static lk_status launch_fused_tt(const lk::DevState& S, int64_t* stat, const dou
     return launch_fused_dp<32, T>(S, stat, qscale, sms, st);
 }
 
-bool yy_fused_ok(const lk::DevState& S) { return S.t_groups <= 32 && S.d <= 32; }
+// the fused path owns the lazy bound encoding (allocated for d <= 32, t <= 32
+// and no tensor cores)
+bool yy_fused_ok(const lk::DevState& S) { return S.lazy != 0; }
 
 template <int DP, int T>
 static lk_status fused_attr_dp() {
