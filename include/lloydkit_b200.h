@@ -96,7 +96,8 @@ typedef enum {
     LK_BUF_LABELS = 3,     /* int32  [n_local]       current labels */
     LK_BUF_UB = 4,         /* float  [n_local]       upper bounds */
     LK_BUF_LB = 5,         /* float  [nlb, n_local]  lower bounds (group-major) */
-    LK_BUF_DELTA = 6,      /* int64  [delta_len]     all-reduce payload */
+    LK_BUF_DELTA = 6,      /* int64  [delta_len]     all-reduce payload; accumulated by
+                              lk_step_assign, consumed and zeroed by lk_step_update */
     LK_BUF_STATS = 7,      /* int64  [t_max, LK_NSTAT] per-iteration counters */
     LK_BUF_SSE = 8,        /* double [t_max]         per-iteration SSE */
     LK_BUF_GROUP_OF = 9,   /* int32  [k]             centroid -> group */
@@ -166,7 +167,7 @@ lk_status lk_set_centroids(lk_ctx *ctx, const double *c64, void *stream);
  * graph captured from one iteration replays every later one; t only selects
  * the first-iteration (full scan) path. */
 lk_status lk_step_assign(lk_ctx *ctx, int32_t t, void *stream);
-/* Iteration t: apply the (reduced) deltas, new centroids (empty clusters keep
+/* Iteration t: apply the (reduced) deltas and zero them, new centroids (empty clusters keep
  * theirs), drifts, bound tables, SSE into LK_BUF_SSE[t-1], done flag. */
 lk_status lk_step_update(lk_ctx *ctx, int32_t t, void *stream);
 
