@@ -149,6 +149,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 
+// tcgen05.ld without the wait (several loads in flight, one tcgen05.wait::ld)
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // ---- certification (D-space error bound) ------------------------------------
 
 // |D_true - D~| <= kappa * |x| |c| + 8u (|x|^2 + |c|^2) for the 3xTF32 form;
@@ -350,6 +369,11 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
             // MODE_COLLECT: every j with D' <= thr goes into the row's candidate slots
             float b1 = INFINITY, b2 = INFINITY;
             int j1 = 0;
+            // SPLIT top-2: four chains over columns of residue e mod 4, merged below
+            float cb1[4], cb2[4];
+            int cj1[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) { cb1[e] = INFINITY; cb2[e] = INFINITY; cj1[e] = 0x7fffffff; }
             float thr = -INFINITY;
             int cnt = 0;
             int* slots = nullptr;
@@ -365,9 +389,77 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * NACC * BN;
                 const int jbase = ct * BN;
+                if (SPLIT && MODE == kCollect) {
+                    // this warp's 64 columns: every j under the row's threshold
+                    const int c0 = h * 64;
+                    uint32_t r0[32], r1[32], x0[32], x1[32];
+                    tmem_ld32_async(taddr + c0, r0);
+                    tmem_ld32_async(taddr + c0 + 32, r1);
+                    tmem_ld32_async(taddr + BN + c0, x0);
+                    tmem_ld32_async(taddr + BN + c0 + 32, x1);
+                    const int jb = jbase + c0;
+                    const float4* cp = reinterpret_cast<const float4*>(S.cn2 + jb);
+                    float4 cv[16];
+#pragma unroll
+                    for (int c4 = 0; c4 < 16; c4++) cv[c4] = __ldg(cp + c4);
+                    tmem_wait_ld();
+                    unsigned hit0 = 0, hit1 = 0;  // columns under the threshold
+#pragma unroll
+                    for (int c4 = 0; c4 < 16; c4++) {
+                        const float cc[4] = {cv[c4].x, cv[c4].y, cv[c4].z, cv[c4].w};
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            const int col = c4 * 4 + e;
+                            const float vh = __uint_as_float(col < 32 ? r0[col & 31] : r1[col & 31]);
+                            const float vx = __uint_as_float(col < 32 ? x0[col & 31] : x1[col & 31]);
+                            const bool in = fmaf(-2.0f, vh + vx, cc[e]) <= thr;
+                            if (col < 32) hit0 |= (unsigned)in << (col & 31);
+                            else hit1 |= (unsigned)in << (col & 31);
+                        }
+                    }
+                    if (valid) {
+                        for (unsigned m = hit0; m; m &= m - 1) {
+                            if (cnt < cap) slots[cnt] = jb + __ffs(m) - 1;
+                            cnt++;
+                        }
+                        for (unsigned m = hit1; m; m &= m - 1) {
+                            if (cnt < cap) slots[cnt] = jb + 32 + __ffs(m) - 1;
+                            cnt++;
+                        }
+                    }
+                }
+                if (SPLIT && MODE == kTop2) {
+                    // this warp's 64 columns of both accumulators: four loads in
+                    // flight, one wait; four independent top-2 chains (ILP)
+                    const int c0 = h * 64;
+                    uint32_t r0[32], r1[32], x0[32], x1[32];
+                    tmem_ld32_async(taddr + c0, r0);
+                    tmem_ld32_async(taddr + c0 + 32, r1);
+                    tmem_ld32_async(taddr + BN + c0, x0);
+                    tmem_ld32_async(taddr + BN + c0 + 32, x1);
+                    const int jb = jbase + c0;
+                    const float4* cp = reinterpret_cast<const float4*>(S.cn2 + jb);
+                    float4 cv[16];
+#pragma unroll
+                    for (int c4 = 0; c4 < 16; c4++) cv[c4] = __ldg(cp + c4);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c4 = 0; c4 < 16; c4++) {
+                        const float cc[4] = {cv[c4].x, cv[c4].y, cv[c4].z, cv[c4].w};
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            const int col = c4 * 4 + e;
+                            const float vh = __uint_as_float(col < 32 ? r0[col & 31] : r1[col & 31]);
+                            const float vx = __uint_as_float(col < 32 ? x0[col & 31] : x1[col & 31]);
+                            const float dp = fmaf(-2.0f, vh + vx, cc[e]);
+                            if (dp < cb1[e]) { cb2[e] = cb1[e]; cb1[e] = dp; cj1[e] = jb + col; }
+                            else cb2[e] = fminf(cb2[e], dp);
+                        }
+                    }
+                }
 #pragma unroll 1
                 for (int c0 = 0; c0 < BN; c0 += 32) {
-                    if (SPLIT && ((c0 >> 5) & 1) != h) continue;
+                    if (SPLIT) break;  // handled above
                     float v[32];
                     tmem_ld32(taddr + c0, v);
                     if (SPLIT) {
@@ -424,7 +516,17 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                 continue;
             }
             if (SPLIT) {
-                // merge the two halves' top-2 in (value, index) order
+                // merge the four chains, then the two halves, in (value, index) order
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    if (cb1[e] < b1 || (cb1[e] == b1 && cj1[e] < j1)) {
+                        b2 = fminf(b1, cb2[e]);
+                        b1 = cb1[e];
+                        j1 = cj1[e];
+                    } else {
+                        b2 = fminf(b2, cb1[e]);
+                    }
+                }
                 if (h == 1) {
                     xb1[par][row_in_tile] = b1;
                     xb2[par][row_in_tile] = b2;
