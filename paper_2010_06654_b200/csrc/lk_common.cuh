@@ -108,13 +108,19 @@ __device__ __forceinline__ float store_ub(const DevState& S, float U, int label)
 }
 
 // Finalize a row's lower bounds from one certified bound on every non-winning
-// centroid (Hamerly: the single slot; Yinyang: every group slot).
-// The bound table is group-major, lb[g * n + row], so a warp's loads of one
-// group's bounds are coalesced.  Lazy encoding: lb_s[g] = v + Dg[g] and
-// glb_s = v + Dm, rounded down.
+// centroid (Hamerly: the single slot; Yinyang: every group slot).  Lazy
+// encoding: lb_s[g] = v + Dg[g] and glb_s = v + Dm, rounded down.
+// Index of (row, group g) in the bound table: group-major [nlb, n] (a warp's
+// loads of one group coalesce), except in the lazy encoding, which is
+// row-major [n, nlb] (only failing rows read their groups: one contiguous
+// 16-128 B row, no sectors fetched for rows that prune).
+__device__ __forceinline__ int64_t lb_index(const DevState& S, int64_t row, int g) {
+    return S.lazy ? row * S.nlb + g : (int64_t)g * S.n + row;
+}
+
 __device__ __forceinline__ void write_lb_all(const DevState& S, int64_t row, float v) {
     if (S.lazy) {
-        for (int g = 0; g < S.nlb; g++) S.lb[(int64_t)g * S.n + row] = __fadd_rd(v, S.dgcum[g]);
+        for (int g = 0; g < S.nlb; g++) S.lb[row * S.nlb + g] = __fadd_rd(v, S.dgcum[g]);
         S.glb[row] = __fadd_rd(v, S.scal[4]);
         return;
     }

@@ -247,10 +247,10 @@ __global__ void __launch_bounds__(kThreads) k_seed_yinyang(DevState S, int64_t* 
                 else b2 = fminf(b2, acc);
             }
             if (valid && j9 > j0)
-                S.lb[(int64_t)g * ln + i] =
+                S.lb[lb_index(S, i, g)] =
                     fmaxf((sqrtf(b1) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
             else if (valid)
-                S.lb[(int64_t)g * ln + i] = INFINITY;
+                S.lb[lb_index(S, i, g)] = INFINITY;
             if (b1 < bestD) {
                 secD = fminf(secD, bestD);
                 bestD = b1; bestP = p1; bestG = g; bestg2 = b2;
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kThreads) k_seed_yinyang(DevState S, int64_t* 
             S.labels[i] = j1;
             // iteration 1: the cumulative drifts of the lazy encoding are 0
             S.ub[i] = U1;
-            S.lb[(int64_t)bestG * ln + i] =
+            S.lb[lb_index(S, i, bestG)] =
                 isinf(bestg2) ? INFINITY
                               : fmaxf((sqrtf(bestg2) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
             if (S.glb) S.glb[i] = fmaxf(L2, 0.f);  // bounds every non-winner: min of the groups

@@ -108,7 +108,6 @@ __device__ __forceinline__ void drain(const DevState& S, int64_t* stat, const do
                                    Queue<DP>& Q, int nrow, int npair, const Shared& sh,
                                    const float* cg, int cstride, int lg_parts, float rho,
                                    float cmax, int64_t& n_dist) {
-    const int64_t ln = S.n;
     // ---- bucket offsets of the groups
     if (threadIdx.x < 32) {
         const int c = threadIdx.x < T ? sh.bcnt[threadIdx.x] : 0;
@@ -243,7 +242,7 @@ __device__ __forceinline__ void drain(const DevState& S, int64_t* stat, const do
                 mv = bestJ != a;
                 if (mv) S.labels[i] = bestJ;
                 S.ub[i] = __fsub_ru(U1, S.dcum[bestJ]);
-                float* lbr = S.lb + i;
+                float* lbr = S.lb + i * T;  // row-major group table (lazy encoding)
                 float gnew = Q.lun[q];  // min over the unscanned groups
                 e = poff;
                 for (unsigned mm = mask; mm; mm &= mm - 1, e++) {
@@ -252,7 +251,7 @@ __device__ __forceinline__ void drain(const DevState& S, int64_t* stat, const do
                     const float gm = (sh.rp1[e] == bestJ) ? sh.rb2[e] : sh.rb1[e];
                     const float lg = isinf(gm) ? INFINITY : (sqrtf(gm) - a2) * (1.0f - rho);
                     gnew = fminf(gnew, lg);
-                    lbr[(int64_t)g * ln] = __fadd_rd(lg, sh.dg[g]);
+                    lbr[g] = __fadd_rd(lg, sh.dg[g]);
                 }
                 if (mv) {
                     // the old label joins its group's competitors (needed when
@@ -260,7 +259,7 @@ __device__ __forceinline__ void drain(const DevState& S, int64_t* stat, const do
                     const int go = S.group_of[a];
                     const float la = (sqrtf(acc_a) - kU32 * (xn + S.cnorm[a])) * (1.0f - rho);
                     gnew = fminf(gnew, la);
-                    lbr[(int64_t)go * ln] = fminf(lbr[(int64_t)go * ln], __fadd_rd(la, sh.dg[go]));
+                    lbr[go] = fminf(lbr[go], __fadd_rd(la, sh.dg[go]));
                 }
                 S.glb[i] = __fadd_rd(gnew, sh.dm);
             } else {
@@ -348,7 +347,6 @@ __global__ void __launch_bounds__(kThreads, (DP <= 4 ? 3 : 2)) k_yy_fused(DevSta
 
     const float rho = simt_rel_err(S.d);
     const float cmax = S.scal[0];
-    const int64_t ln = S.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t n_dist = 0, n_active = 0, n_need = 0, n_pairs = 0;
     int q0 = 0, p0 = 0;  // queued rows / pairs (block-uniform)
@@ -399,9 +397,15 @@ __global__ void __launch_bounds__(kThreads, (DP <= 4 ? 3 : 2)) k_yy_fused(DevSta
                 n_active++;
                 // the group table, loaded alongside the point for the tighten
                 float v[T];
-                const float* lp = S.lb + i;
+                const float4* lp = reinterpret_cast<const float4*>(S.lb + i * T);
 #pragma unroll
-                for (int g = 0; g < T; g++) v[g] = __ldcs(lp + g * ln);
+                for (int g4 = 0; g4 < T / 4; g4++) {
+                    const float4 q4 = __ldcs(lp + g4);
+                    v[4 * g4] = q4.x;
+                    v[4 * g4 + 1] = q4.y;
+                    v[4 * g4 + 2] = q4.z;
+                    v[4 * g4 + 3] = q4.w;
+                }
                 const float* xp = S.X32 + i * S.ldx;
                 const float* cp = STAGED ? cgs + c_ginv[a] * sd : S.C32 + (int64_t)a * ldc;
                 float xn2 = 0.f;
