@@ -211,11 +211,18 @@ def run_ours(args):
     from paper_2010_06654_b200.device import DeviceLloyd
 
     ws, rank, local = dist_env()
+    # one process per GPU; LK_DIST_BACKEND=gloo (host-staged exchange) lets the
+    # multi-rank flow run on a single-GPU box for testing
+    backend = os.environ.get("LK_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     group = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
 
     cfg = datasets.CONFIGS[args.workload]
@@ -339,6 +346,43 @@ def run_ours(args):
 
     # e2e through the public API, pinned host input
     e2e = None
+    if ws > 1:
+        # multi-GPU public API (distributed.py): each rank binds its pinned host
+        # shard, runs the sharded protocol (one NCCL all-reduce per iteration)
+        # and reads its labels back; wall time max over ranks
+        import torch.distributed as dist
+        from paper_2010_06654_b200.distributed import DeviceEngine, ShardedLloyd
+        xs = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+
+        def sharded_call():
+            dev = DeviceLloyd(xs, k, gpu_strat, T, kernel=args.kernel, comm=group, n_total=n,
+                              groups=n_groups, group_seed=cfg.seed_init, record_history=False)
+            drv = ShardedLloyd(DeviceEngine(dev), group)
+            drv.bind()
+            out = drv.run(init, T)
+            dev.close()
+            return out
+
+        sharded_call()  # warm-up
+        walls = []
+        for _ in range(3):
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = sharded_call()
+            torch.cuda.synchronize()
+            w = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            dist.all_reduce(w, op=dist.ReduceOp.MAX)
+            walls.append(float(w.item()))
+        wall = statistics.median(walls)
+        its = res.iterations
+        e2e = {"value": its / wall, "unit": "iterations/s",
+               "h2d_bytes_per_step": int((x_full.nbytes + ws * init.nbytes) / its),
+               "d2h_bytes_per_step": int((8 * n + ws * k * d * 8) / its),
+               "iterations": its, "wall_s": wall, "calls": 3, "statistic": "median",
+               "includes": "per rank: context+workspace setup, H2D of its pinned shard, the "
+                           "sharded iterations (one all-reduce of the int64 delta each), its "
+                           "labels and the centroids D2H; wall time max over ranks"}
     if ws == 1:
         import paper_2010_06654_b200 as lk
         xp = torch.from_numpy(x_full).pin_memory()
