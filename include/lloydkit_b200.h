@@ -86,6 +86,11 @@ typedef struct {
     int32_t has_x64;       /* 1: an fp64 copy of X is bound (input not fp32-exact) */
     int32_t device;        /* CUDA device ordinal */
     int64_t history_cap;   /* label-history log entries (0: no history log) */
+    int32_t ranks;         /* ranks sharing the rows (0 or 1: single process);
+                              informational, every delta of an iteration is
+                              produced by lk_step_assign, before the caller's
+                              all-reduce */
+    int32_t reserved;
 } lk_config;
 
 /* Named buffers inside the workspace (byte offsets via lk_buffer). */

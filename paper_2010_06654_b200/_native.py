@@ -49,6 +49,8 @@ class LkConfig(ctypes.Structure):
         ("has_x64", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("history_cap", ctypes.c_int64),
+        ("ranks", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -22,6 +22,7 @@
 #include "lk_exact.cuh"
 #include "lk_internal.h"
 
+
 namespace lk {
 
 constexpr int kThreads = 256;
@@ -229,9 +230,52 @@ __global__ void __launch_bounds__(kThreads) k_assign_gen(DevState S, const int32
 }
 
 // ---------------------------------------------------------------------------
-// K1x: exact fp64 recheck, numpy pairwise order (one warp per flagged row)
+// K1x: exact fp64 recheck, numpy pairwise order (one block per flagged row)
 
-constexpr int kRcWarps = 4;
+// One flagged row, the whole block: x staged in shared memory (xr: >= d
+// doubles), every thread takes k/256 centroids, lexicographic top-2 merge.
+// Block-uniform call.
+__device__ __forceinline__ void recheck_row_block(const DevState& S, int64_t* stat,
+                                                  const double* qscale_inline, int64_t row,
+                                                  double* xr) {
+    __shared__ double rb1[kThreads / 32], rb2[kThreads / 32];
+    __shared__ int rj1[kThreads / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    for (int z = threadIdx.x; z < S.d; z += kThreads)
+        xr[z] = S.X64 ? S.X64[row * S.d + z] : (double)S.X32[row * S.ldx + z];
+    __syncthreads();
+    double b1 = INFINITY, b2 = INFINITY;
+    int j1 = 0x7fffffff;
+    for (int j = threadIdx.x; j < S.k; j += kThreads) {
+        double dd = __dsqrt_rn(pw_dist2(xr, S.C64 + (int64_t)j * S.d, S.pw_prog, S.pw_len));
+        if (dd < b1) { b2 = b1; b1 = dd; j1 = j; }
+        else b2 = fmin(b2, dd);
+    }
+    // lexicographic (value, index) top-2 merge: warp, then block
+    for (int o = 16; o > 0; o >>= 1)
+        merge_top2(b1, j1, b2, __shfl_xor_sync(LK_FULL_MASK, b1, o),
+                   __shfl_xor_sync(LK_FULL_MASK, j1, o), __shfl_xor_sync(LK_FULL_MASK, b2, o));
+    if (lane == 0) { rb1[warp] = b1; rj1[warp] = j1; rb2[warp] = b2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kThreads / 32; w++) merge_top2(b1, j1, b2, rb1[w], rj1[w], rb2[w]);
+        const int old = S.labels[row];
+        S.labels[row] = j1;
+        if (S.strategy != LK_STRAT_LLOYD) {
+            S.ub[row] = store_ub(S, __double2float_ru(b1 * (1.0 + 1e-12)), j1);
+            write_lb_all(S, row, isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12)));
+        }
+        if (old != j1) {
+            unsigned long long p = atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), 1ull);
+            S.moved[p] = make_int2((int)row, old);
+            if (qscale_inline) {
+                refine_move(S, qscale_inline, row, old, j1);
+                atomicAdd((unsigned long long*)(S.delta + (int64_t)S.k * S.d + 2 * S.k), 1ull);
+            }
+        }
+    }
+}
 
 // qscale_inline != nullptr: the assignment kernel already refined its own
 // moved rows (lk_yy_fused.cu), so the rows moved here add their fixed-point
@@ -240,48 +284,9 @@ __global__ void __launch_bounds__(kThreads) k_recheck_fp64(DevState S, int64_t* 
                                                            const double* qscale_inline) {
     if (*S.done) return;
     extern __shared__ double xr[];  // [d]
-    __shared__ double rb1[kThreads / 32], rb2[kThreads / 32];
-    __shared__ int rj1[kThreads / 32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t m = stat[LK_STAT_FLAGGED];
-    for (int64_t f = blockIdx.x; f < m; f += gridDim.x) {
-        const int64_t row = S.flagged[f];
-        __syncthreads();
-        for (int z = threadIdx.x; z < S.d; z += kThreads)
-            xr[z] = S.X64 ? S.X64[row * S.d + z] : (double)S.X32[row * S.ldx + z];
-        __syncthreads();
-        double b1 = INFINITY, b2 = INFINITY;
-        int j1 = 0x7fffffff;
-        for (int j = threadIdx.x; j < S.k; j += kThreads) {
-            double dd = __dsqrt_rn(pw_dist2(xr, S.C64 + (int64_t)j * S.d, S.pw_prog, S.pw_len));
-            if (dd < b1) { b2 = b1; b1 = dd; j1 = j; }
-            else b2 = fmin(b2, dd);
-        }
-        // lexicographic (value, index) top-2 merge: warp, then block
-        for (int o = 16; o > 0; o >>= 1)
-            merge_top2(b1, j1, b2, __shfl_xor_sync(LK_FULL_MASK, b1, o),
-                       __shfl_xor_sync(LK_FULL_MASK, j1, o), __shfl_xor_sync(LK_FULL_MASK, b2, o));
-        if (lane == 0) { rb1[warp] = b1; rj1[warp] = j1; rb2[warp] = b2; }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int w = 1; w < kThreads / 32; w++) merge_top2(b1, j1, b2, rb1[w], rj1[w], rb2[w]);
-            const int old = S.labels[row];
-            S.labels[row] = j1;
-            if (S.strategy != LK_STRAT_LLOYD) {
-                S.ub[row] = store_ub(S, __double2float_ru(b1 * (1.0 + 1e-12)), j1);
-                write_lb_all(S, row, isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12)));
-            }
-            if (old != j1) {
-                unsigned long long p =
-                    atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), 1ull);
-                S.moved[p] = make_int2((int)row, old);
-                if (qscale_inline) {
-                    refine_move(S, qscale_inline, row, old, j1);
-                    atomicAdd((unsigned long long*)(S.delta + (int64_t)S.k * S.d + 2 * S.k), 1ull);
-                }
-            }
-        }
-    }
+    for (int64_t f = blockIdx.x; f < m; f += gridDim.x)
+        recheck_row_block(S, stat, qscale_inline, S.flagged[f], xr);
 }
 
 // K1c: exact fp64 re-decision of the tensor-core pass's ambiguous rows over
@@ -525,12 +530,12 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const double* qscale,
-                                                               const double* qinv,
-                                                               double* sse_part) {
-    if (*S.done) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int j = blockIdx.x * (kThreads / 32) + warp;
+// One centroid j per warp (warp-uniform call): divide with the empty rule,
+// drift (+ cumulative drift), fp32 / tf32 copies, norms, SSE part; zeroes the
+// consumed delta payload of j.
+__device__ __forceinline__ void update_centroid_warp(const DevState& S, int j, const double* qinv,
+                                                     double* sse_part) {
+    const int lane = threadIdx.x & 31;
     int64_t* dS = S.delta;
     int64_t* dN = S.delta + (int64_t)S.k * S.d;
     int64_t* dQ = dN + S.k;
@@ -585,6 +590,15 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
     }
     for (int z = lane; z < S.d; z += 32) dS[(int64_t)j * S.d + z] = 0;
     }
+}
+
+__global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const double* qscale,
+                                                               const double* qinv,
+                                                               double* sse_part) {
+    if (*S.done) return;
+    const int warp = threadIdx.x >> 5;
+    const int j = blockIdx.x * (kThreads / 32) + warp;
+    update_centroid_warp(S, j, qinv, sse_part);
     // the last block to finish reduces the per-centroid results (threadfence
     // reduction: its reads see every block's writes)
     __shared__ bool last;
@@ -609,11 +623,10 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
 constexpr int kHsT = 64;
 constexpr int kHsDC = 32;
 
-__global__ void __launch_bounds__(kThreads) k_half_sep(DevState S) {
-    if (*S.done) return;
+__device__ __forceinline__ void half_sep_tile(const DevState& S, int tj, int tjp) {
     __shared__ float ta[kHsDC][kHsT + 4];
     __shared__ float tb[kHsDC][kHsT + 4];
-    const int j0 = blockIdx.y * kHsT, jp0 = blockIdx.x * kHsT;
+    const int j0 = tj * kHsT, jp0 = tjp * kHsT;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads
     float acc[4][4];
 #pragma unroll
@@ -668,12 +681,16 @@ __global__ void __launch_bounds__(kThreads) k_half_sep(DevState S) {
     }
 }
 
+__global__ void __launch_bounds__(kThreads) k_half_sep(DevState S) {
+    if (*S.done) return;
+    half_sep_tile(S, blockIdx.y, blockIdx.x);
+}
+
 // Label history as a log: the moved rows of iteration t with their new label
 // (iteration 1 moves every row off -1).  The host rebuilds per-iteration label
 // vectors from it (lloyd.py:140 assign_history) without copying n labels per
 // iteration.  Runs after the refine kernel, before the update.
-__global__ void k_log_history(DevState S) {
-    if (*S.done) return;
+__device__ __forceinline__ void log_history_grid(const DevState& S) {
     const int t = *S.iter;
     if (t < 1 || t > S.t_max) return;
     const int64_t m = S.cur[LK_STAT_CHANGED];
@@ -686,6 +703,11 @@ __global__ void k_log_history(DevState S) {
         const int row = S.moved[e].x;
         S.hlog[base + e] = make_int2(row, S.labels[row]);
     }
+}
+
+__global__ void k_log_history(DevState S) {
+    if (*S.done) return;
+    log_history_grid(S);
 }
 
 __global__ void k_fill_inf(DevState S) {
@@ -834,6 +856,7 @@ lk_status launch_log_history(const DevState& S, int sms, cudaStream_t st) {
 }
 
 lk_status init_simt_attributes() {
+
     const int cap = 96 * 1024;
     LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_reg<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
     LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_reg<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));

@@ -30,6 +30,11 @@ def _torch():
     return torch
 
 
+def _world_size(comm) -> int:
+    import torch.distributed as dist
+    return dist.get_world_size(comm)
+
+
 GROUP_STRATEGIES = ("yinyang", "elkan", "regroup")
 
 
@@ -165,7 +170,8 @@ class DeviceLloyd:
                            strategy=nat.STRAT_IDS[strategy], groups=int(groups),
                            t_max=max(1, self.t_max), kernel=nat.KERNEL_IDS[kernel],
                            has_x64=int(has_x64), device=self.dev.index,
-                           history_cap=self.history_cap)
+                           history_cap=self.history_cap,
+                           ranks=self._ranks(comm))
         self.cfg = cfg
         nbytes = ctypes.c_uint64(0)
         nat.check(self.lib.lk_workspace_bytes(ctypes.byref(cfg), ctypes.byref(nbytes)),
@@ -199,6 +205,14 @@ class DeviceLloyd:
             self.lb = self._view("lb", torch.float32, (self.nlb, self.n))
         self.h2d_bytes = 0
         self._bind(src, has_x64)
+
+    def _ranks(self, comm) -> int:
+        """Ranks sharing the rows: > 1 whenever this context holds one shard
+        (a communicator, or n_total > n), so every delta is produced before
+        the caller's all-reduce."""
+        if comm is not None:
+            return max(2, _world_size(comm))
+        return 2 if self.n_total != self.n else 0
 
     # -- plumbing ---------------------------------------------------------
     def _view(self, name, dtype, shape):
