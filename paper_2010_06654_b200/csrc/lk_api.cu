@@ -40,7 +40,7 @@ enum InternalBuf {
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
-    B_SELF, B_DCUM, B_DGCUM, B_GLB, B_COUNT_
+    B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_COUNT_
 };
 
 struct Layout {
@@ -141,6 +141,13 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_OVF] = (uint64_t)n * 4;
         L->size[B_XG_HI] = (uint64_t)n * L->ldx * 4;
         L->size[B_XG_LO] = (uint64_t)n * L->ldx * 4;
+        // tile centering (rows sorted by label, tiles shifted by a centroid)
+        L->size[B_PTAB] = (uint64_t)k * kpad * 4;
+        L->size[B_PERM] = (uint64_t)n * 4;
+        L->size[B_LCUR] = (uint64_t)(k + 1) * 4;
+        L->size[B_TILE_LAB] = (uint64_t)(n / 128 + 2) * 4;
+        L->size[B_ROWR] = (uint64_t)n * 8;
+        L->size[B_ROWXO] = (uint64_t)n * 4;
 
     }
     if (is_group_strategy(c.strategy)) {
@@ -368,6 +375,19 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.cn2 = buf<float>(c, B_CN2);
     S.Xg_hi = buf<float>(c, B_XG_HI);
     S.Xg_lo = buf<float>(c, B_XG_LO);
+    S.ptab = buf<float>(c, B_PTAB);
+    S.perm = buf<int32_t>(c, B_PERM);
+    S.lcur = buf<int32_t>(c, B_LCUR);
+    S.tile_lab = buf<int32_t>(c, B_TILE_LAB);
+    S.rowR = buf<double>(c, B_ROWR);
+    S.rowxo = buf<float>(c, B_ROWXO);
+    S.kpad = (int32_t)((cfg->k + 255) / 256 * 256);
+    {
+        const char* e = getenv("LK_TC_CENTER");  // A/B knob for the tile centering
+        // measured: pays at d <= 32 (one K chunk, resident A tiles; cfg5 138 -> 121
+        // ms), not at d = 128 / 784 where few rows are ambiguous anyway
+        S.center = (S.ptab != nullptr && (e ? atoi(e) != 0 : cfg->d <= 32)) ? 1 : 0;
+    }
     S.cand_rows = buf<int32_t>(c, B_CAND_ROWS);
     S.cand_thr = buf<float>(c, B_CAND_THR);
     S.cand_lb = buf<float>(c, B_CAND_LB);
@@ -632,8 +652,11 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             c->launches += 1;
         } else if (c->cfg.strategy == LK_STRAT_LLOYD || t == 1) {
             ProfScope p(c, 0, st);
-            s = use_tc ? lkh::launch_assign_tc(S, nullptr, nullptr, stat, n, c->sms, st)
-                       : lkh::launch_assign_simt(S, nullptr, nullptr, stat, n, c->sms, st);
+            // iteration >= 2 on the tensor cores: label-sorted, centroid-shifted tiles
+            s = (use_tc && t >= 2) ? lkh::launch_assign_tc_centered(S, nullptr, nullptr, stat, n,
+                                                                     c->cfg.n_total == n, c->sms, st)
+                : use_tc ? lkh::launch_assign_tc(S, nullptr, nullptr, stat, n, c->sms, st)
+                         : lkh::launch_assign_simt(S, nullptr, nullptr, stat, n, c->sms, st);
             if (s != LK_OK) return s;
             c->launches += 1;
         } else if (is_group_strategy(c->cfg.strategy)) {
@@ -679,7 +702,8 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             }
             ProfScope p(c, 0, st);
             // full rescans: capacity overflow, or every failing row when full_only
-            s = use_tc ? lkh::launch_assign_tc(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st)
+            s = use_tc ? lkh::launch_assign_tc_centered(S, S.work, stat + LK_STAT_WORK, stat, n,
+                                                        false, c->sms, st)
                        : lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
             if (s != LK_OK) return s;
             c->launches += 4;
@@ -691,7 +715,8 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
                 if (s != LK_OK) return s;
             }
             ProfScope p(c, 0, st);
-            s = use_tc ? lkh::launch_assign_tc(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st)
+            s = use_tc ? lkh::launch_assign_tc_centered(S, S.work, stat + LK_STAT_WORK, stat, n,
+                                                        false, c->sms, st)
                        : lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
             if (s != LK_OK) return s;
             c->launches += 2;
@@ -743,6 +768,10 @@ lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
     lk_status s = lkh::launch_update(c->S, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV),
                                      buf<double>(c, B_SSE_PART), need_half, st);
     c->launches += need_half ? 2 : 1;
+    if (s == LK_OK && c->S.center) {
+        s = lkh::launch_pair_table(c->S, st);  // centering offsets of the next iteration
+        c->launches += 1;
+    }
     return s;
 }
 

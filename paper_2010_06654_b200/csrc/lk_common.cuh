@@ -72,6 +72,16 @@ struct DevState {
     int32_t* cand_slots;    // [n, LK_MAX_CAND] collected candidates
     int32_t* cand_cnt;      // [n] candidates found (> LK_MAX_CAND: overflow)
     int32_t* ovf;           // [n] overflow rows (fp32 difference-form rescan)
+    // tile centering of the tensor-core pass (rows sorted by label; each
+    // 128-row tile shifted by its first row's label centroid)
+    int32_t center;         // 1: full passes and rescans run centered
+    int32_t kpad;           // row stride of ptab (k rounded up to 256)
+    float* ptab;            // [k, kpad] ||c_a - c_j||^2 (fp32 difference form), +inf pad
+    int32_t* perm;          // [n] rows sorted by label
+    int32_t* lcur;          // [k + 1] per-label histogram / cursors
+    int32_t* tile_lab;      // [n / 128 + 1] label whose centroid a tile is centered on (-1: none)
+    double* rowR;           // [n] ||x'||^2 + 2 x'.o of each gathered row (x' = x - o)
+    float* rowxo;           // [n] ||x'|| rounded up
     // Yinyang group bounds
     int32_t* gperm;         // [k] centroid ids sorted by group
     int32_t* ginv;          // [k] position of centroid j in gperm

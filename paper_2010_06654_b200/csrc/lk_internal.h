@@ -43,6 +43,12 @@ lk_status launch_yy_merge(const lk::DevState& S, int64_t* stat, int sms, cudaStr
 // tcgen05 path (lk_tc.cu): full-scan assignment with 3xTF32 products.
 bool tc_supported(const lk::DevState& S);
 lk_status launch_tc_prep_points(const lk::DevState& S, int sms, cudaStream_t st);
+// tile centering: the k x k table of squared centroid distances (after every
+// centroid update) and the centered full pass / rescan (iteration >= 2)
+lk_status launch_pair_table(const lk::DevState& S, cudaStream_t st);
+lk_status launch_assign_tc_centered(const lk::DevState& S, const int32_t* rowlist,
+                                    const int64_t* rowcount, int64_t* stat, int64_t max_rows,
+                                    bool counts_are_local, int sms, cudaStream_t st);
 lk_status launch_collect_tc(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
                             cudaStream_t st);
 lk_status launch_assign_tc(const lk::DevState& S, const int32_t* rowlist,

@@ -36,13 +36,19 @@ constexpr int kEpiWarps = 4;
 constexpr int kMaxCand = LK_MAX_CAND;
 constexpr int kThreadsTC = 64 + 32 * kEpiWarps;
 
-template <int BN>
+// Dynamic shared memory: [stages][resident A (ARES)][barriers 256 B][beta x 2]
+// ARES (d <= 32, one K chunk): a row tile's A (x_hi, x_lo) is loaded once and
+// stays resident while the centroid tiles stream through the stages.
+template <int BN, bool ARES = false>
 struct Smem {
     static constexpr int A_BYTES = BM * KC * 4;   // 16 KB
     static constexpr int B_BYTES = BN * KC * 4;   // 16/32 KB
-    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-    static constexpr int STAGES = BN == 256 ? 2 : 3;
-    static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int STAGE_BYTES = ARES ? 2 * B_BYTES : 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int STAGES = ARES ? 4 : (BN == 256 ? 2 : 3);
+    static constexpr int ARES_OFF = STAGES * STAGE_BYTES;
+    static constexpr int BAR_OFF = ARES_OFF + (ARES ? 2 * A_BYTES : 0);
+    static constexpr int BETA_OFF = BAR_OFF + 256;
+    static constexpr int TOTAL = BETA_OFF + 1024 /*align*/;  // + 2 * kpad * 4 when staging beta
 };
 
 // ---- PTX helpers -----------------------------------------------------------
@@ -89,6 +95,14 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// 1-D bulk copy global -> shared, completing on an mbarrier (transaction bytes)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -168,6 +182,13 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // ---- certification (D-space error bound) ------------------------------------
 
 // |D_true - D~| <= kappa * |x| |c| + 8u (|x|^2 + |c|^2) for the 3xTF32 form;
@@ -215,6 +236,8 @@ __device__ __forceinline__ int64_t epi_append(bool pred, unsigned long long* cou
 struct TcArgs {
     int64_t m;            // rows of A (n for a full scan, worklist size for a rescan)
     const int32_t* rowlist;   // A row r -> global row (nullptr: identity)
+    int center;           // A rows are label-sorted tiles shifted by a centroid (k_gather_center)
+    int sbeta;            // centered: the tiles' beta rows are double-buffered in shared memory
     const int64_t* rowcount;  // device row count (overrides m when non-null)
     int n_ct;             // centroid tiles
     int n_kc;             // K chunks
@@ -234,22 +257,34 @@ struct TcShape {
     static constexpr int NACC = SPLIT ? 2 : 1;                     // accumulators per tile
 };
 
-template <int BN, int MODE, bool SPLIT>
+template <int BN, int MODE, bool SPLIT, bool ARES>
 __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
     k_assign_tc(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                 DevState S, TcArgs A, int64_t* stat) {
     if (*S.done) return;
-    using SM = Smem<BN>;
+    using SM = Smem<BN, ARES>;
     constexpr int EW = TcShape<SPLIT>::EW, NACC = TcShape<SPLIT>::NACC;
     static_assert(2 * NACC * BN <= 512, "TMEM holds 512 fp32 columns");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = (uint64_t*)(smem + SM::STAGES * SM::STAGE_BYTES);
+    uint8_t* abuf = smem + SM::ARES_OFF;    // resident A (ARES)
+    uint64_t* full = (uint64_t*)(smem + SM::BAR_OFF);
     uint64_t* empty = full + SM::STAGES;
     uint64_t* tfull = empty + SM::STAGES;   // [2]
     uint64_t* tempty = tfull + 2;           // [2]
-    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    uint64_t* afull = tempty + 2;           // resident A loaded
+    uint64_t* aempty = afull + 1;           // resident A free (all MMAs of the row tile done)
+    uint64_t* bfull = aempty + 1;           // [2] staged beta rows
+    uint64_t* bempty = bfull + 2;           // [2]
+    uint32_t* tmem_slot = (uint32_t*)(bempty + 2);
+    float* sbeta = (float*)(smem + SM::BETA_OFF);  // [2][kpad] (A.sbeta)
+    // per-centroid offsets of a tile: ||c_j||^2, or ||c_j - o||^2 when centered
+    auto beta_src = [&](int64_t t_) -> const float* {
+        if (!A.center) return S.cn2;
+        const int at = S.tile_lab[t_];
+        return at >= 0 ? S.ptab + (int64_t)at * S.kpad : S.cn2;
+    };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t m = A.rowcount ? *A.rowcount : A.m;
@@ -263,7 +298,11 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
         for (int b = 0; b < 2; b++) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], EW);
+            mbar_init(&bfull[b], 1);
+            mbar_init(&bempty[b], EW);
         }
+        mbar_init(afull, 1);
+        mbar_init(aempty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_map(&map_ahi);
         prefetch_map(&map_alo);
@@ -286,18 +325,34 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x) {
+            int it = 0;
+            for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x, it++) {
+                if (A.sbeta) {
+                    // the tile's beta row into the double buffer (freed by the epilogue)
+                    const int bb = it & 1;
+                    mbar_wait(&bempty[bb], ((it >> 1) & 1) ^ 1);
+                    mbar_expect_tx(&bfull[bb], (uint32_t)S.kpad * 4);
+                    bulk_load(sbeta + bb * S.kpad, beta_src(rt), (uint32_t)S.kpad * 4, &bfull[bb]);
+                }
+                if (ARES) {
+                    mbar_wait(aempty, (it & 1) ^ 1);
+                    mbar_expect_tx(afull, 2 * SM::A_BYTES);
+                    tma_load_2d(&map_ahi, afull, abuf, 0, (int)(rt * BM));
+                    tma_load_2d(&map_alo, afull, abuf + SM::A_BYTES, 0, (int)(rt * BM));
+                }
                 for (int ct = 0; ct < A.n_ct; ct++) {
                     for (int kc = 0; kc < A.n_kc; kc++) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* st = smem + stage * SM::STAGE_BYTES;
                         mbar_expect_tx(&full[stage], SM::STAGE_BYTES);
                         const int k0 = kc * KC;
-                        tma_load_2d(&map_ahi, &full[stage], st, k0, (int)(rt * BM));
-                        tma_load_2d(&map_alo, &full[stage], st + SM::A_BYTES, k0, (int)(rt * BM));
-                        tma_load_2d(&map_bhi, &full[stage], st + 2 * SM::A_BYTES, k0, ct * BN);
-                        tma_load_2d(&map_blo, &full[stage], st + 2 * SM::A_BYTES + SM::B_BYTES, k0,
-                                    ct * BN);
+                        uint8_t* bst = st + (ARES ? 0 : 2 * SM::A_BYTES);
+                        if (!ARES) {
+                            tma_load_2d(&map_ahi, &full[stage], st, k0, (int)(rt * BM));
+                            tma_load_2d(&map_alo, &full[stage], st + SM::A_BYTES, k0, (int)(rt * BM));
+                        }
+                        tma_load_2d(&map_bhi, &full[stage], bst, k0, ct * BN);
+                        tma_load_2d(&map_blo, &full[stage], bst + SM::B_BYTES, k0, ct * BN);
                         if (++stage == SM::STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -311,7 +366,12 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x) {
+            int it = 0;
+            for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x, it++) {
+                if (ARES) {
+                    mbar_wait(afull, it & 1);
+                    tc_fence_after();
+                }
                 for (int ct = 0; ct < A.n_ct; ct++) {
                     mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
@@ -321,10 +381,12 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
                         uint8_t* st = smem + stage * SM::STAGE_BYTES;
-                        const uint64_t dahi = umma_desc(st);
-                        const uint64_t dalo = umma_desc(st + SM::A_BYTES);
-                        const uint64_t dbhi = umma_desc(st + 2 * SM::A_BYTES);
-                        const uint64_t dblo = umma_desc(st + 2 * SM::A_BYTES + SM::B_BYTES);
+                        uint8_t* ast = ARES ? abuf : st;
+                        uint8_t* bst = st + (ARES ? 0 : 2 * SM::A_BYTES);
+                        const uint64_t dahi = umma_desc(ast);
+                        const uint64_t dalo = umma_desc(ast + SM::A_BYTES);
+                        const uint64_t dbhi = umma_desc(bst);
+                        const uint64_t dblo = umma_desc(bst + SM::B_BYTES);
 #pragma unroll
                         for (int k = 0; k < KC / UK; k++) {
                             const uint64_t off = (uint64_t)((k * UK * 4) >> 4);
@@ -346,6 +408,7 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                     mma_commit(&tfull[acc]);
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
+                if (ARES) mma_commit(aempty);  // the resident A is free once these MMAs finish
             }
         }
     } else {
@@ -362,7 +425,17 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
         __shared__ float xb1[2][BM], xb2[2][BM];
         __shared__ int xj1[2][BM];
         int par = 0;
-        for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x) {
+        int it = 0;
+        for (int64_t rt = blockIdx.x; rt < n_rt; rt += gridDim.x, it++) {
+            // centered runs: the producer staged this tile's beta row (bfull)
+            const int bb = it & 1;
+            const float* beta;
+            if (A.sbeta) {
+                mbar_wait(&bfull[bb], (it >> 1) & 1);
+                beta = sbeta + bb * S.kpad;
+            } else {
+                beta = beta_src(rt);
+            }
             const int64_t r = rt * BM + row_in_tile;
             const bool valid = r < m;
             // MODE_TOP2: running top-2 of D' = |c|^2 - 2 x.c (ties keep the lower index)
@@ -399,14 +472,12 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                     tmem_ld32_async(taddr + BN + c0 + 32, x1);
                     const int jb = jbase + c0;
                     const float4* cp = reinterpret_cast<const float4*>(S.cn2 + jb);
-                    float4 cv[16];
-#pragma unroll
-                    for (int c4 = 0; c4 < 16; c4++) cv[c4] = __ldg(cp + c4);
                     tmem_wait_ld();
                     unsigned hit0 = 0, hit1 = 0;  // columns under the threshold
 #pragma unroll
                     for (int c4 = 0; c4 < 16; c4++) {
-                        const float cc[4] = {cv[c4].x, cv[c4].y, cv[c4].z, cv[c4].w};
+                        const float4 cv = __ldg(cp + c4);
+                        const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
                         for (int e = 0; e < 4; e++) {
                             const int col = c4 * 4 + e;
@@ -438,14 +509,22 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                     tmem_ld32_async(taddr + BN + c0, x0);
                     tmem_ld32_async(taddr + BN + c0 + 32, x1);
                     const int jb = jbase + c0;
-                    const float4* cp = reinterpret_cast<const float4*>(S.cn2 + jb);
-                    float4 cv[16];
-#pragma unroll
-                    for (int c4 = 0; c4 < 16; c4++) cv[c4] = __ldg(cp + c4);
+                    const float4* cp = reinterpret_cast<const float4*>(beta + jb);
+                    // staged beta: explicit shared-memory loads (a select between a
+                    // shared and a global pointer compiles to slow generic loads)
+                    const uint32_t sb = smem_u32(sbeta + bb * S.kpad + jb);
                     tmem_wait_ld();
 #pragma unroll
                     for (int c4 = 0; c4 < 16; c4++) {
-                        const float cc[4] = {cv[c4].x, cv[c4].y, cv[c4].z, cv[c4].w};
+                        float4 cv;
+                        if (A.sbeta) {
+                            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                         : "=f"(cv.x), "=f"(cv.y), "=f"(cv.z), "=f"(cv.w)
+                                         : "r"(sb + 16 * c4));
+                        } else {
+                            cv = __ldg(cp + c4);
+                        }
+                        const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
                         for (int e = 0; e < 4; e++) {
                             const int col = c4 * 4 + e;
@@ -495,6 +574,7 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                 if (lane == 0) mbar_arrive(&tempty[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
+            if (A.sbeta && lane == 0) mbar_arrive(&bempty[bb]);  // this tile's beta row is free
             if (MODE == kCollect) {
                 if (SPLIT) {
                     // the h = 0 warp appends the other half's slots after its own
@@ -557,6 +637,47 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                 const float xn = sqrtf(xn2) * (1.0f + 2 * kU32);
                 const float cn1 = S.cnorm[j1];
                 const float cmax = S.scal[0];
+                if (A.center) {
+                    // D_j = R + D'_j with D'_j = beta_j - 2 x'.c_j (x' = x - o).  Errors:
+                    // the dot, kappa |x'| |c_j|; beta (fp32 difference form),
+                    // (d + 4) u beta_j with beta_j <= |D'_j| + 2 |x'| |c_j|; the final
+                    // FFMA, u |D'_j|; and x' = fl(x - o) moves the point by
+                    // delta <= 2^-24 |x'|: |dD| <= delta (2 sqrt(D) + delta).
+                    // L2 is evaluated at the second-smallest D'~ (the lower bound
+                    // over j != j1 is increasing in D'~_j).
+                    const double R = S.rowR[r];
+                    const double xo = (double)S.rowxo[r];
+                    const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
+                    const double e1 = (double)kappa * xo * cn1 + gb * (fabs((double)b1) + 2.0 * xo * cn1) +
+                                      2.0 * 5.9604644775390625e-08 * fabs((double)b1);
+                    const double eo = (double)kappa * xo * cmax + gb * (fabs((double)b2) + 2.0 * xo * cmax) +
+                                      2.0 * 5.9604644775390625e-08 * fabs((double)b2);
+                    const double ex = isinf(b2) ? 0.0
+                                      : 2.384185791015625e-07 * xo * (sqrt(fmax(R + b2 + eo, 0.0)) + xo);
+                    const double U = (R + b1 + e1 + ex) * (1.0 + 1e-12) + 1e-300;
+                    const double L2 = isinf(b2) ? INFINITY : (R + b2 - eo - ex) - fabs(R) * 1e-12;
+                    if (L2 > U) {
+                        old = S.labels[row];
+                        moved = old != j1;
+                        S.labels[row] = j1;
+                        if (S.strategy != LK_STRAT_LLOYD) {
+                            S.ub[row] = store_ub(S, __double2float_ru(sqrt(fmax(U, 0.0)) * (1.0 + 1e-12)), j1);
+                            write_lb_all(S, row, isinf(L2) ? INFINITY
+                                                            : __double2float_rd(sqrt(fmax(L2, 0.0)) * (1.0 - 1e-12)));
+                        }
+                    } else {
+                        // thresholds of the (uncentered) collect pass: D'unc_j = ||c_j||^2
+                        // - 2 x.c_j; every possible winner has D_j <= U, so
+                        // D'unc~_j <= U - ||x||^2 + e_unc
+                        amb = true;
+                        const double eunc = (double)kappa * xn * cmax + 8.0 * 5.9604644775390625e-08 *
+                                            ((double)xn2 + (double)cmax * cmax);
+                        const double thr = (U - (double)xn2 * (1.0 - 2.384185791015625e-07) + eunc) *
+                                           (1.0 + 1e-9) + 1e-30;
+                        thr_out = __double2float_ru(thr);
+                        lb_out = __double2float_rd(sqrt(fmax(U, 0.0)) * (1.0 - 1e-12));
+                    }
+                } else {
                 const float e1 = kappa * xn * cn1 + 8.0f * kU32 * (xn2 + cn1 * cn1);
                 const float eo = kappa * xn * cmax + 8.0f * kU32 * (xn2 + cmax * cmax);
                 const float U = (xn2 + b1) + e1;
@@ -574,6 +695,7 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                     amb = true;
                     thr_out = (b1 + e1 + eo) * (1.0f + 4 * kU32) + fabsf(b1) * 4 * kU32 + 1e-30f;
                     lb_out = __fsqrt_rd(fmaxf(U, 0.f));
+                }
                 }
             }
             // 128-thread aggregated appends across the epilogue warps (named barrier 1)
@@ -633,6 +755,160 @@ __global__ void k_gather_rows(DevState S, const int32_t* rows, const int64_t* co
     }
 }
 
+// ---- tile centering -----------------------------------------------------------
+//
+// The dot-form error scales with |x| |c|.  Rows sorted by label
+// make a 128-row tile (mostly) one cluster; shifting the tile by the centroid
+// o = c_a of its first row's label gives
+//     ||x - c_j||^2 = R(x') + beta_j - 2 x'.c_j,   x' = x - o,
+//     R(x') = ||x'||^2 + 2 x'.o,   beta_j = ||c_j - o||^2 = ptab[a][j],
+// so the contraction runs on x' (small) against the unshifted centroids (the
+// B operand stays shared by every tile) and the error scales with |x'| |c|.
+
+constexpr int kPtT = 64;
+
+// ptab[a][j] = sum_z (c_a,z - c_j,z)^2 in fp32 difference form (fmaf chain in
+// dimension order), +inf for padding columns j >= k.  64 x 64 tiles.
+__global__ void __launch_bounds__(256) k_pair_table(DevState S) {
+    if (*S.done) return;
+    __shared__ float ta[32][kPtT + 1];
+    __shared__ float tb[32][kPtT + 1];
+    const int a0 = blockIdx.y * kPtT, j0 = blockIdx.x * kPtT;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    float acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int v = 0; v < 4; v++) acc[u][v] = 0.f;
+    for (int z0 = 0; z0 < S.d; z0 += 32) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPtT * 32; e += 256) {
+            const int r = e / 32, z = e % 32, zz = z0 + z;
+            ta[z][r] = (a0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(a0 + r) * S.ldc + zz] : 0.f;
+            tb[z][r] = (j0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(j0 + r) * S.ldc + zz] : 0.f;
+        }
+        __syncthreads();
+        const int zn = min(32, S.d - z0);
+        for (int z = 0; z < zn; z++) {
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    const float t = ta[z][ty + 16 * u] - tb[z][tx + 16 * v];
+                    acc[u][v] = fmaf(t, t, acc[u][v]);
+                }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        const int a = a0 + ty + 16 * u;
+        if (a >= S.k) continue;
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const int j = j0 + tx + 16 * v;
+            if (j < S.kpad) S.ptab[(int64_t)a * S.kpad + j] = j < S.k ? acc[u][v] : INFINITY;
+        }
+    }
+}
+
+// Per-label histogram of a row list (rowlist == nullptr: the label counts of
+// the last refinement are used instead).
+__global__ void k_label_count(DevState S, const int32_t* rowlist, const int64_t* count) {
+    if (*S.done) return;
+    const int64_t m = count ? *count : S.n;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(S.lcur + S.labels[rowlist ? rowlist[p] : p], 1);
+}
+
+// lcur := exclusive prefix of the histogram (from lcur, or from S.counts).
+__global__ void __launch_bounds__(1024) k_label_scan(DevState S, int from_counts) {
+    if (*S.done) return;
+    __shared__ int part[1024];
+    const int k = S.k, per = (k + 1023) / 1024;
+    const int b = threadIdx.x * per;
+    int sum = 0;
+    for (int j = b; j < b + per && j < k; j++) sum += from_counts ? (int)S.counts[j] : S.lcur[j];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int run = part[threadIdx.x] - sum;
+    for (int j = b; j < b + per && j < k; j++) {
+        const int c = from_counts ? (int)S.counts[j] : S.lcur[j];
+        S.lcur[j] = run;
+        run += c;
+    }
+}
+
+// perm[cursor[label]++] = row (order inside a label is arbitrary: labels are
+// certified per row, independent of the tiling).
+__global__ void k_label_scatter(DevState S, const int32_t* rowlist, const int64_t* count) {
+    if (*S.done) return;
+    const int64_t m = count ? *count : S.n;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int row = rowlist ? rowlist[p] : (int)p;
+        S.perm[atomicAdd(S.lcur + S.labels[row], 1)] = row;
+    }
+}
+
+// Gather the sorted rows, shifted by their tile's centroid, split for 3xTF32;
+// per row the fp64 row constant R and |x'| (rounded up); per tile its label.
+// L lanes per row (float4 columns), 32 / L rows per warp in flight.
+__global__ void __launch_bounds__(256) k_gather_center(DevState S, const int64_t* count, int L) {
+    if (*S.done) return;
+    const int64_t m = count ? *count : S.n;
+    const int lane = threadIdx.x & 31, sub = lane & (L - 1);
+    const int rpw = 32 / L;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int c4n = S.ldx / 4;
+    for (int64_t p0 = warp * rpw; p0 < m; p0 += nwarps * rpw) {
+        const int64_t p = p0 + lane / L;
+        const bool ok = p < m;
+        double x2 = 0.0, xo = 0.0;
+        int a = -1;
+        if (ok) {
+            const int64_t row = S.perm[p];
+            a = S.labels[S.perm[p & ~(int64_t)127]];
+            const float4* xp = reinterpret_cast<const float4*>(S.X32 + row * S.ldx);
+            const float4* op = reinterpret_cast<const float4*>(S.C32 + (int64_t)(a >= 0 ? a : 0) * S.ldc);
+            float4* hp = reinterpret_cast<float4*>(S.Xg_hi + p * S.ldx);
+            float4* lp = reinterpret_cast<float4*>(S.Xg_lo + p * S.ldx);
+            for (int c = sub; c < c4n; c += L) {
+                const float4 x = xp[c];
+                const float4 o = a >= 0 ? __ldg(op + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float xs[4] = {x.x - o.x, x.y - o.y, x.z - o.z, x.w - o.w};
+                const float ov[4] = {o.x, o.y, o.z, o.w};
+                float h[4], l[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    h[e] = __uint_as_float(__float_as_uint(xs[e]) & 0xFFFFE000u);
+                    l[e] = xs[e] - h[e];
+                    x2 = fma((double)xs[e], (double)xs[e], x2);
+                    xo = fma((double)xs[e], (double)ov[e], xo);
+                }
+                hp[c] = make_float4(h[0], h[1], h[2], h[3]);
+                lp[c] = make_float4(l[0], l[1], l[2], l[3]);
+            }
+        }
+        for (int o = L >> 1; o > 0; o >>= 1) {
+            x2 += __shfl_xor_sync(LK_FULL_MASK, x2, o);
+            xo += __shfl_xor_sync(LK_FULL_MASK, xo, o);
+        }
+        if (ok && sub == 0) {
+            S.rowR[p] = x2 + 2.0 * xo;
+            S.rowxo[p] = __double2float_ru(sqrt(x2) * (1.0 + 1e-12));
+            if ((p & 127) == 0) S.tile_lab[p >> 7] = a;
+        }
+    }
+}
+
 }  // namespace tc
 }  // namespace lk
 
@@ -680,20 +956,34 @@ bool tc_supported(const DevState& S) {
     return S.Xlo != nullptr && S.d >= 8 && (S.ldx % 4) == 0 && get_encode() != nullptr;
 }
 
-lk_status init_tc_attributes() {
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kTop2, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kCollect, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<256, kTop2, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<256>::TOTAL));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<256, kCollect, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<256>::TOTAL));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kTop2, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
-    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<128, kCollect, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<128>::TOTAL));
+static int g_tc_max_dyn = 0;  // dynamic smem limit of the split kernels (device opt-in max)
+static int tc_max_dyn_smem() { return g_tc_max_dyn; }
+
+template <int BN, int MODE, bool SPLIT, bool ARES>
+static lk_status tc_attr(int optin) {
+    cudaFuncAttributes fa;
+    LK_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_assign_tc<BN, MODE, SPLIT, ARES>));
+    const int lim = optin - (int)fa.sharedSizeBytes;
+    if (SPLIT && (g_tc_max_dyn == 0 || lim < g_tc_max_dyn)) g_tc_max_dyn = lim;
+    LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc<BN, MODE, SPLIT, ARES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SPLIT ? lim : Smem<BN>::TOTAL));
     return LK_OK;
+}
+
+lk_status init_tc_attributes() {
+    int dev = 0, optin = 0;
+    LK_CUDA_CHECK(cudaGetDevice(&dev));
+    LK_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    lk_status s = tc_attr<128, kTop2, false, false>(optin);
+    if (s == LK_OK) s = tc_attr<128, kCollect, false, false>(optin);
+    if (s == LK_OK) s = tc_attr<256, kTop2, false, false>(optin);
+    if (s == LK_OK) s = tc_attr<256, kCollect, false, false>(optin);
+    if (s == LK_OK) s = tc_attr<128, kTop2, true, false>(optin);
+    if (s == LK_OK) s = tc_attr<128, kCollect, true, false>(optin);
+    if (s == LK_OK) s = tc_attr<128, kTop2, true, true>(optin);
+    if (s == LK_OK) s = tc_attr<128, kCollect, true, true>(optin);
+    return s;
 }
 
 // Split accumulators (tighter certification, fewer ambiguous rows) unless
@@ -713,7 +1003,7 @@ lk_status launch_tc_prep_points(const DevState& S, int sms, cudaStream_t st) {
     return LK_OK;
 }
 
-template <int BN, int MODE, bool SPLIT>
+template <int BN, int MODE, bool SPLIT, bool ARES>
 static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo, int64_t a_rows,
                            TcArgs A, int64_t max_rows, int64_t* stat, int sms, cudaStream_t st) {
     CUtensorMap mah, mal, mbh, mbl;
@@ -725,11 +1015,12 @@ static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo
     A.m = max_rows;
     A.n_ct = (S.k + BN - 1) / BN;
     A.n_kc = (S.d + KC - 1) / KC;
-    const int smem = Smem<BN>::TOTAL;
+    int smem = Smem<BN, ARES>::TOTAL;
+    if (A.sbeta) smem += 2 * S.kpad * 4;
     int64_t tiles = (max_rows + BM - 1) / BM;
     int grid = (int)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
-    k_assign_tc<BN, MODE, SPLIT><<<grid, TcShape<SPLIT>::THREADS, smem, st>>>(mah, mal, mbh, mbl, S,
-                                                                             A, stat);
+    k_assign_tc<BN, MODE, SPLIT, ARES><<<grid, TcShape<SPLIT>::THREADS, smem, st>>>(mah, mal, mbh, mbl,
+                                                                                  S, A, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
@@ -737,9 +1028,17 @@ static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo
 template <int MODE>
 static lk_status launch_mode(const DevState& S, const float* ahi, const float* alo, TcArgs A,
                              int64_t max_rows, int64_t* stat, int sms, cudaStream_t st) {
-    if (tc_split()) return launch_bn<128, MODE, true>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
-    if (S.k <= 128) return launch_bn<128, MODE, false>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
-    return launch_bn<256, MODE, false>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
+    if (tc_split()) {
+        // one K chunk (d <= 32): the row tile's A stays resident across centroid tiles
+        const bool ares = S.d <= KC;
+        const int base = ares ? Smem<128, true>::TOTAL : Smem<128, false>::TOTAL;
+        if (A.sbeta && base + 2 * S.kpad * 4 > tc_max_dyn_smem()) A.sbeta = 0;
+        if (ares) return launch_bn<128, MODE, true, true>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
+        return launch_bn<128, MODE, true, false>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
+    }
+    A.sbeta = 0;
+    if (S.k <= 128) return launch_bn<128, MODE, false, false>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
+    return launch_bn<256, MODE, false, false>(S, ahi, alo, S.n, A, max_rows, stat, sms, st);
 }
 
 lk_status launch_assign_tc(const DevState& S, const int32_t* rowlist, const int64_t* rowcount,
@@ -754,6 +1053,46 @@ lk_status launch_assign_tc(const DevState& S, const int32_t* rowlist, const int6
         return launch_mode<kTop2>(S, S.Xg_hi, S.Xg_lo, A, max_rows, stat, sms, st);
     }
     return launch_mode<kTop2>(S, S.X32, S.Xlo, A, max_rows, stat, sms, st);
+}
+
+lk_status launch_pair_table(const DevState& S, cudaStream_t st) {
+    if (!S.center) return LK_OK;
+    const dim3 g((unsigned)(S.kpad / kPtT), (unsigned)((S.k + kPtT - 1) / kPtT));
+    k_pair_table<<<g, 256, 0, st>>>(S);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+// Tensor-core assignment of a row list (nullptr: every row) on label-sorted,
+// centroid-shifted tiles.  Labels must be valid (iteration >= 2).
+lk_status launch_assign_tc_centered(const DevState& S, const int32_t* rowlist,
+                                    const int64_t* rowcount, int64_t* stat, int64_t max_rows,
+                                    bool counts_are_local, int sms, cudaStream_t st) {
+    if (!S.center || !tc_split()) return launch_assign_tc(S, rowlist, rowcount, stat, max_rows, sms, st);
+    const int grid = sms * 8;
+    if (rowlist == nullptr && counts_are_local) {
+        k_label_scan<<<1, 1024, 0, st>>>(S, 1);  // the label counts are the histogram
+        LK_LAUNCH_CHECK();
+    } else {
+        LK_CUDA_CHECK(cudaMemsetAsync(S.lcur, 0, (size_t)(S.k + 1) * 4, st));
+        // (every local row of a shard: its counts are global, histogram the labels)
+        k_label_count<<<grid, 256, 0, st>>>(S, rowlist, rowcount);
+        LK_LAUNCH_CHECK();
+        k_label_scan<<<1, 1024, 0, st>>>(S, 0);
+        LK_LAUNCH_CHECK();
+    }
+    k_label_scatter<<<grid, 256, 0, st>>>(S, rowlist, rowcount);
+    LK_LAUNCH_CHECK();
+    int L = 1;
+    while (L < 32 && L * 2 <= S.ldx / 4) L *= 2;
+    k_gather_center<<<sms * 8, 256, 0, st>>>(S, rowcount, L);
+    LK_LAUNCH_CHECK();
+    TcArgs A = {};
+    A.rowlist = S.perm;
+    A.rowcount = rowcount;
+    A.center = 1;
+    A.sbeta = 1;  // (dropped by launch_mode when the double buffer does not fit)
+    return launch_mode<kTop2>(S, S.Xg_hi, S.Xg_lo, A, max_rows, stat, sms, st);
 }
 
 // Second pass over the ambiguous rows: collect every centroid under the row's
