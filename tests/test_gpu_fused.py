@@ -100,3 +100,37 @@ def test_fused_tiny_pair_buffer():
     r = subprocess.run([sys.executable, "-c", SMALL_QUEUE.format(repo=repo, tests=tests)],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+CENTER_CASE = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
+from oracle import oracle
+import paper_2010_06654_b200 as m
+from paper_2010_06654_b200 import datasets
+from test_gpu_parity import check_trajectory, centroid_ok
+x = datasets.generate({name!r}, {n})
+init = m.make_init(m.RunContext(seed=5), x, {k}, "random")
+ref = oracle.run_lloyd(x, {k}, init, 6)
+for strat in ("lloyd", "hamerly"):
+    res = (m.run_lloyd(x, {k}, init=init, t_max=6, kernel="tc") if strat == "lloyd"
+           else m.run_pruner(x, {k}, strat, init=init, t_max=6, kernel="tc"))
+    check_trajectory(oracle, x, init, res.assign_history, ref["history"], strat)
+    assert centroid_ok(res.centroids, ref["centroids"], x)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("name,n,k,center", [("cfg5", 30000, 600, "1"), ("cfg5", 30000, 600, "0"),
+                                              ("cfg3", 8000, 300, "1"), ("cfg4", 3000, 256, "1")])
+def test_tensor_core_tile_centering(name, n, k, center):
+    """The centered tensor-core pass (label-sorted rows, tiles shifted by a
+    centroid, bias rows from the k x k table) and the plain one, forced on and
+    off by LK_TC_CENTER, both land on the oracle's trajectory."""
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tests = os.path.join(repo, "tests")
+    env = dict(os.environ, LK_TC_CENTER=center)
+    code = CENTER_CASE.format(repo=repo, tests=tests, name=name, n=n, k=k)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
