@@ -130,6 +130,16 @@ enum {
 };
 
 int32_t lk_version(void);
+
+/* k-means++ seeding (init_kmeanspp, core.py:192-217): one D^2 update over n
+ * device rows (x32 fp32 [n, ldx], or x64 fp64 [n, ldx] when non-null),
+ *   d2[i] = first ? s_i : min(d2[i], s_i),  s_i = sum_z (x_iz - c_z)^2
+ * in fp64 with numpy's pairwise association over d -- the same values as the
+ * reference's np.sum((data - data[j]) ** 2, axis=1), so the host-side draws
+ * (rng.choice(n, p=d2 / d2.sum())) are the reference's.  No context needed;
+ * c and d2 are device pointers; stream-ordered. */
+lk_status lk_d2_update(const float *x32, const double *x64, int64_t n, int32_t d, int64_t ldx,
+                       const double *c, double *d2, int32_t first, void *stream);
 /* Last error message of the calling thread ("" if none). */
 const char *lk_last_error(void);
 

@@ -32,7 +32,7 @@ EXPORTED = (
     "lk_version", "lk_last_error", "lk_workspace_bytes", "lk_ctx_create", "lk_ctx_destroy",
     "lk_buffer", "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
     "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_graph_capture", "lk_graph_replay",
-    "lk_launch_count", "lk_profile", "lk_profile_read",
+    "lk_launch_count", "lk_profile", "lk_profile_read", "lk_d2_update",
 )
 
 
@@ -100,10 +100,11 @@ def load():
     L.lk_launch_count.restype = i64
     L.lk_profile.argtypes = [vp, i32]
     L.lk_profile_read.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
+    L.lk_d2_update.argtypes = [vp, vp, i64, i32, i64, vp, vp, i32, vp]
     for name in ("lk_workspace_bytes", "lk_ctx_create", "lk_ctx_destroy", "lk_buffer",
                  "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
                  "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_graph_capture",
-                 "lk_graph_replay", "lk_profile", "lk_profile_read"):
+                 "lk_graph_replay", "lk_profile", "lk_profile_read", "lk_d2_update"):
         getattr(L, name).restype = i32
     _lib = L
     return L

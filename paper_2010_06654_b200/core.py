@@ -136,10 +136,15 @@ def init_kmeanspp(ctx: RunContext, data, k: int) -> np.ndarray:
     unchosen rows when every weight is zero).  Host numpy; the squared
     distances are formed with the same elementwise ops so the probabilities,
     hence the draws, are identical."""
-    x = _host64(as_points(data))
-    n = x.shape[0]
+    pts = as_points(data)
+    n = pts.shape[0]
     if not 1 <= k <= n:
         raise ContractError(f"k={k} out of range for n={n}")
+    if k > 1 and n * pts.shape[1] >= KMEANSPP_DEVICE_MIN:
+        dev = _kmeanspp_device(ctx, pts, k)
+        if dev is not None:
+            return dev
+    x = _host64(pts)
     picks = np.empty(k, dtype=np.int64)
     picks[0] = ctx.rng.integers(n)
     d2 = np.sum((x - x[picks[0]]) ** 2, axis=1)
@@ -151,6 +156,63 @@ def init_kmeanspp(ctx: RunContext, data, k: int) -> np.ndarray:
             picks[j] = ctx.rng.choice(np.setdiff1d(np.arange(n), picks[:j]))
         d2 = np.minimum(d2, np.sum((x - x[picks[j]]) ** 2, axis=1))
     return x[picks].copy()
+
+
+# k-means++ moves its D^2 updates to the GPU from this many elements on
+KMEANSPP_DEVICE_MIN = 1 << 16
+
+
+def _kmeanspp_device(ctx: RunContext, pts, k: int):
+    """init_kmeanspp with the D^2 updates on the GPU (lk_d2_update: fp64,
+    numpy's pairwise order, so d2 is bit-identical to the host expression) and
+    the draws on the host with the same numpy calls on the same d2 array
+    (core.py:205-215 of the reference: d2.sum(), d2 / total, rng.choice), so
+    the picks are the reference's.  None when no CUDA device / library."""
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return None
+        from . import _native as nat
+        lib = nat.load()
+    except Exception:  # noqa: BLE001  (no device or no library: host path)
+        return None
+    import ctypes
+    n, d = pts.shape
+    if isinstance(pts, torch.Tensor):
+        src = pts.detach()
+    else:
+        src = torch.from_numpy(np.ascontiguousarray(pts))
+    xd = src.to("cuda").contiguous()
+    is32 = xd.dtype == torch.float32
+    x64h = _host64(pts)
+    d2d = torch.empty(n, dtype=torch.float64, device="cuda")
+    d2h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    cd = torch.empty(d, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    x32p = ctypes.c_void_p(xd.data_ptr()) if is32 else None
+    x64p = None if is32 else ctypes.c_void_p(xd.data_ptr())
+
+    def update(row: int, first: int):
+        cd.copy_(xd[row])  # device-side widening of the chosen row (exact)
+        nat.check(lib.lk_d2_update(x32p, x64p, n, d, d, ctypes.c_void_p(cd.data_ptr()),
+                                   ctypes.c_void_p(d2d.data_ptr()), first, sh), "lk_d2_update")
+        d2h.copy_(d2d, non_blocking=True)
+        stream.synchronize()
+        return d2h.numpy()
+
+    picks = np.empty(k, dtype=np.int64)
+    picks[0] = ctx.rng.integers(n)
+    d2 = update(int(picks[0]), 1)
+    for j in range(1, k):
+        total = d2.sum()
+        if total > 0.0:
+            picks[j] = ctx.rng.choice(n, p=d2 / total)
+        else:
+            picks[j] = ctx.rng.choice(np.setdiff1d(np.arange(n), picks[:j]))
+        if j < k - 1:
+            d2 = update(int(picks[j]), 0)
+    return x64h[picks].copy()
 
 
 INITS = {"random": init_random, "kmeanspp": init_kmeanspp}

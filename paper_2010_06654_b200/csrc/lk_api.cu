@@ -276,6 +276,24 @@ extern "C" {
 
 int32_t lk_version(void) { return 1; }
 
+lk_status lk_d2_update(const float* x32, const double* x64, int64_t n, int32_t d, int64_t ldx,
+                       const double* c, double* d2, int32_t first, void* stream) {
+    if ((!x32 && !x64) || !c || !d2 || n < 0 || d < 1 || ldx < d) {
+        set_error("lk_d2_update: bad arguments");
+        return LK_ERR_ARG;
+    }
+    std::vector<int32_t> prog;
+    build_pw(0, d, prog);
+    lk::PwProg pp;
+    if (prog.size() > sizeof(pp.ops) / sizeof(pp.ops[0])) {
+        set_error("lk_d2_update: d=%d too large for the pairwise program", d);
+        return LK_ERR_UNSUPPORTED;
+    }
+    pp.len = (int32_t)prog.size();
+    for (size_t i = 0; i < prog.size(); i++) pp.ops[i] = prog[i];
+    return lkh::launch_d2_update(x32, x64, n, d, ldx, c, d2, first, pp, (cudaStream_t)stream);
+}
+
 const char* lk_last_error(void) { return lkh::g_err; }
 
 lk_status lk_workspace_bytes(const lk_config* cfg, uint64_t* bytes) {

@@ -117,6 +117,13 @@ __device__ __forceinline__ float store_ub(const DevState& S, float U, int label)
     return S.lazy ? __fsub_ru(U, S.dcum[label]) : U;
 }
 
+// numpy pairwise-sum association program passed by value (k-means++ D^2
+// updates): (0, start, len) = leaf, (1, 0, 0) = add the two top values.
+struct PwProg {
+    int32_t len;
+    int32_t ops[189];
+};
+
 // Finalize a row's lower bounds from one certified bound on every non-winning
 // centroid (Hamerly: the single slot; Yinyang: every group slot).  Lazy
 // encoding: lb_s[g] = v + Dg[g] and glb_s = v + Dm, rounded down.

@@ -21,6 +21,9 @@ lk_status launch_update(const lk::DevState& S, const double* qscale, const doubl
                         double* sse_part, bool need_half, cudaStream_t st);
 lk_status launch_log_history(const lk::DevState& S, int sms, cudaStream_t st);
 lk_status init_simt_attributes();
+lk_status launch_d2_update(const float* x32, const double* x64, int64_t n, int d, int64_t ldx,
+                           const double* c, double* d2, int first, const lk::PwProg& prog,
+                           cudaStream_t st);
 lk_status init_tc_attributes();
 lk_status init_yy_attributes();
 lk_status launch_scan_exp(const lk::DevState& S, int sms, cudaStream_t st);

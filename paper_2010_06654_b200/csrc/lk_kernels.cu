@@ -848,6 +848,49 @@ lk_status launch_update(const DevState& S, const double* qscale, const double* q
     return LK_OK;
 }
 
+// ---------------------------------------------------------------------------
+// k-means++ seeding (init_kmeanspp, core.py:192-217): one D^2 update
+//   d2[i] = (first ? s_i : min(d2[i], s_i)),  s_i = np.sum((x_i - c) ** 2)
+// in fp64 with numpy's pairwise order over d (the same values the reference's
+// numpy expression produces, so the host's draws are identical).
+
+__global__ void k_d2_update(const float* __restrict__ x32, const double* __restrict__ x64, int64_t n,
+                            int d, int64_t ldx, const double* __restrict__ c, double* __restrict__ d2,
+                            int first, PwProg prog) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double sum;
+        if (prog.len == 3) {
+            sum = x64 ? pw_leaf(x64 + i * ldx, c, 0, d) : pw_leaf(x32 + i * ldx, c, 0, d);
+        } else {
+            double st[24];
+            int sp = 0;
+            for (int p = 0; p < prog.len; p += 3) {
+                if (prog.ops[p] == 0) {
+                    st[sp++] = x64 ? pw_leaf(x64 + i * ldx, c, prog.ops[p + 1], prog.ops[p + 2])
+                                   : pw_leaf(x32 + i * ldx, c, prog.ops[p + 1], prog.ops[p + 2]);
+                } else {
+                    const double b = st[--sp], a = st[--sp];
+                    st[sp++] = __dadd_rn(a, b);
+                }
+            }
+            sum = st[0];
+        }
+        d2[i] = first ? sum : fmin(d2[i], sum);
+    }
+}
+
+lk_status launch_d2_update(const float* x32, const double* x64, int64_t n, int d, int64_t ldx,
+                           const double* c, double* d2, int first, const PwProg& prog,
+                           cudaStream_t st) {
+    if (n <= 0) return LK_OK;
+    const int64_t blocks = (n + kThreads - 1) / kThreads;
+    k_d2_update<<<(unsigned)(blocks < 4096 ? blocks : 4096), kThreads, 0, st>>>(x32, x64, n, d, ldx, c,
+                                                                                d2, first, prog);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
 lk_status launch_log_history(const DevState& S, int sms, cudaStream_t st) {
     if (!S.hlog) return LK_OK;
     k_log_history<<<sms * 2, kThreads, 0, st>>>(S);
