@@ -11,6 +11,7 @@ from .core import ContractError, Counters, RunContext, make_init, sse
 from .engine import BOUND_STRATEGIES, INDEX_MODES, KnobConfig, run_engine
 from .lloyd import IterationStats, RunResult, run_lloyd
 from .pruners import STRATEGIES, run_pruner
+from .runlog import RunLog, read_runlogs, runlog_from_result, write_runlogs
 
 __version__ = "0.1.0"
 
@@ -22,12 +23,16 @@ __all__ = [
     "IterationStats",
     "KnobConfig",
     "RunContext",
+    "RunLog",
     "RunResult",
     "STRATEGIES",
     "make_init",
+    "read_runlogs",
     "run_engine",
     "run_lloyd",
     "run_pruner",
+    "runlog_from_result",
     "sse",
+    "write_runlogs",
     "__version__",
 ]
