@@ -35,7 +35,7 @@ namespace yyf {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxPairs = 1536;  // pair slots of the block queue
+constexpr int kMaxPairs = 512;   // pair slots of the block queue (swept: 512-1536, 512 best on cfg2)
 constexpr int kQRows = 512;      // row slots of the block queue
 // per-centroid filter info (cumulative drift, half-separation, norm, group
 // position) is read through L1 rather than staged: k * 16 B stays L1-resident
