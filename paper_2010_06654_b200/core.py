@@ -83,8 +83,11 @@ def as_points(data):
                 raise ContractError(f"empty data matrix with shape {tuple(data.shape)}")
             if data.dtype not in (torch.float32, torch.float64):
                 data = data.to(torch.float64)
-            if not bool(torch.isfinite(data).all()):
-                raise ContractError("data contains non-finite values")
+            if data.is_cuda:
+                if not bool(torch.isfinite(data).all()):
+                    raise ContractError("data contains non-finite values")
+            # host tensors: checked on the device right after the upload
+            # (DeviceLloyd._bind), before any iteration runs
             return data
     except ImportError:  # pragma: no cover
         pass

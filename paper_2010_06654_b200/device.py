@@ -38,10 +38,24 @@ def _world_size(comm) -> int:
 GROUP_STRATEGIES = ("yinyang", "elkan", "regroup")
 
 
+_GROUP_CACHE: dict = {}
+
+
 def group_centroids(centers: np.ndarray, t: int, seed: int = 0, n_iters: int = 5) -> np.ndarray:
     """Partition k centroids into t groups by a few Lloyd passes over the
     centroids (the idea of bounds.py:175-196; any grouping yields the same
-    labels, it only changes how much the group bounds prune)."""
+    labels, it only changes how much the group bounds prune).  The last
+    result is cached (a pure function of the centroids, t and the seed)."""
+    key = (hash(centers.tobytes()), centers.shape, t, seed, n_iters)
+    hit = _GROUP_CACHE.get("key")
+    if hit == key:
+        return _GROUP_CACHE["groups"].copy()
+    g = _group_centroids(centers, t, seed, n_iters)
+    _GROUP_CACHE.update(key=key, groups=g.copy())
+    return g
+
+
+def _group_centroids(centers: np.ndarray, t: int, seed: int, n_iters: int) -> np.ndarray:
     k = centers.shape[0]
     t = max(1, min(t, k))
     if t == k:
@@ -74,21 +88,55 @@ class IterRecord:
     update_ms: float
 
 
+class DeviceLogChunk:
+    """The moved-row log of iterations t0+1..t1, kept on the device until the
+    history is first read (most callers never read it)."""
+
+    def __init__(self, t0: int, t1: int, offs: np.ndarray, log):
+        self.t0, self.t1, self.offs, self.log = t0, t1, offs, log
+
+    def download(self):
+        torch = _torch()
+        if self.log is None:
+            log = np.empty((0, 2), dtype=np.int32)
+        else:
+            host = torch.empty(tuple(self.log.shape), dtype=torch.int32, pin_memory=True)
+            host.copy_(self.log)
+            log = host.numpy()
+        out = []
+        for t in range(self.t0, self.t1):
+            seg = log[self.offs[t - self.t0]: self.offs[t - self.t0 + 1]]
+            out.append((t, seg[:, 0], seg[:, 1]))
+        self.log = None
+        return out
+
+
 class LabelHistory(Sequence):
     """assign_history (lloyd.py:140) rebuilt lazily from the device's moved-row
     log: iteration 1 sets every row, iteration t applies its (row, label)
     moves to iteration t-1's vector.  Behaves like the reference's list of
     int64 arrays (len, indexing, iteration)."""
 
-    def __init__(self, n: int, parts):
+    def __init__(self, n: int, parts, iters: int | None = None):
         self._n = n
         self._parts = parts
+        self._iters = len(parts) if iters is None else iters
         self._cache = {}
 
     def __len__(self):
-        return len(self._parts)
+        return self._iters
+
+    def _resolve(self):
+        """Device chunks (t0, t1, offsets, device log) -> host (t, rows, labels)
+        parts, downloaded once on first access."""
+        if self._parts and isinstance(self._parts[0], DeviceLogChunk):
+            parts = []
+            for ch in self._parts:
+                parts.extend(ch.download())
+            self._parts = [p for p in parts if p[0] < self._iters]
 
     def _build(self, t: int) -> np.ndarray:
+        self._resolve()
         """Materialize iteration t from the nearest cached vector at or
         before it; keeps the last vector plus a checkpoint every 8 iterations
         (bounded host memory for long runs at large n)."""
@@ -246,6 +294,12 @@ class DeviceLloyd:
                 else:
                     self.x32[:, : self.d].copy_(s32, non_blocking=True)
                 self.h2d_bytes += s32.numel() * 4
+            if isinstance(src, torch.Tensor) and not src.is_cuda:
+                # host tensors are validated here, on the device copy (core.as_points)
+                chk = self.x64 if has_x64 else self.x32[:, : self.d]
+                if not bool(torch.isfinite(chk).all()):
+                    from .core import ContractError as _CE
+                    raise _CE("data contains non-finite values")
             st = self.stream_handle()
             nat.check(self.lib.lk_scan_points(self.ctx, st), "lk_scan_points")
             if self.comm is not None:
@@ -426,7 +480,8 @@ class DeviceLloyd:
             stream.synchronize()
             res["labels"] = lab.numpy()
             if record_history:
-                res["history"] = LabelHistory(self.n, [p for p in log_parts if p[0] < iters])
+                res["history"] = LabelHistory(self.n, [c for c in log_parts if c.t0 < iters],
+                                              iters=iters)
         return res
 
     def _drain_history(self, t0: int, t1: int, parts: list):
@@ -435,16 +490,8 @@ class DeviceLloyd:
         offs = self.hlog_off[t0: t1 + 1].to("cpu").numpy()
         if np.any(offs < 0):
             raise nat.NativeError("label-history log overflow")
-        if offs[-1] > 0:
-            # pinned destination (torch's caching host allocator): a full-rate D2H
-            torch = _torch()
-            host = torch.empty((int(offs[-1]), 2), dtype=torch.int32, pin_memory=True)
-            host.copy_(self.hlog[: offs[-1]], non_blocking=True)
-            torch.cuda.current_stream(self.dev).synchronize()
-            log = host.numpy()
-        else:
-            log = np.empty((0, 2), dtype=np.int32)
-        for t in range(t0, t1):
-            seg = log[offs[t - t0]: offs[t - t0 + 1]]
-            parts.append((t, seg[:, 0], seg[:, 1]))
+        # the segment stays on the device (a copy: the log is rewound and reused)
+        # and is downloaded when the history is first read
+        log = self.hlog[: offs[-1]].clone() if offs[-1] > 0 else None
+        parts.append(DeviceLogChunk(t0, t1, offs, log))
         self.hlog_off[t1].zero_()
