@@ -296,49 +296,55 @@ __global__ void __launch_bounds__(kThreads) k_recheck_fp64(DevState S, int64_t* 
 // exactly as the oracle computes them (numpy order, fp64), ties to the lowest
 // index.  Rows whose set overflowed LK_MAX_CAND go to the fp32
 // difference-form rescan (tight error bound), and from there to fp64 if needed.
+// 16 lanes per ambiguous row (two rows per warp): lane i computes candidate
+// slot i exactly (fp64, numpy's pairwise order), a 16-lane (value, index)
+// top-2 merge picks the winner.
+template <int kL>  // lanes per row; lane i takes candidate slots i, i + kL, ...
 __global__ void __launch_bounds__(kThreads) k_recheck_cand(DevState S, int64_t* stat) {
     if (*S.done) return;
     __shared__ unsigned long long scr[kThreads / 32 + 1];
+    constexpr int kRows = kThreads / kL;
+    const int sub = threadIdx.x & (kL - 1);
     const int64_t m = stat[LK_STAT_CANDIDATE];
-    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < m;
-         base += (int64_t)gridDim.x * kThreads) {
-        const int64_t e = base + threadIdx.x;
-        bool mv = false, over = false;
+    for (int64_t base = (int64_t)blockIdx.x * kRows; base < m; base += (int64_t)gridDim.x * kRows) {
+        const int64_t e = base + threadIdx.x / kL;
+        const bool ok = e < m;
         int64_t row = 0;
-        int old = 0;
-        if (e < m) {
+        int cnt = 0;
+        if (ok) {
             row = S.cand_rows[e];
-            const int cnt = S.cand_cnt[e];
-            if (cnt < 1 || cnt > LK_MAX_CAND) {
-                over = true;
-            } else {
-                double b1 = INFINITY, b2 = INFINITY;
-                int j1 = 0x7fffffff;
-                const int* sl = S.cand_slots + e * LK_MAX_CAND;
-                for (int i = 0; i < cnt; i++) {
-                    const int j = sl[i];
-                    const double* cp = S.C64 + (int64_t)j * S.d;
-                    double dd = S.X64 ? pw_dist2(S.X64 + row * S.d, cp, S.pw_prog, S.pw_len)
-                                      : pw_dist2(S.X32 + row * S.ldx, cp, S.pw_prog, S.pw_len);
-                    dd = __dsqrt_rn(dd);
-                    if (dd < b1 || (dd == b1 && j < j1)) {
-                        b2 = b1;
-                        b1 = dd;
-                        j1 = j;
-                    } else {
-                        b2 = fmin(b2, dd);
-                    }
-                }
-                old = S.labels[row];
-                mv = old != j1;
-                S.labels[row] = j1;
-                if (S.strategy != LK_STRAT_LLOYD) {
-                    S.ub[row] = store_ub(S, __double2float_ru(b1 * (1.0 + 1e-12)), j1);
-                    const float l2 = isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12));
-                    write_lb_all(S, row, fminf(l2, S.cand_lb[e]));
-                }
+            cnt = S.cand_cnt[e];
+        }
+        const bool over_row = ok && (cnt < 1 || cnt > LK_MAX_CAND);
+        double b1 = INFINITY, b2 = INFINITY;
+        int j1 = 0x7fffffff;
+        if (ok && !over_row) {
+            for (int i = sub; i < cnt; i += kL) {
+                const int j = S.cand_slots[e * LK_MAX_CAND + i];
+                const double* cp = S.C64 + (int64_t)j * S.d;
+                const double dd = __dsqrt_rn(S.X64 ? pw_dist2(S.X64 + row * S.d, cp, S.pw_prog, S.pw_len)
+                                                   : pw_dist2(S.X32 + row * S.ldx, cp, S.pw_prog, S.pw_len));
+                merge_top2(b1, j1, b2, dd, j, INFINITY);
             }
         }
+#pragma unroll
+        for (int o = kL / 2; o > 0; o >>= 1)
+            merge_top2(b1, j1, b2, __shfl_xor_sync(LK_FULL_MASK, b1, o, kL),
+                       __shfl_xor_sync(LK_FULL_MASK, j1, o, kL), __shfl_xor_sync(LK_FULL_MASK, b2, o, kL));
+        const bool lead = ok && sub == 0;
+        bool mv = false;
+        int old = 0;
+        if (lead && !over_row) {
+            old = S.labels[row];
+            mv = old != j1;
+            S.labels[row] = j1;
+            if (S.strategy != LK_STRAT_LLOYD) {
+                S.ub[row] = store_ub(S, __double2float_ru(b1 * (1.0 + 1e-12)), j1);
+                const float l2 = isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12));
+                write_lb_all(S, row, fminf(l2, S.cand_lb[e]));
+            }
+        }
+        const bool over = lead && over_row;
         int64_t pos = block_append(mv, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
         if (mv) S.moved[pos] = make_int2((int)row, old);
         int64_t fpos = block_append(over, (unsigned long long*)(stat + LK_STAT_OVERFLOW), scr);
@@ -801,8 +807,13 @@ lk_status launch_recheck(const DevState& S, int64_t* stat, int64_t max_rows, int
 
 lk_status launch_recheck_cand(const DevState& S, int64_t* stat, int64_t max_rows, int sms,
                               cudaStream_t st) {
-    int grid = grid_for(max_rows, kThreads, sms * 4);
-    k_recheck_cand<<<grid, kThreads, 0, st>>>(S, stat);
+    // long rows: one candidate per lane (cfg4: 0.39 -> 0.19 ms); short rows
+    // (few candidates, cheap distances): one thread per row is fastest
+    if (S.d > 64) {
+        k_recheck_cand<LK_MAX_CAND><<<grid_for(max_rows, kThreads / LK_MAX_CAND, sms * 8), kThreads, 0, st>>>(S, stat);
+    } else {
+        k_recheck_cand<1><<<grid_for(max_rows, kThreads, sms * 4), kThreads, 0, st>>>(S, stat);
+    }
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
