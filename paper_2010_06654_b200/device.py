@@ -434,7 +434,7 @@ class DeviceLloyd:
                               "lk_step_update")
                 e2.record(stream)
                 chg[t - 1].copy_(self.stats[t - 1, nat.STAT["changed_global"]], non_blocking=True)
-                if t % check_every == 0 or t == T or t == 1:
+                if t % check_every == 0 or t == T:  # (t=1 cannot converge: n rows move)
                     stream.synchronize()
                     z = np.nonzero(chg[checked:t].numpy() == 0)[0]
                     t_end = checked + int(z[0]) + 1 if len(z) else t
