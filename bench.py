@@ -236,7 +236,7 @@ def run_ours(args):
     strategy = args.strategy
     gpu_strat = strategy
     from paper_2010_06654_b200.pruners import gpu_groups
-    n_groups = args.groups or gpu_groups(gpu_strat, n, k)
+    n_groups = args.groups or gpu_groups(gpu_strat, n, k, d)
     eng = DeviceLloyd(x, k, gpu_strat, T, kernel=args.kernel, comm=group, n_total=n,
                       groups=n_groups, group_seed=cfg.seed_init, record_history=False)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")

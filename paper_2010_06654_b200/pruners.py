@@ -36,12 +36,16 @@ GPU_STRATEGY = {
 STRATEGIES = dict(GPU_STRATEGY)
 
 
-def gpu_groups(strategy: str, n: int, k: int) -> int:
+def gpu_groups(strategy: str, n: int, k: int, d: int = 0) -> int:
     """Group count t for the group-bound strategies.  The reference uses
     t = ceil(k/10) (pruners.py:395); the GPU caps it so the n*t bound table
     stays a small fraction of an iteration's HBM traffic.  Elkan keeps one
-    bound per centroid while n*k is small."""
+    bound per centroid while n*k is small; for d <= 32 it runs on the fused
+    group-bound kernel with the finest grouping it supports (32 groups, or one
+    centroid per group when k <= 32) -- every grouping returns Lloyd's labels."""
     if strategy == "elkan":
+        if 0 < d <= 32:
+            return min(k, 32)
         return k if n * k <= (1 << 26) else min(k, 64)
     if strategy == "yinyang":
         # ~64 centroids per group (the reference's k/10 would make the n*t
@@ -67,5 +71,5 @@ def run_pruner(data, k: int, strategy: str, *, init=None, init_method: str = "km
         return res
     gs = GPU_STRATEGY[strategy]
     return run_device(x, k, centers, gs, t_max, ctx, label=strategy, kernel=kernel,
-                      record_history=record_history, groups=gpu_groups(gs, x.shape[0], k),
+                      record_history=record_history, groups=gpu_groups(gs, x.shape[0], k, x.shape[1]),
                       group_seed=ctx.seed)
