@@ -189,6 +189,25 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// Paired fp32 arithmetic (FADD2 / FFMA2 on sm_100a): two epilogue columns per
+// instruction, each lane still rounded as its scalar counterpart.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+// (cc - 2 (vh + vx)) for two columns: exactly fmaf(-2, vh + vx, cc) per lane
+__device__ __forceinline__ void dp2(float vh0, float vh1, float vx0, float vx1, float c0, float c1,
+                                    float& d0, float& d1) {
+    unsigned long long s, r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s) : "l"(pk2(vh0, vh1)), "l"(pk2(vx0, vx1)));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(s), "l"(pk2(-2.0f, -2.0f)), "l"(pk2(c0, c1)));
+    upk2(r, d0, d1);
+}
+
 // ---- certification (D-space error bound) ------------------------------------
 
 // |D_true - D~| <= kappa * |x| |c| + 8u (|x|^2 + |c|^2) for the 3xTF32 form;
@@ -525,12 +544,20 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                             cv = __ldg(cp + c4);
                         }
                         const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
+                        float dpv[4];
+#pragma unroll
+                        for (int e = 0; e < 4; e += 2) {
+                            const int col = c4 * 4 + e;
+                            const float vh0 = __uint_as_float(col < 32 ? r0[col & 31] : r1[col & 31]);
+                            const float vh1 = __uint_as_float(col < 32 ? r0[(col + 1) & 31] : r1[(col + 1) & 31]);
+                            const float vx0 = __uint_as_float(col < 32 ? x0[col & 31] : x1[col & 31]);
+                            const float vx1 = __uint_as_float(col < 32 ? x0[(col + 1) & 31] : x1[(col + 1) & 31]);
+                            dp2(vh0, vh1, vx0, vx1, cc[e], cc[e + 1], dpv[e], dpv[e + 1]);
+                        }
 #pragma unroll
                         for (int e = 0; e < 4; e++) {
                             const int col = c4 * 4 + e;
-                            const float vh = __uint_as_float(col < 32 ? r0[col & 31] : r1[col & 31]);
-                            const float vx = __uint_as_float(col < 32 ? x0[col & 31] : x1[col & 31]);
-                            const float dp = fmaf(-2.0f, vh + vx, cc[e]);
+                            const float dp = dpv[e];
                             if (dp < cb1[e]) { cb2[e] = cb1[e]; cb1[e] = dp; cj1[e] = jb + col; }
                             else cb2[e] = fminf(cb2[e], dp);
                         }
