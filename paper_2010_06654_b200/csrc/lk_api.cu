@@ -681,20 +681,15 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             // tensor-core runs: every row failing the bounds is rescanned in full
             const bool full_only = use_tc;
             if (lkh::yy_fused_ok(S)) {
-                // one kernel: filter, group scans, certified merge, refinement
-                // deltas (lk_yy_fused.cu); then the fp64 recheck of the rows it
-                // left ambiguous, which refines the rows it moves itself
+                // one kernel: filter, group scans, certified merge, the fp64
+                // recheck of the rows the merge leaves ambiguous, refinement
+                // deltas (lk_yy_fused.cu)
                 {
                     ProfScope p(c, 1, st);
                     s = lkh::launch_yy_fused(S, stat, buf<double>(c, B_QSCALE), c->sms, st);
                     if (s != LK_OK) return s;
                 }
-                {
-                    ProfScope p(c, 2, st);
-                    s = lkh::launch_recheck(S, stat, n, c->sms, st, buf<double>(c, B_QSCALE));
-                    if (s != LK_OK) return s;
-                }
-                c->launches += 2;
+                c->launches += 1;
                 if (S.hlog) {
                     ProfScope p(c, 3, st);
                     s = lkh::launch_log_history(S, c->sms, st);

@@ -232,51 +232,6 @@ __global__ void __launch_bounds__(kThreads) k_assign_gen(DevState S, const int32
 // ---------------------------------------------------------------------------
 // K1x: exact fp64 recheck, numpy pairwise order (one block per flagged row)
 
-// One flagged row, the whole block: x staged in shared memory (xr: >= d
-// doubles), every thread takes k/256 centroids, lexicographic top-2 merge.
-// Block-uniform call.
-__device__ __forceinline__ void recheck_row_block(const DevState& S, int64_t* stat,
-                                                  const double* qscale_inline, int64_t row,
-                                                  double* xr) {
-    __shared__ double rb1[kThreads / 32], rb2[kThreads / 32];
-    __shared__ int rj1[kThreads / 32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();
-    for (int z = threadIdx.x; z < S.d; z += kThreads)
-        xr[z] = S.X64 ? S.X64[row * S.d + z] : (double)S.X32[row * S.ldx + z];
-    __syncthreads();
-    double b1 = INFINITY, b2 = INFINITY;
-    int j1 = 0x7fffffff;
-    for (int j = threadIdx.x; j < S.k; j += kThreads) {
-        double dd = __dsqrt_rn(pw_dist2(xr, S.C64 + (int64_t)j * S.d, S.pw_prog, S.pw_len));
-        if (dd < b1) { b2 = b1; b1 = dd; j1 = j; }
-        else b2 = fmin(b2, dd);
-    }
-    // lexicographic (value, index) top-2 merge: warp, then block
-    for (int o = 16; o > 0; o >>= 1)
-        merge_top2(b1, j1, b2, __shfl_xor_sync(LK_FULL_MASK, b1, o),
-                   __shfl_xor_sync(LK_FULL_MASK, j1, o), __shfl_xor_sync(LK_FULL_MASK, b2, o));
-    if (lane == 0) { rb1[warp] = b1; rj1[warp] = j1; rb2[warp] = b2; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < kThreads / 32; w++) merge_top2(b1, j1, b2, rb1[w], rj1[w], rb2[w]);
-        const int old = S.labels[row];
-        S.labels[row] = j1;
-        if (S.strategy != LK_STRAT_LLOYD) {
-            S.ub[row] = store_ub(S, __double2float_ru(b1 * (1.0 + 1e-12)), j1);
-            write_lb_all(S, row, isinf(b2) ? INFINITY : __double2float_rd(b2 * (1.0 - 1e-12)));
-        }
-        if (old != j1) {
-            unsigned long long p = atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), 1ull);
-            S.moved[p] = make_int2((int)row, old);
-            if (qscale_inline) {
-                refine_move(S, qscale_inline, row, old, j1);
-                atomicAdd((unsigned long long*)(S.delta + (int64_t)S.k * S.d + 2 * S.k), 1ull);
-            }
-        }
-    }
-}
-
 // qscale_inline != nullptr: the assignment kernel already refined its own
 // moved rows (lk_yy_fused.cu), so the rows moved here add their fixed-point
 // deltas and changed count directly.
@@ -286,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_recheck_fp64(DevState S, int64_t* 
     extern __shared__ double xr[];  // [d]
     const int64_t m = stat[LK_STAT_FLAGGED];
     for (int64_t f = blockIdx.x; f < m; f += gridDim.x)
-        recheck_row_block(S, stat, qscale_inline, S.flagged[f], xr);
+        recheck_row_block<kThreads>(S, stat, qscale_inline, S.flagged[f], xr);
 }
 
 // K1c: exact fp64 re-decision of the tensor-core pass's ambiguous rows over

@@ -18,8 +18,8 @@
 //     scan   2^lg lanes per pair, fp32 difference-form top-2 over the group
 //     merge  one thread per queued row: certified label, ub, rewritten group
 //            bounds; a moved row adds its fixed-point refinement deltas
-//            ambiguous rows go to the fp64 recheck kernel (k_recheck_fp64,
-//            which refines the rows it moves itself)
+//            ambiguous rows are re-decided in place by the exact fp64
+//            recheck (recheck_row_block, which refines the rows it moves)
 //
 // Only the labels, the bound table, the refinement deltas and the moved-row
 // log touch HBM; the pair list and the scan results never leave the SM.
@@ -270,12 +270,14 @@ __device__ __forceinline__ void drain(const DevState& S, int64_t* stat, const do
     }
     __syncthreads();
 
-    // ---- ambiguous rows go to the exact fp64 recheck kernel (which also adds
-    // the refinement deltas of the rows it moves)
+    // ---- ambiguous rows (a few per iteration) are re-decided here by the exact
+    // fp64 recheck (numpy order over all k, the whole block per row), which
+    // also adds the refinement deltas of the rows it moves: no recheck launch
     const int nfl = *sh.nflag;
-    for (int f = threadIdx.x; f < nfl; f += kThreads) {
-        const unsigned long long p = atomicAdd((unsigned long long*)(stat + LK_STAT_FLAGGED), 1ull);
-        S.flagged[p] = Q.row[Q.flag[f]];
+    if (nfl > 0) {
+        __shared__ double xr[32];
+        if (threadIdx.x == 0) atomicAdd((unsigned long long*)(stat + LK_STAT_FLAGGED), (unsigned long long)nfl);
+        for (int f = 0; f < nfl; f++) recheck_row_block<kThreads>(S, stat, qscale, Q.row[Q.flag[f]], xr);
     }
 }
 
