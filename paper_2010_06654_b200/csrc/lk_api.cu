@@ -40,7 +40,7 @@ enum InternalBuf {
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
-    B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_COUNT_
+    B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB, B_COUNT_
 };
 
 struct Layout {
@@ -148,6 +148,9 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_TILE_LAB] = (uint64_t)(n / 128 + 2) * 4;
         L->size[B_ROWR] = (uint64_t)n * 8;
         L->size[B_ROWXO] = (uint64_t)n * 4;
+        L->size[B_ROWBV] = (uint64_t)n * 4;
+        L->size[B_ROWXN2] = (uint64_t)n * 4;
+        L->size[B_ROWLAB] = (uint64_t)n * 4;
 
     }
     if (is_group_strategy(c.strategy)) {
@@ -399,6 +402,9 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.tile_lab = buf<int32_t>(c, B_TILE_LAB);
     S.rowR = buf<double>(c, B_ROWR);
     S.rowxo = buf<float>(c, B_ROWXO);
+    S.rowbv = buf<float>(c, B_ROWBV);
+    S.rowxn2 = buf<float>(c, B_ROWXN2);
+    S.rowlab = buf<int32_t>(c, B_ROWLAB);
     S.kpad = (int32_t)((cfg->k + 255) / 256 * 256);
     {
         const char* e = getenv("LK_TC_CENTER");  // A/B knob for the tile centering

@@ -82,6 +82,9 @@ struct DevState {
     int32_t* tile_lab;      // [n / 128 + 1] label whose centroid a tile is centered on (-1: none)
     double* rowR;           // [n] ||x'||^2 + 2 x'.o of each gathered row (x' = x - o)
     float* rowxo;           // [n] ||x'|| rounded up
+    float* rowbv;           // [n] search threshold of a gathered row (k_assign_tc2; +inf: none)
+    float* rowxn2;          // [n] ||x||^2 of each gathered row (contiguous copy for the certification)
+    int32_t* rowlab;        // [n] label of each gathered row before the pass
     // Yinyang group bounds
     int32_t* gperm;         // [k] centroid ids sorted by group
     int32_t* ginv;          // [k] position of centroid j in gperm

@@ -1001,7 +1001,7 @@ __device__ __forceinline__ void tc_certify(const DevState& S, const TcArgs& A, f
                                            float b1, float b2, int j1, int64_t& row, bool& moved,
                                            int& old, bool& amb, float& thr_out, float& lb_out) {
     row = A.rowlist ? (int64_t)A.rowlist[r] : r;
-    const float xn2 = S.xn2[row];
+    const float xn2 = A.center ? S.rowxn2[r] : S.xn2[row];
     const float xn = sqrtf(xn2) * (1.0f + 2 * kU32);
     const float cmax = S.scal[0];
     const float cn1 = j1 >= 0 ? S.cnorm[j1] : cmax;  // (unknown column: max |c|)
@@ -1017,9 +1017,9 @@ __device__ __forceinline__ void tc_certify(const DevState& S, const TcArgs& A, f
         const double U = (R + b1 + e1 + ex) * (1.0 + 1e-12) + 1e-300;
         const double L2 = isinf(b2) ? INFINITY : (R + b2 - eo - ex) - fabs(R) * 1e-12;
         if (L2 > U && j1 >= 0) {
-            old = S.labels[row];
+            old = S.rowlab[r];
             moved = old != j1;
-            S.labels[row] = j1;
+            if (moved) S.labels[row] = j1;
             if (S.strategy != LK_STRAT_LLOYD) {
                 S.ub[row] = store_ub(S, __double2float_ru(sqrt(fmax(U, 0.0)) * (1.0 + 1e-12)), j1);
                 write_lb_all(S, row, isinf(L2) ? INFINITY : __double2float_rd(sqrt(fmax(L2, 0.0)) * (1.0 - 1e-12)));
@@ -1221,24 +1221,21 @@ __global__ void __launch_bounds__(320, 1)
         __shared__ unsigned long long escr[9];
         int acc = 0;
         uint32_t acc_phase = 0;
+        // search thresholds (rowbv, written by k_gather_center) one pair ahead
+        auto load_bv = [&](int it_) -> float {
+            if (!A.center || it_ >= n_it) return INFINITY;
+            const int64_t r_ = (2 * (blockIdx.x + (int64_t)it_ * gridDim.x) + s) * BM + q * 32 + lane;
+            return r_ < m ? __ldcs(S.rowbv + r_) : INFINITY;
+        };
+        float bv_next = load_bv(0);
         for (int it = 0; it < n_it; it++) {
             const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
             const int64_t rt = 2 * rp + s;
             const int64_t r = rt * BM + q * 32 + lane;
             const bool valid = r < m;
-            const int at = (A.center && rt < n_rt) ? S.tile_lab[rt] : -1;
-            float b1 = INFINITY, b2 = INFINITY, bv = INFINITY;
+            float b1 = INFINITY, b2 = INFINITY, bv = bv_next;
             int bj = -1;
-            if (A.center && valid && at >= 0 && r < (int64_t)S.lcur[at]) {
-                // upper bound on the TC value of the row's own label column
-                const double R = S.rowR[r], xo = (double)S.rowxo[r];
-                const double ca = (double)S.cnorm[at];
-                const double est = xo * xo - R;
-                const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
-                const double ea = (double)kappa * xo * ca + gb * (fabs(est) + 2.0 * xo * ca) +
-                                  2.0 * 5.9604644775390625e-08 * fabs(est);
-                bv = __double2float_ru(est + 2.0 * ea + 1e-30);
-            }
+            bv_next = load_bv(it + 1);
             mbar_wait(bfull, it & 1);
             const uint32_t sb0 = smem_u32(sbeta + s * S.kpad);
             for (int ct = 0; ct < A.n_ct; ct++) {
@@ -1495,8 +1492,9 @@ __global__ void __launch_bounds__(256) k_gather_center(DevState S, const int64_t
         const bool ok = p < m;
         double x2 = 0.0, xo = 0.0;
         int a = -1;
+        int64_t row = 0;
         if (ok) {
-            const int64_t row = S.perm[p];
+            row = S.perm[p];
             a = S.labels[S.perm[p & ~(int64_t)127]];
             const float4* xp = reinterpret_cast<const float4*>(S.X32 + row * S.ldx);
             const float4* op = reinterpret_cast<const float4*>(S.C32 + (int64_t)(a >= 0 ? a : 0) * S.ldc);
@@ -1524,9 +1522,27 @@ __global__ void __launch_bounds__(256) k_gather_center(DevState S, const int64_t
             xo += __shfl_xor_sync(LK_FULL_MASK, xo, o);
         }
         if (ok && sub == 0) {
-            S.rowR[p] = x2 + 2.0 * xo;
-            S.rowxo[p] = __double2float_ru(sqrt(x2) * (1.0 + 1e-12));
+            const double R = x2 + 2.0 * xo;
+            const float xof = __double2float_ru(sqrt(x2) * (1.0 + 1e-12));
+            S.rowR[p] = R;
+            S.rowxo[p] = xof;
             if ((p & 127) == 0) S.tile_lab[p >> 7] = a;
+            // contiguous copies for k_assign_tc2's certification, and its search
+            // threshold: an upper bound on the TC value of the row's own label
+            // column (rows of the tile's label: D'_a = ||x'||^2 - R up to the dot error)
+            const int lab = S.labels[row];
+            S.rowlab[p] = lab;
+            S.rowxn2[p] = S.xn2[row];
+            float bv = INFINITY;
+            if (a >= 0 && lab == a) {
+                const double xd = (double)xof, ca = (double)S.cnorm[a];
+                const double est = xd * xd - R;
+                const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
+                const double ea = (double)tc_kappa_ordered(S.d) * xd * ca + gb * (fabs(est) + 2.0 * xd * ca) +
+                                  2.0 * 5.9604644775390625e-08 * fabs(est);
+                bv = __double2float_ru(est + 2.0 * ea + 1e-30);
+            }
+            S.rowbv[p] = bv;
         }
     }
 }
