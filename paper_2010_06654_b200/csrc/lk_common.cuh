@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/lloydkit_b200.h"
 
@@ -243,6 +244,39 @@ void set_error(const char* fmt, ...);
             return LK_ERR_CUDA;                                                      \
         }                                                                            \
     } while (0)
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may be
+// scheduled while its predecessor in the stream drains; pdl_wait() blocks until
+// the predecessor has completed and its writes are visible (a no-op for a plain
+// launch).  pdl_trigger() lets the successor be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+namespace lk {
+inline bool pdl_enabled() {
+    static const int v = [] {
+        const char* e = getenv("LK_PDL");  // A/B knob (measured neutral on cfg1 / cfg2: off)
+        return e ? atoi(e) : 0;
+    }();
+    return v != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+}  // namespace lk
 
 #define LK_LAUNCH_CHECK()                                                            \
     do {                                                                             \

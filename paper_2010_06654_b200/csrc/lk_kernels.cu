@@ -556,6 +556,8 @@ __device__ __forceinline__ void update_centroid_warp(const DevState& S, int j, c
 __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const double* qscale,
                                                                const double* qinv,
                                                                double* sse_part) {
+    pdl_wait();
+    pdl_trigger();
     if (*S.done) return;
     const int warp = threadIdx.x >> 5;
     const int j = blockIdx.x * (kThreads / 32) + warp;
@@ -643,6 +645,8 @@ __device__ __forceinline__ void half_sep_tile(const DevState& S, int tj, int tjp
 }
 
 __global__ void __launch_bounds__(kThreads) k_half_sep(DevState S) {
+    pdl_wait();
+    pdl_trigger();
     if (*S.done) return;
     half_sep_tile(S, blockIdx.y, blockIdx.x);
 }
@@ -667,6 +671,8 @@ __device__ __forceinline__ void log_history_grid(const DevState& S) {
 }
 
 __global__ void k_log_history(DevState S) {
+    pdl_wait();
+    pdl_trigger();
     if (*S.done) return;
     log_history_grid(S);
 }
@@ -804,11 +810,11 @@ lk_status launch_refine(const DevState& S, int64_t* stat, const double* qscale, 
 lk_status launch_update(const DevState& S, const double* qscale, const double* qinv,
                         double* sse_part, bool need_half, cudaStream_t st) {
     int grid = (S.k + (kThreads / 32) - 1) / (kThreads / 32);
-    k_update_centroids<<<grid, kThreads, 0, st>>>(S, qscale, qinv, sse_part);
+    LK_CUDA_CHECK(lk::launch_pdl(k_update_centroids, dim3(grid), dim3(kThreads), 0, st, S, qscale, qinv, sse_part));
     LK_LAUNCH_CHECK();
     if (need_half) {
         dim3 g((S.k + kHsT - 1) / kHsT, (S.k + kHsT - 1) / kHsT);
-        k_half_sep<<<g, kThreads, 0, st>>>(S);
+        LK_CUDA_CHECK(lk::launch_pdl(k_half_sep, g, dim3(kThreads), 0, st, S));
         LK_LAUNCH_CHECK();
     }
     return LK_OK;
@@ -859,7 +865,7 @@ lk_status launch_d2_update(const float* x32, const double* x64, int64_t n, int d
 
 lk_status launch_log_history(const DevState& S, int sms, cudaStream_t st) {
     if (!S.hlog) return LK_OK;
-    k_log_history<<<sms * 2, kThreads, 0, st>>>(S);
+    LK_CUDA_CHECK(lk::launch_pdl(k_log_history, dim3(sms * 2), dim3(kThreads), 0, st, S));
     LK_LAUNCH_CHECK();
     return LK_OK;
 }

@@ -601,18 +601,8 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
             // A row whose minimum was never searched is left ambiguous.
             float bv = INFINITY;
             int bj = -1;
-            if (SPLIT && MODE == kTop2 && A.center && A.fast && valid) {
-                const int at = S.tile_lab[rt];
-                if (at >= 0 && r < (int64_t)S.lcur[at]) {  // lcur[a] = end of label a's rows
-                    const double R = S.rowR[r], xo = (double)S.rowxo[r];
-                    const double ca = (double)S.cnorm[at];
-                    const double est = xo * xo - R;
-                    const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
-                    const double ea = (double)kappa * xo * ca + gb * (fabs(est) + 2.0 * xo * ca) +
-                                      2.0 * 5.9604644775390625e-08 * fabs(est);
-                    bv = __double2float_ru(est + 2.0 * ea + 1e-30);
-                }
-            }
+            // (rowbv: written by k_gather_center for rows of their tile's label)
+            if (SPLIT && MODE == kTop2 && A.center && A.fast && valid) bv = __ldcs(S.rowbv + r);
             // MODE_TOP2: running top-2 of D' = |c|^2 - 2 x.c (ties keep the lower index)
             // MODE_COLLECT: every j with D' <= thr goes into the row's candidate slots
             float b1 = INFINITY, b2 = INFINITY;
@@ -886,7 +876,7 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
             float thr_out = 0.f, lb_out = 0.f;
             if (valid) {
                 row = A.rowlist ? (int64_t)A.rowlist[r] : r;
-                const float xn2 = S.xn2[row];
+                const float xn2 = A.center ? S.rowxn2[r] : S.xn2[row];  // (contiguous copy when gathered)
                 const float xn = sqrtf(xn2) * (1.0f + 2 * kU32);
                 const float cn1 = j1 >= 0 ? S.cnorm[j1] : S.scal[0];  // (unknown column: max |c|)
                 const float cmax = S.scal[0];
@@ -910,9 +900,9 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                     const double U = (R + b1 + e1 + ex) * (1.0 + 1e-12) + 1e-300;
                     const double L2 = isinf(b2) ? INFINITY : (R + b2 - eo - ex) - fabs(R) * 1e-12;
                     if (L2 > U && j1 >= 0) {
-                        old = S.labels[row];
+                        old = S.rowlab[r];
                         moved = old != j1;
-                        S.labels[row] = j1;
+                        if (moved) S.labels[row] = j1;
                         if (S.strategy != LK_STRAT_LLOYD) {
                             S.ub[row] = store_ub(S, __double2float_ru(sqrt(fmax(U, 0.0)) * (1.0 + 1e-12)), j1);
                             write_lb_all(S, row, isinf(L2) ? INFINITY
@@ -1384,24 +1374,26 @@ __global__ void k_gather_rows(DevState S, const int32_t* rows, const int64_t* co
 // so the contraction runs on x' (small) against the unshifted centroids (the
 // B operand stays shared by every tile) and the error scales with |x'| |c|.
 
-constexpr int kPtT = 64;
-
 // ptab[a][j] = sum_z (c_a,z - c_j,z)^2 in fp32 difference form (fmaf chain in
-// dimension order), +inf for padding columns j >= k.  64 x 64 tiles.
+// dimension order), +inf for padding columns j >= k.  T x T tiles, 16 x 16
+// threads, (T/16)^2 pairs per thread: T = 64 for many centroids, T = 16 when
+// the 64-tiles would not fill the SMs (few centroids, long rows: cfg4).
+template <int T>
 __global__ void __launch_bounds__(256) k_pair_table(DevState S) {
     if (*S.done) return;
-    __shared__ float ta[32][kPtT + 1];
-    __shared__ float tb[32][kPtT + 1];
-    const int a0 = blockIdx.y * kPtT, j0 = blockIdx.x * kPtT;
+    constexpr int P = T / 16;
+    __shared__ float ta[32][T + 1];
+    __shared__ float tb[32][T + 1];
+    const int a0 = blockIdx.y * T, j0 = blockIdx.x * T;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    float acc[4][4];
+    float acc[P][P];
 #pragma unroll
-    for (int u = 0; u < 4; u++)
+    for (int u = 0; u < P; u++)
 #pragma unroll
-        for (int v = 0; v < 4; v++) acc[u][v] = 0.f;
+        for (int v = 0; v < P; v++) acc[u][v] = 0.f;
     for (int z0 = 0; z0 < S.d; z0 += 32) {
         __syncthreads();
-        for (int e = threadIdx.x; e < kPtT * 32; e += 256) {
+        for (int e = threadIdx.x; e < T * 32; e += 256) {
             const int r = e / 32, z = e % 32, zz = z0 + z;
             ta[z][r] = (a0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(a0 + r) * S.ldc + zz] : 0.f;
             tb[z][r] = (j0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(j0 + r) * S.ldc + zz] : 0.f;
@@ -1410,20 +1402,20 @@ __global__ void __launch_bounds__(256) k_pair_table(DevState S) {
         const int zn = min(32, S.d - z0);
         for (int z = 0; z < zn; z++) {
 #pragma unroll
-            for (int u = 0; u < 4; u++)
+            for (int u = 0; u < P; u++)
 #pragma unroll
-                for (int v = 0; v < 4; v++) {
+                for (int v = 0; v < P; v++) {
                     const float t = ta[z][ty + 16 * u] - tb[z][tx + 16 * v];
                     acc[u][v] = fmaf(t, t, acc[u][v]);
                 }
         }
     }
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < P; u++) {
         const int a = a0 + ty + 16 * u;
         if (a >= S.k) continue;
 #pragma unroll
-        for (int v = 0; v < 4; v++) {
+        for (int v = 0; v < P; v++) {
             const int j = j0 + tx + 16 * v;
             if (j < S.kpad) S.ptab[(int64_t)a * S.kpad + j] = j < S.k ? acc[u][v] : INFINITY;
         }
@@ -1472,7 +1464,12 @@ __global__ void k_label_scatter(DevState S, const int32_t* rowlist, const int64_
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int row = rowlist ? rowlist[p] : (int)p;
-        S.perm[atomicAdd(S.lcur + S.labels[row], 1)] = row;
+        const int lab = S.labels[row];
+        const int pos = atomicAdd(S.lcur + lab, 1);
+        S.perm[pos] = row;
+        // per sorted position: the row's label, and each tile's (first row's) label
+        S.rowlab[pos] = lab;
+        if ((pos & 127) == 0) S.tile_lab[pos >> 7] = lab;
     }
 }
 
@@ -1487,22 +1484,41 @@ __global__ void __launch_bounds__(256) k_gather_center(DevState S, const int64_t
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int c4n = S.ldx / 4;
+    const float kap = tc_kappa_ordered(S.d);
+    // software pipeline: the next group's row id and labels (written by
+    // k_label_scatter per sorted position) load while this group is processed
+    int row_n = 0, lab_n = -1, a_n = -1;
+    {
+        const int64_t p = warp * rpw + lane / L;
+        if (p < m) {
+            row_n = S.perm[p];
+            lab_n = S.rowlab[p];
+            a_n = S.tile_lab[p >> 7];
+        }
+    }
     for (int64_t p0 = warp * rpw; p0 < m; p0 += nwarps * rpw) {
         const int64_t p = p0 + lane / L;
         const bool ok = p < m;
-        double x2 = 0.0, xo = 0.0;
-        int a = -1;
-        int64_t row = 0;
+        const int64_t row = row_n;
+        const int lab = lab_n, a = a_n;
+        {
+            const int64_t pn = p + nwarps * rpw;
+            if (pn < m) {
+                row_n = S.perm[pn];
+                lab_n = S.rowlab[pn];
+                a_n = S.tile_lab[pn >> 7];
+            }
+        }
+        double x2 = 0.0, xo = 0.0, xx = 0.0;
         if (ok) {
-            row = S.perm[p];
-            a = S.labels[S.perm[p & ~(int64_t)127]];
             const float4* xp = reinterpret_cast<const float4*>(S.X32 + row * S.ldx);
             const float4* op = reinterpret_cast<const float4*>(S.C32 + (int64_t)(a >= 0 ? a : 0) * S.ldc);
             float4* hp = reinterpret_cast<float4*>(S.Xg_hi + p * S.ldx);
             float4* lp = reinterpret_cast<float4*>(S.Xg_lo + p * S.ldx);
             for (int c = sub; c < c4n; c += L) {
-                const float4 x = xp[c];
+                const float4 x = __ldcs(xp + c);
                 const float4 o = a >= 0 ? __ldg(op + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float xv[4] = {x.x, x.y, x.z, x.w};
                 const float xs[4] = {x.x - o.x, x.y - o.y, x.z - o.z, x.w - o.w};
                 const float ov[4] = {o.x, o.y, o.z, o.w};
                 float h[4], l[4];
@@ -1512,33 +1528,34 @@ __global__ void __launch_bounds__(256) k_gather_center(DevState S, const int64_t
                     l[e] = xs[e] - h[e];
                     x2 = fma((double)xs[e], (double)xs[e], x2);
                     xo = fma((double)xs[e], (double)ov[e], xo);
+                    xx = fma((double)xv[e], (double)xv[e], xx);
                 }
-                hp[c] = make_float4(h[0], h[1], h[2], h[3]);
-                lp[c] = make_float4(l[0], l[1], l[2], l[3]);
+                __stcs(hp + c, make_float4(h[0], h[1], h[2], h[3]));
+                __stcs(lp + c, make_float4(l[0], l[1], l[2], l[3]));
             }
         }
         for (int o = L >> 1; o > 0; o >>= 1) {
             x2 += __shfl_xor_sync(LK_FULL_MASK, x2, o);
             xo += __shfl_xor_sync(LK_FULL_MASK, xo, o);
+            xx += __shfl_xor_sync(LK_FULL_MASK, xx, o);
         }
         if (ok && sub == 0) {
             const double R = x2 + 2.0 * xo;
             const float xof = __double2float_ru(sqrt(x2) * (1.0 + 1e-12));
             S.rowR[p] = R;
             S.rowxo[p] = xof;
-            if ((p & 127) == 0) S.tile_lab[p >> 7] = a;
-            // contiguous copies for k_assign_tc2's certification, and its search
-            // threshold: an upper bound on the TC value of the row's own label
-            // column (rows of the tile's label: D'_a = ||x'||^2 - R up to the dot error)
-            const int lab = S.labels[row];
-            S.rowlab[p] = lab;
-            S.rowxn2[p] = S.xn2[row];
+            // contiguous |x|^2 for k_assign_tc2's certification (fp64 sum rounded
+            // once: within the 2^-22 the bound allows of k_split_points' value;
+            // exact fp64 input keeps that value), and its search threshold: an
+            // upper bound on the TC value of the row's own label column (rows of
+            // the tile's label: D'_a = ||x'||^2 - R up to the dot error)
+            S.rowxn2[p] = S.X64 ? S.xn2[row] : (float)xx;
             float bv = INFINITY;
             if (a >= 0 && lab == a) {
                 const double xd = (double)xof, ca = (double)S.cnorm[a];
                 const double est = xd * xd - R;
                 const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
-                const double ea = (double)tc_kappa_ordered(S.d) * xd * ca + gb * (fabs(est) + 2.0 * xd * ca) +
+                const double ea = (double)kap * xd * ca + gb * (fabs(est) + 2.0 * xd * ca) +
                                   2.0 * 5.9604644775390625e-08 * fabs(est);
                 bv = __double2float_ru(est + 2.0 * ea + 1e-30);
             }
@@ -1780,8 +1797,14 @@ lk_status launch_assign_tc(const DevState& S, const int32_t* rowlist, const int6
 
 lk_status launch_pair_table(const DevState& S, cudaStream_t st) {
     if (!S.center) return LK_OK;
-    const dim3 g((unsigned)(S.kpad / kPtT), (unsigned)((S.k + kPtT - 1) / kPtT));
-    k_pair_table<<<g, 256, 0, st>>>(S);
+    const int64_t tiles64 = (int64_t)(S.kpad / 64) * ((S.k + 63) / 64);
+    if (tiles64 >= 148) {
+        const dim3 g((unsigned)(S.kpad / 64), (unsigned)((S.k + 63) / 64));
+        k_pair_table<64><<<g, 256, 0, st>>>(S);
+    } else {
+        const dim3 g((unsigned)(S.kpad / 16), (unsigned)((S.k + 15) / 16));
+        k_pair_table<16><<<g, 256, 0, st>>>(S);
+    }
     LK_LAUNCH_CHECK();
     return LK_OK;
 }

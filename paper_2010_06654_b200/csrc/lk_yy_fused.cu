@@ -285,6 +285,8 @@ template <int DP, int T, bool STAGED>
 __global__ void __launch_bounds__(kThreads, (DP <= 4 ? 3 : 2)) k_yy_fused(DevState S, int64_t* stat,
                                                       const double* qscale, int pcap,
                                                       int lg_parts) {
+    pdl_wait();
+    pdl_trigger();  // the update may be scheduled while this kernel drains
     if (*S.done) return;
     // dynamic: staged centroids (group order) + per-centroid info | pair list
     // | sorted order | scan results
@@ -558,7 +560,7 @@ static lk_status launch_fused_t(const lk::DevState& S, int64_t* stat, const doub
     int64_t blocks = (S.n + kThreads - 1) / kThreads;
     if (blocks > (int64_t)sms * occ) blocks = (int64_t)sms * occ;
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, kThreads, smem, st>>>(S, stat, qscale, pcap, lg);
+    LK_CUDA_CHECK(lk::launch_pdl(kern, dim3((unsigned)blocks), dim3(kThreads), smem, st, S, stat, qscale, pcap, lg));
     LK_LAUNCH_CHECK();
     return LK_OK;
 }

@@ -134,3 +134,21 @@ def test_tensor_core_tile_centering(name, n, k, center):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("env_set", [{"LK_TC2": "0"}, {"LK_TC2": "0", "LK_TC_CL": "2"},
+                                     {"LK_TC2": "0", "LK_TC_CL": "4"}, {"LK_TC_FAST": "0", "LK_TC2": "0"},
+                                     {"LK_TC_SPLIT": "0"}])
+def test_tensor_core_d32_variants(env_set):
+    """The d <= 32 tensor-core variants behind the A/B knobs -- the single-row-
+    tile kernel (LK_TC2=0), its 2- and 4-CTA multicast clusters (LK_TC_CL), the
+    per-column top-2 epilogue (LK_TC_FAST=0), one unordered accumulator
+    (LK_TC_SPLIT=0) -- all land on the oracle's trajectory (an odd number of row
+    tiles and k not a multiple of 128 exercise the dummy tiles and padding)."""
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tests = os.path.join(repo, "tests")
+    env = dict(os.environ, **env_set)
+    code = CENTER_CASE.format(repo=repo, tests=tests, name="cfg5", n=20000, k=600)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
