@@ -284,6 +284,128 @@ __global__ void __launch_bounds__(kThreads) k_seed_yinyang(DevState S, int64_t* 
     }
 }
 
+// d <= 2 seed (cfg2's first iteration, 1e9 pairs): centroids staged as
+// negated pairs (-a0, -b0, -a1, -b1) so one LDS.128 feeds two distances in
+// paired fp32 (FADD2 / FMUL2 / FFMA2: each lane rounded exactly as dist2_dp's
+// fmaf chain), per-group minima by FMNMX3; the exact top-2 with its index runs
+// only over the winning group.  Same values, bounds and labels as
+// k_seed_yinyang<2>.
+__device__ __forceinline__ unsigned long long f2pk(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2upk(unsigned long long v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ float fmin3s(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+__global__ void __launch_bounds__(kThreads) k_seed_yinyang_d2(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    extern __shared__ __align__(16) float4 cpair[];  // [pairs]; then int pair offsets [T + 1]
+    __shared__ unsigned long long scr[kThreads / 32 + 1];
+    const int T = S.t_groups, ldc = S.ldc;
+    int* poff = reinterpret_cast<int*>(cpair + (S.k + T));
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int g = 0; g < T; g++) {
+            poff[g] = acc;
+            acc += (S.goff[g + 1] - S.goff[g] + 1) >> 1;
+        }
+        poff[T] = acc;
+    }
+    __syncthreads();
+    for (int g = 0; g < T; g++) {
+        const int j0 = S.goff[g], j9 = S.goff[g + 1];
+        const int np = (j9 - j0 + 1) >> 1;
+        for (int q = threadIdx.x; q < np; q += kThreads) {
+            const int ja = j0 + 2 * q, jb = min(ja + 1, j9 - 1);  // odd group: the last member twice
+            const float* ca = S.Cg + (int64_t)ja * ldc;
+            const float* cb = S.Cg + (int64_t)jb * ldc;
+            const float a1 = S.d > 1 ? ca[1] : 0.f, b1 = S.d > 1 ? cb[1] : 0.f;
+            cpair[poff[g] + q] = make_float4(-ca[0], -cb[0], -a1, -b1);
+        }
+    }
+    __syncthreads();
+    const float rho = simt_rel_err(S.d);
+    const float cmax = S.scal[0];
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < S.n; base += (int64_t)gridDim.x * kThreads) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < S.n;
+        float xr[2];
+        const float* xp = S.X32 + i * S.ldx;
+        float xn2 = 0.f;
+#pragma unroll
+        for (int z = 0; z < 2; z++) {
+            xr[z] = (valid && z < S.d) ? __ldg(xp + z) : 0.f;
+            xn2 = fmaf(xr[z], xr[z], xn2);
+        }
+        const float xn = sqrtf(xn2);
+        const unsigned long long xx = f2pk(xr[0], xr[0]), xy = f2pk(xr[1], xr[1]);
+        float bestD = INFINITY, secD = INFINITY;
+        int bestG = 0;
+        for (int g = 0; g < T; g++) {
+            const int p0 = poff[g], p9 = poff[g + 1];
+            float m = INFINITY;
+#pragma unroll 4
+            for (int q = p0; q < p9; q++) {
+                const float4 c = cpair[q];
+                unsigned long long t, u, dd;
+                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(xx), "l"(f2pk(c.x, c.y)));
+                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(u) : "l"(xy), "l"(f2pk(c.z, c.w)));
+                asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(dd) : "l"(t));
+                asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(dd) : "l"(u), "l"(dd));
+                float d0, d1;
+                f2upk(dd, d0, d1);
+                m = fmin3s(m, d0, d1);
+            }
+            if (valid)
+                S.lb[lb_index(S, i, g)] = p9 > p0 ? fmaxf((sqrtf(m) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f)
+                                                  : INFINITY;
+            if (m < bestD) {
+                secD = fminf(secD, bestD);
+                bestD = m;
+                bestG = g;
+            } else {
+                secD = fminf(secD, m);
+            }
+        }
+        // the winning group exactly (first minimum in group order, second best)
+        float b1 = INFINITY, b2 = INFINITY;
+        int bestP = S.goff[bestG];
+        for (int jj = S.goff[bestG]; jj < S.goff[bestG + 1]; jj++) {
+            const float acc = dist2_dp<2>(xr, S.Cg + (int64_t)jj * ldc, S.d);
+            if (acc < b1) { b2 = b1; b1 = acc; bestP = jj; }
+            else b2 = fminf(b2, acc);
+        }
+        secD = fminf(secD, b2);
+        const int j1 = S.gperm[bestP];
+        const float U1 = (sqrtf(bestD) + kU32 * (xn + S.cnorm[j1])) * (1.0f + rho);
+        const float L2 = isinf(secD) ? INFINITY : (sqrtf(secD) - kU32 * (xn + cmax)) * (1.0f - rho);
+        const bool certain = valid && L2 > U1;
+        const bool flag = valid && !certain;
+        bool moved = false;
+        int old = 0;
+        if (certain) {
+            old = S.labels[i];
+            moved = old != j1;
+            S.labels[i] = j1;
+            S.ub[i] = U1;  // iteration 1: the cumulative drifts of the lazy encoding are 0
+            S.lb[lb_index(S, i, bestG)] =
+                isinf(b2) ? INFINITY : fmaxf((sqrtf(b2) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f);
+            if (S.glb) S.glb[i] = fmaxf(L2, 0.f);
+        }
+        int64_t pos = block_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED), scr);
+        if (moved) S.moved[pos] = make_int2((int)i, old);
+        int64_t fpos = block_append(flag, (unsigned long long*)(stat + LK_STAT_FLAGGED), scr);
+        if (flag) S.flagged[fpos] = (int)i;
+    }
+}
+
 __device__ __forceinline__ float dist2_ptr(const float* xp, const float* cp, int d, bool vec4) {
     float acc = 0.f;
     int z = 0;
@@ -509,6 +631,13 @@ static void launch_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStrea
 
 lk_status launch_yy_seed(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     const int d = S.d;
+    // (pairs <= (k + t) / 1 float4 + t + 1 offsets)
+    const size_t d2smem = (size_t)(S.k + S.t_groups) * 16 + (size_t)(S.t_groups + 1) * 4;
+    if (d <= 2 && d2smem <= 48 * 1024) {
+        k_seed_yinyang_d2<<<grid_for_rows(S.n, sms, 6), kThreads, d2smem, st>>>(S, stat);
+        LK_LAUNCH_CHECK();
+        return LK_OK;
+    }
     if (d <= 2) launch_seed<2>(S, stat, sms, st);
     else if (d <= 4) launch_seed<4>(S, stat, sms, st);
     else if (d <= 8) launch_seed<8>(S, stat, sms, st);
