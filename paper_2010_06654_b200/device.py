@@ -174,7 +174,7 @@ class DeviceLloyd:
     def __init__(self, data, k: int, strategy: str = "lloyd", t_max: int = 10, *,
                  device=None, kernel: str = "auto", groups: int = 0, comm=None,
                  n_total: int | None = None, group_seed: int = 0,
-                 record_history: bool = True, history_iters: int = 8):
+                 record_history: bool = True, history_iters: int = 0):
         torch = _torch()
         if not torch.cuda.is_available():
             raise nat.NativeError("no CUDA device: the B200 path has no CPU fallback")
@@ -212,8 +212,13 @@ class DeviceLloyd:
         self.n_total = int(n_total)
 
         # the history log holds the moves of history_iters iterations between
-        # drains; every iteration moves at most n rows
-        self.history_cap = self.n * history_iters if record_history and self.n else 0
+        # drains (every iteration moves at most n rows); by default all t_max
+        # iterations within a 4 GB log, so a run needs no mid-run host sync
+        if history_iters <= 0:
+            per_iter = max(1, self.n) * 8
+            history_iters = max(8, min(max(1, self.t_max), (4 << 30) // per_iter))
+        self.history_iters = int(history_iters)
+        self.history_cap = self.n * self.history_iters if record_history and self.n else 0
         cfg = nat.LkConfig(n_local=self.n, n_total=self.n_total, d=self.d, k=self.k,
                            strategy=nat.STRAT_IDS[strategy], groups=int(groups),
                            t_max=max(1, self.t_max), kernel=nat.KERNEL_IDS[kernel],
@@ -386,7 +391,7 @@ class DeviceLloyd:
                 raise ContractError("rebind: fp64 input not fp32-exact on an fp32 context")
         self._bind(src, has_x64)
 
-    def run(self, init, *, record_history: bool = True, check_every: int = 8,
+    def run(self, init, *, record_history: bool = True, check_every: int = 0,
             use_graphs: bool = True):
         """Run up to t_max iterations from ``init``; stop after the first with
         changed == 0 (lloyd.py:169-171).  Returns a dict of host arrays.
@@ -398,6 +403,8 @@ class DeviceLloyd:
         torch = _torch()
         self.set_centroids(init)
         T = self.t_max
+        if check_every <= 0:
+            check_every = self.history_iters  # the log drains at its capacity
         res = {"iterations": 0, "converged": False, "history": [], "records": []}
         if T <= 0:
             res["centroids"] = np.array(init, dtype=np.float64, copy=True)
@@ -447,9 +454,19 @@ class DeviceLloyd:
                         converged = True
                         break
                     checked = t
+            # one sync for every result: stats, SSE, centroids, int64 labels
+            # (widened on the device) into pinned buffers
+            h_stats = torch.empty(tuple(self.stats[:iters].shape), dtype=self.stats.dtype, pin_memory=True)
+            h_sse = torch.empty(tuple(self.sse_buf[:iters].shape), dtype=self.sse_buf.dtype, pin_memory=True)
+            h_c64 = torch.empty(tuple(self.c64.shape), dtype=self.c64.dtype, pin_memory=True)
+            lab = torch.empty(self.n, dtype=torch.int64, pin_memory=True)
+            h_stats.copy_(self.stats[:iters], non_blocking=True)
+            h_sse.copy_(self.sse_buf[:iters], non_blocking=True)
+            h_c64.copy_(self.c64, non_blocking=True)
+            lab.copy_(self.labels, non_blocking=True)
             stream.synchronize()
-            stats = self.stats[:iters].to("cpu").numpy().copy()
-            sse = self.sse_buf[:iters].to("cpu").numpy().copy()
+            stats = h_stats.numpy().copy()
+            sse = h_sse.numpy().copy()
             if self.comm is not None:
                 import torch.distributed as dist
                 st_t = torch.as_tensor(stats, device=self.dev)
@@ -473,12 +490,8 @@ class DeviceLloyd:
             res["iterations"] = iters
             res["converged"] = converged
             res["records"] = recs
-            res["centroids"] = self.c64.to("cpu").numpy().copy()
-            # int64 labels (lloyd.py:52) widened on the device, one pinned D2H
-            lab = torch.empty(self.n, dtype=torch.int64, pin_memory=True)
-            lab.copy_(self.labels, non_blocking=True)
-            stream.synchronize()
-            res["labels"] = lab.numpy()
+            res["centroids"] = h_c64.numpy().copy()
+            res["labels"] = lab.numpy()  # int64 labels (lloyd.py:52)
             if record_history:
                 res["history"] = LabelHistory(self.n, [c for c in log_parts if c.t0 < iters],
                                               iters=iters)
