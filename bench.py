@@ -407,8 +407,8 @@ def run_ours(args):
                "d2h_bytes_per_step": int((8 * n + k * d * 8 + 8 * its * (16 + 1)) / its),
                "iterations": its, "wall_s": wall, "calls": 3, "statistic": "median",
                "includes": "validation, H2D of the points from pinned memory (cached device "
-                           "context), centroid grouping, iterations (CUDA-graph replay) with the "
-                           "changed count read back every 8 iterations, per-iteration counters, "
+                           "context), centroid grouping, iterations (CUDA-graph replay; one host sync "
+                           "at the end, the device stops itself at convergence), per-iteration counters, "
                            "final int64 labels and centroids D2H; the label history stays on "
                            "the device until read (lazy RunResult.assign_history)"}
 
