@@ -424,10 +424,11 @@ __global__ void __launch_bounds__(kThreads) k_refine_moved(DevState S, int64_t* 
 // max ||c||, top-2 drift, group drifts, done flag.
 __device__ __forceinline__ void update_global_block(const DevState& S, const double* sse_part) {
     const int t = *S.iter;
-    __shared__ double ssum[kThreads];
-    __shared__ float smax[kThreads], sd1[kThreads], sd2[kThreads];
-    __shared__ int sarg[kThreads];
-    const int tid = threadIdx.x;
+    __shared__ double ssum[kThreads / 32];
+    __shared__ float smax[kThreads / 32], sd1[kThreads / 32], sd2[kThreads / 32];
+    __shared__ int sarg[kThreads / 32];
+    __shared__ float sg[1024];  // group drift maxima (t <= 1024)
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     double acc = 0.0;
     float cm = 0.f, d1 = -1.f, d2 = -1.f;
     int a1 = -1;
@@ -438,29 +439,40 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
         if (dj > d1) { d2 = d1; d1 = dj; a1 = j; }
         else d2 = fmaxf(d2, dj);
     }
-    ssum[tid] = acc; smax[tid] = cm; sd1[tid] = d1; sd2[tid] = d2; sarg[tid] = a1;
-    __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if (tid < s) {
-            ssum[tid] += ssum[tid + s];
-            smax[tid] = fmaxf(smax[tid], smax[tid + s]);
-            float od1 = sd1[tid + s], od2 = sd2[tid + s];
-            int oa = sarg[tid + s];
-            if (od1 > sd1[tid] || (od1 == sd1[tid] && oa >= 0 && (sarg[tid] < 0 || oa < sarg[tid]))) {
-                sd2[tid] = fmaxf(sd1[tid], od2);
-                sd1[tid] = od1;
-                sarg[tid] = oa;
-            } else {
-                sd2[tid] = fmaxf(sd2[tid], od1);
-            }
+    // fixed-order reductions: xor butterflies in each warp, then the warps in order
+    auto merge_d = [](float& x1, float& x2, int& xa, float o1, float o2, int oa) {
+        if (o1 > x1 || (o1 == x1 && oa >= 0 && (xa < 0 || oa < xa))) {
+            x2 = fmaxf(x1, o2);
+            x1 = o1;
+            xa = oa;
+        } else {
+            x2 = fmaxf(x2, o1);
         }
-        __syncthreads();
+    };
+    for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(LK_FULL_MASK, acc, o);
+        cm = fmaxf(cm, __shfl_xor_sync(LK_FULL_MASK, cm, o));
+        const float o1 = __shfl_xor_sync(LK_FULL_MASK, d1, o), o2 = __shfl_xor_sync(LK_FULL_MASK, d2, o);
+        const int oa = __shfl_xor_sync(LK_FULL_MASK, a1, o);
+        merge_d(d1, d2, a1, o1, o2, oa);
     }
+    if (lane == 0) { ssum[wid] = acc; smax[wid] = cm; sd1[wid] = d1; sd2[wid] = d2; sarg[wid] = a1; }
+    for (int g = tid; g < S.t_groups && g < 1024; g += blockDim.x) sg[g] = 0.f;
+    __syncthreads();
     if (tid == 0) {
-        S.scal[0] = smax[0];
-        S.scal[1] = fmaxf(sd1[0], 0.f);
-        S.scal[2] = fmaxf(sd2[0], 0.f);
-        S.scal[3] = __int_as_float(sarg[0]);
+        double ss = ssum[0];
+        float mx = smax[0], x1 = sd1[0], x2 = sd2[0];
+        int xa = sarg[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) {
+            ss += ssum[w];
+            mx = fmaxf(mx, smax[w]);
+            merge_d(x1, x2, xa, sd1[w], sd2[w], sarg[w]);
+        }
+        ssum[0] = ss;
+        S.scal[0] = mx;
+        S.scal[1] = fmaxf(x1, 0.f);
+        S.scal[2] = fmaxf(x2, 0.f);
+        S.scal[3] = __int_as_float(xa);
         const int64_t changed = __ldcg(S.delta + (int64_t)S.k * S.d + 2 * S.k);
         S.delta[(int64_t)S.k * S.d + 2 * S.k] = 0;
         S.cur[LK_STAT_CHANGED_GLOBAL] = changed;
@@ -475,12 +487,20 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
     // s_half is rebuilt by k_half_sep's atomicMin: start from +inf
     // (gate off: s = 0 never prunes)
     for (int j = tid; j < S.k; j += blockDim.x) S.s_half[j] = S.sgate ? INFINITY : 0.f;
-    // group drifts (Yinyang): max drift over each group's members
+    // group drifts (Yinyang): max drift over each group's members (shared-memory
+    // maxima when the groups fit, global atomics otherwise)
     if (S.gdrift) {
-        __syncthreads();
-        for (int g = tid; g < S.t_groups; g += blockDim.x) S.gdrift[g] = 0.f;
-        __syncthreads();
-        for (int j = tid; j < S.k; j += blockDim.x) atomic_max_pos(S.gdrift + S.group_of[j], __ldcg(S.drift + j));
+        if (S.t_groups <= 1024) {
+            for (int j = tid; j < S.k; j += blockDim.x)
+                atomicMax(reinterpret_cast<int*>(sg + S.group_of[j]), __float_as_int(__ldcg(S.drift + j)));
+            __syncthreads();
+            for (int g = tid; g < S.t_groups; g += blockDim.x) S.gdrift[g] = sg[g];
+        } else {
+            __syncthreads();
+            for (int g = tid; g < S.t_groups; g += blockDim.x) S.gdrift[g] = 0.f;
+            __syncthreads();
+            for (int j = tid; j < S.k; j += blockDim.x) atomic_max_pos(S.gdrift + S.group_of[j], __ldcg(S.drift + j));
+        }
         if (S.lazy) {
             // cumulative group and global drifts of the lazy bound encoding
             __syncthreads();
@@ -597,16 +617,17 @@ __device__ __forceinline__ void half_sep_tile(const DevState& S, int tj, int tjp
 #pragma unroll
         for (int b = 0; b < 4; b++) acc[a][b] = 0.f;
     for (int z0 = 0; z0 < S.d; z0 += kHsDC) {
+        const int zn = min(kHsDC, S.d - z0);  // (short rows: only the real dimensions)
         __syncthreads();
-        for (int e = threadIdx.x; e < kHsT * kHsDC; e += kThreads) {
-            int r = e / kHsDC, z = e % kHsDC;
+        for (int e = threadIdx.x; e < kHsT * zn; e += kThreads) {
+            int r = e / zn, z = e % zn;
             int zz = z0 + z;
-            ta[z][r] = (j0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(j0 + r) * S.ldc + zz] : 0.f;
-            tb[z][r] = (jp0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(jp0 + r) * S.ldc + zz] : 0.f;
+            ta[z][r] = (j0 + r < S.k) ? S.C32[(int64_t)(j0 + r) * S.ldc + zz] : 0.f;
+            tb[z][r] = (jp0 + r < S.k) ? S.C32[(int64_t)(jp0 + r) * S.ldc + zz] : 0.f;
         }
         __syncthreads();
 #pragma unroll 8
-        for (int z = 0; z < kHsDC; z++) {
+        for (int z = 0; z < zn; z++) {
             float av[4], bv[4];
 #pragma unroll
             for (int a = 0; a < 4; a++) av[a] = ta[z][ty + 16 * a];
