@@ -361,11 +361,92 @@ __global__ void __launch_bounds__(kThreads) k_filter_hamerly(DevState S, int64_t
 
 
 // G lanes per moved row (G = power of two >= min(d, 32)); warp-uniform loop.
+// d in 17..32 (one lane per dimension): a warp takes 8 consecutive moved rows.
+// The moved list of a centered tensor-core pass is in label-sorted order, so
+// consecutive rows mostly leave the same cluster: the old-label side is summed
+// in registers along a run of equal old labels and added once per run (integer
+// sums: the result is the same in any order); the new side per row.
+__device__ __forceinline__ void refine_batch32(const DevState& S, const double* qscale, int64_t e0,
+                                               int64_t m) {
+    constexpr int B = 8;
+    const int lane = threadIdx.x & 31;
+    int64_t* dS = S.delta;
+    int64_t* dN = S.delta + (int64_t)S.k * S.d;
+    int64_t* dQ = dN + S.k;
+    int row[B], old[B], nw[B];
+    double v[B];
+#pragma unroll
+    for (int b = 0; b < B; b++) {
+        row[b] = -1;
+        old[b] = -1;
+        if (e0 + b < m) {
+            const int2 mv = S.moved[e0 + b];
+            row[b] = mv.x;
+            old[b] = mv.y;
+        }
+    }
+    const double sc = lane < S.d ? qscale[lane] : 0.0;
+#pragma unroll
+    for (int b = 0; b < B; b++) {
+        nw[b] = row[b] >= 0 ? S.labels[row[b]] : 0;
+        v[b] = (row[b] >= 0 && lane < S.d) ? load_x(S, row[b], lane) : 0.0;
+    }
+    const double scq = qscale[S.d];
+    long long run_q = 0, run_qq = 0;
+    int run_old = -1, run_n = 0;
+#pragma unroll
+    for (int b = 0; b < B; b++) {
+        if (row[b] < 0) continue;  // (warp-uniform)
+        const long long q = lane < S.d ? __double2ll_rn(v[b] * sc) : 0;
+        double x2 = v[b] * v[b];
+        // ||x||^2 as k_refine_moved<32> forms it: lane z holds x_z^2 (one term per
+        // lane), then the fixed xor tree
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(LK_FULL_MASK, x2, o);
+        const long long qq = __double2ll_rn(x2 * scq);
+        if (q) atomicAdd((unsigned long long*)(dS + (int64_t)nw[b] * S.d + lane), (unsigned long long)q);
+        if (lane == 0) {
+            atomicAdd((unsigned long long*)(dN + nw[b]), 1ull);
+            atomicAdd((unsigned long long*)(dQ + nw[b]), (unsigned long long)qq);
+        }
+        if (old[b] != run_old) {
+            if (run_old >= 0) {
+                if (run_q) atomicAdd((unsigned long long*)(dS + (int64_t)run_old * S.d + lane), (unsigned long long)(-run_q));
+                if (lane == 0) {
+                    atomicAdd((unsigned long long*)(dN + run_old), (unsigned long long)(-(long long)run_n));
+                    atomicAdd((unsigned long long*)(dQ + run_old), (unsigned long long)(-run_qq));
+                }
+            }
+            run_old = old[b];
+            run_q = 0;
+            run_qq = 0;
+            run_n = 0;
+        }
+        run_q += q;
+        run_qq += qq;
+        run_n++;
+    }
+    if (run_old >= 0) {
+        if (run_q) atomicAdd((unsigned long long*)(dS + (int64_t)run_old * S.d + lane), (unsigned long long)(-run_q));
+        if (lane == 0) {
+            atomicAdd((unsigned long long*)(dN + run_old), (unsigned long long)(-(long long)run_n));
+            atomicAdd((unsigned long long*)(dQ + run_old), (unsigned long long)(-run_qq));
+        }
+    }
+}
+
 template <int G>
 __global__ void __launch_bounds__(kThreads) k_refine_moved(DevState S, int64_t* stat,
                                                            const double* qscale) {
     if (*S.done) return;
     const int64_t m = stat[LK_STAT_CHANGED];
+    if (G == 32 && S.d > 16 && S.d <= 32) {
+        const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+        const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
+        for (int64_t e0 = gw * 8; e0 < m; e0 += nwarps * 8) refine_batch32(S, qscale, e0, m);
+        if (blockIdx.x == 0 && threadIdx.x == 0) S.delta[(int64_t)S.k * S.d + 2 * S.k] = m;
+        return;
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sub = lane % G;
     constexpr int kGroupsPerWarp = 32 / G;
