@@ -350,19 +350,30 @@ __global__ void __launch_bounds__(kThreads) k_seed_yinyang_d2(DevState S, int64_
         int bestG = 0;
         for (int g = 0; g < T; g++) {
             const int p0 = poff[g], p9 = poff[g + 1];
-            float m = INFINITY;
-#pragma unroll 4
-            for (int q = p0; q < p9; q++) {
-                const float4 c = cpair[q];
+            auto pair_d = [&](const float4 c, float& d0, float& d1) {
                 unsigned long long t, u, dd;
                 asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(xx), "l"(f2pk(c.x, c.y)));
                 asm("add.rn.f32x2 %0, %1, %2;" : "=l"(u) : "l"(xy), "l"(f2pk(c.z, c.w)));
                 asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(dd) : "l"(t));
                 asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(dd) : "l"(u), "l"(dd));
-                float d0, d1;
                 f2upk(dd, d0, d1);
+            };
+            // two independent minimum chains (ILP), merged at the end
+            float m = INFINITY, m2 = INFINITY;
+            int q = p0;
+            for (; q + 1 < p9; q += 2) {
+                float d0, d1, d2, d3;
+                pair_d(cpair[q], d0, d1);
+                pair_d(cpair[q + 1], d2, d3);
+                m = fmin3s(m, d0, d1);
+                m2 = fmin3s(m2, d2, d3);
+            }
+            if (q < p9) {
+                float d0, d1;
+                pair_d(cpair[q], d0, d1);
                 m = fmin3s(m, d0, d1);
             }
+            m = fminf(m, m2);
             if (valid)
                 S.lb[lb_index(S, i, g)] = p9 > p0 ? fmaxf((sqrtf(m) - kU32 * (xn + cmax)) * (1.0f - rho), 0.f)
                                                   : INFINITY;
@@ -374,11 +385,18 @@ __global__ void __launch_bounds__(kThreads) k_seed_yinyang_d2(DevState S, int64_
                 secD = fminf(secD, m);
             }
         }
-        // the winning group exactly (first minimum in group order, second best)
+        // the winning group exactly (first minimum in group order, second best),
+        // from the staged pairs: x + (-c) is x - c, the same fmaf chain as dist2_dp
         float b1 = INFINITY, b2 = INFINITY;
-        int bestP = S.goff[bestG];
-        for (int jj = S.goff[bestG]; jj < S.goff[bestG + 1]; jj++) {
-            const float acc = dist2_dp<2>(xr, S.Cg + (int64_t)jj * ldc, S.d);
+        const int g0 = S.goff[bestG], g9 = S.goff[bestG + 1];
+        int bestP = g0;
+        for (int jj = g0; jj < g9; jj++) {
+            const float4 c = cpair[poff[bestG] + ((jj - g0) >> 1)];
+            const bool hi = (jj - g0) & 1;
+            const float t0 = xr[0] + (hi ? c.y : c.x);
+            const float t1 = xr[1] + (hi ? c.w : c.z);
+            float acc = fmaf(t0, t0, 0.f);
+            if (S.d > 1) acc = fmaf(t1, t1, acc);
             if (acc < b1) { b2 = b1; b1 = acc; bestP = jj; }
             else b2 = fminf(b2, acc);
         }
