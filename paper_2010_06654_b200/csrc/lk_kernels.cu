@@ -307,6 +307,94 @@ __global__ void __launch_bounds__(kThreads) k_recheck_cand(DevState S, int64_t* 
     }
 }
 
+// K2 on the tensor-core path (d >= 32: no tighten, the rescan decides): a pure
+// streaming pass.  Four rows per thread (int4 / float4 loads and stores), one
+// block-level scan and one global atomic per 1024 rows for the rescan list,
+// the active count accumulated locally.  20 B per row + 4 B per listed row.
+__global__ void __launch_bounds__(kThreads) k_filter_hamerly_tc(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    __shared__ int wsum[kThreads / 32 + 1];
+    __shared__ unsigned long long sbase;
+    const float dmax1 = S.scal[1], dmax2 = S.scal[2];
+    const int amax = __float_as_int(S.scal[3]);
+    const int64_t n = S.n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t n_active = 0;
+    for (int64_t base = (int64_t)blockIdx.x * kThreads * 4; base < n;
+         base += (int64_t)gridDim.x * kThreads * 4) {
+        const int64_t i0 = base + 4 * (int64_t)threadIdx.x;
+        int a[4];
+        float ub[4], lb[4];
+        bool need[4];
+        const bool full4 = i0 + 3 < n;
+        if (full4) {
+            const int4 a4 = __ldcs(reinterpret_cast<const int4*>(S.labels + i0));
+            const float4 u4 = __ldcs(reinterpret_cast<const float4*>(S.ub + i0));
+            const float4 l4 = __ldcs(reinterpret_cast<const float4*>(S.lb + i0));
+            a[0] = a4.x; a[1] = a4.y; a[2] = a4.z; a[3] = a4.w;
+            ub[0] = u4.x; ub[1] = u4.y; ub[2] = u4.z; ub[3] = u4.w;
+            lb[0] = l4.x; lb[1] = l4.y; lb[2] = l4.z; lb[3] = l4.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const bool ok = i0 + e < n;
+                a[e] = ok ? S.labels[i0 + e] : 0;
+                ub[e] = ok ? S.ub[i0 + e] : 0.f;
+                lb[e] = ok ? S.lb[i0 + e] : 0.f;
+            }
+        }
+        int cnt = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const bool ok = i0 + e < n;
+            const float u = __fadd_ru(ub[e], __ldg(S.drift + a[e]));
+            const float l = fmaxf(__fsub_rd(lb[e], a[e] == amax ? dmax2 : dmax1), 0.f);
+            const float gate = fmaxf(l, __ldg(S.s_half + a[e]));
+            need[e] = ok && !(gate > u);
+            cnt += need[e];
+            ub[e] = u;
+            lb[e] = l;
+        }
+        if (full4) {
+            __stcs(reinterpret_cast<float4*>(S.ub + i0), make_float4(ub[0], ub[1], ub[2], ub[3]));
+            __stcs(reinterpret_cast<float4*>(S.lb + i0), make_float4(lb[0], lb[1], lb[2], lb[3]));
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; e++)
+                if (i0 + e < n) {
+                    S.ub[i0 + e] = ub[e];
+                    S.lb[i0 + e] = lb[e];
+                }
+        }
+        n_active += cnt;
+        // block exclusive scan of the counts, one atomic for the block's slots
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(LK_FULL_MASK, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < kThreads / 32; w++) {
+                const int c = wsum[w];
+                wsum[w] = tot;
+                tot += c;
+            }
+            sbase = tot ? atomicAdd((unsigned long long*)(stat + LK_STAT_WORK), (unsigned long long)tot) : 0ull;
+        }
+        __syncthreads();
+        int64_t pos = (int64_t)sbase + wsum[warp] + incl - cnt;
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if (need[e]) S.work[pos++] = (int)(i0 + e);
+        __syncthreads();  // wsum / sbase reusable
+    }
+    warp_add(n_active, stat + LK_STAT_ACTIVE);
+}
+
 // ---------------------------------------------------------------------------
 // K2: Hamerly bound decay + gate + tighten + compaction of the rows to rescan
 
@@ -882,6 +970,12 @@ lk_status launch_recheck_cand(const DevState& S, int64_t* stat, int64_t max_rows
 }
 
 lk_status launch_filter_hamerly(const DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    if (S.Xlo != nullptr && S.d >= 32 && (reinterpret_cast<uintptr_t>(S.labels) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(S.ub) & 15) == 0 && (reinterpret_cast<uintptr_t>(S.lb) & 15) == 0) {
+        k_filter_hamerly_tc<<<grid_for(S.n, kThreads * 4, sms * 8), kThreads, 0, st>>>(S, stat);
+        LK_LAUNCH_CHECK();
+        return LK_OK;
+    }
     int grid = grid_for(S.n, kThreads, sms * 8);
     k_filter_hamerly<<<grid, kThreads, 0, st>>>(S, stat);
     LK_LAUNCH_CHECK();
