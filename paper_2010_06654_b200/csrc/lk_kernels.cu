@@ -523,18 +523,23 @@ __device__ __forceinline__ void refine_batch32(const DevState& S, const double* 
     }
 }
 
+// (its own kernel: the batched registers must not lower the occupancy of the
+// one-row-per-warp kernel used for longer rows)
+__global__ void __launch_bounds__(kThreads) k_refine_moved_b32(DevState S, int64_t* stat,
+                                                               const double* qscale) {
+    if (*S.done) return;
+    const int64_t m = stat[LK_STAT_CHANGED];
+    const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
+    for (int64_t e0 = gw * 8; e0 < m; e0 += nwarps * 8) refine_batch32(S, qscale, e0, m);
+    if (blockIdx.x == 0 && threadIdx.x == 0) S.delta[(int64_t)S.k * S.d + 2 * S.k] = m;
+}
+
 template <int G>
 __global__ void __launch_bounds__(kThreads) k_refine_moved(DevState S, int64_t* stat,
                                                            const double* qscale) {
     if (*S.done) return;
     const int64_t m = stat[LK_STAT_CHANGED];
-    if (G == 32 && S.d > 16 && S.d <= 32) {
-        const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-        const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
-        for (int64_t e0 = gw * 8; e0 < m; e0 += nwarps * 8) refine_batch32(S, qscale, e0, m);
-        if (blockIdx.x == 0 && threadIdx.x == 0) S.delta[(int64_t)S.k * S.d + 2 * S.k] = m;
-        return;
-    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sub = lane % G;
     constexpr int kGroupsPerWarp = 32 / G;
@@ -997,7 +1002,10 @@ lk_status launch_refine(const DevState& S, int64_t* stat, const double* qscale, 
         case 4: k_refine_moved<4><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
         case 8: k_refine_moved<8><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
         case 16: k_refine_moved<16><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
-        default: k_refine_moved<32><<<grid, kThreads, 0, st>>>(S, stat, qscale); break;
+        default:
+            if (S.d <= 32) k_refine_moved_b32<<<grid_for(max_rows, kThreads / 4, sms * 8), kThreads, 0, st>>>(S, stat, qscale);
+            else k_refine_moved<32><<<grid, kThreads, 0, st>>>(S, stat, qscale);
+            break;
     }
     LK_LAUNCH_CHECK();
     return LK_OK;
