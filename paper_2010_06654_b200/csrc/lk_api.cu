@@ -518,29 +518,29 @@ lk_status lk_scan_points(lk_ctx* c, void* stream) {
     return LK_OK;
 }
 
+// Fixed-point scales from the scanned exponents, on the device (no host round
+// trip): per dimension 2^(B - e_z), B = 62 - ceil(log2(n_total + 1)), so a sum
+// of n_total values each < 2^B stays below 2^62.
+static __global__ void k_set_quant(const int32_t* qexp, double* qscale, double* qinv, int d, int B) {
+    for (int z = threadIdx.x; z <= d; z += blockDim.x) {
+        const int ez = qexp[z] < -1000 ? 0 : qexp[z];
+        const int sh = B - ez;
+        qscale[z] = ldexp(1.0, sh);
+        qinv[z] = ldexp(1.0, -sh);
+    }
+}
+
 lk_status lk_set_quant(lk_ctx* c, void* stream) {
     if (!c) return LK_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const int d = c->cfg.d;
-    std::vector<int32_t> e(d + 1);
-    LK_CUDA_CHECK(cudaMemcpyAsync(e.data(), c->S.qexp, (d + 1) * 4, cudaMemcpyDeviceToHost, st));
-    LK_CUDA_CHECK(cudaStreamSynchronize(st));
     // Sum of n_total values each < 2^B in magnitude must stay below 2^62.
     int lg = 0;
     while ((1LL << lg) <= c->cfg.n_total) lg++;
     const int B = 62 - lg;
-    std::vector<double> sc(d + 1), inv(d + 1);
-    for (int z = 0; z <= d; z++) {
-        int ez = e[z] < -1000 ? 0 : e[z];
-        int sh = B - ez;
-        sc[z] = ldexp(1.0, sh);
-        inv[z] = ldexp(1.0, -sh);
-    }
-    LK_CUDA_CHECK(cudaMemcpyAsync(buf<double>(c, B_QSCALE), sc.data(), (d + 1) * 8,
-                                  cudaMemcpyHostToDevice, st));
-    LK_CUDA_CHECK(cudaMemcpyAsync(buf<double>(c, B_QINV), inv.data(), (d + 1) * 8,
-                                  cudaMemcpyHostToDevice, st));
-    LK_CUDA_CHECK(cudaStreamSynchronize(st));
+    k_set_quant<<<1, 128, 0, st>>>(c->S.qexp, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV), d, B);
+    LK_LAUNCH_CHECK();
+    c->launches += 1;
     c->quant_set = true;
     return LK_OK;
 }
