@@ -603,6 +603,17 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
     __shared__ int sarg[kThreads / 32];
     __shared__ float sg[1024];  // group drift maxima (t <= 1024)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const bool sg_ok = S.gdrift && S.t_groups <= 1024;
+    // everything the block reads is issued up front (one dependent L2 round
+    // trip instead of one per phase): the changed count, the counters of the
+    // iteration, the cumulative group drifts
+    int64_t changed = 0, curv = 0;
+    if (tid == 0) changed = __ldcg(S.delta + (int64_t)S.k * S.d + 2 * S.k);
+    if (tid < LK_NSTAT) curv = __ldcg(S.cur + tid);
+    float dgc = 0.f;
+    if (S.gdrift && S.lazy && tid < S.t_groups) dgc = __ldcg(S.dgcum + tid);
+    for (int g = tid; g < S.t_groups && g < 1024; g += blockDim.x) sg[g] = 0.f;
+    __syncthreads();
     double acc = 0.0;
     float cm = 0.f, d1 = -1.f, d2 = -1.f;
     int a1 = -1;
@@ -612,6 +623,8 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
         float dj = __ldcg(S.drift + j);
         if (dj > d1) { d2 = d1; d1 = dj; a1 = j; }
         else d2 = fmaxf(d2, dj);
+        // group drifts (Yinyang): max drift over each group's members
+        if (sg_ok) atomicMax(reinterpret_cast<int*>(sg + __ldg(S.group_of + j)), __float_as_int(dj));
     }
     // fixed-order reductions: xor butterflies in each warp, then the warps in order
     auto merge_d = [](float& x1, float& x2, int& xa, float o1, float o2, int oa) {
@@ -631,7 +644,6 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
         merge_d(d1, d2, a1, o1, o2, oa);
     }
     if (lane == 0) { ssum[wid] = acc; smax[wid] = cm; sd1[wid] = d1; sd2[wid] = d2; sarg[wid] = a1; }
-    for (int g = tid; g < S.t_groups && g < 1024; g += blockDim.x) sg[g] = 0.f;
     __syncthreads();
     if (tid == 0) {
         double ss = ssum[0];
@@ -643,44 +655,46 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
             merge_d(x1, x2, xa, sd1[w], sd2[w], sarg[w]);
         }
         ssum[0] = ss;
+        smax[0] = fmaxf(x1, 0.f);  // (the max drift, for the cumulative offset below)
         S.scal[0] = mx;
         S.scal[1] = fmaxf(x1, 0.f);
         S.scal[2] = fmaxf(x2, 0.f);
         S.scal[3] = __int_as_float(xa);
-        const int64_t changed = __ldcg(S.delta + (int64_t)S.k * S.d + 2 * S.k);
         S.delta[(int64_t)S.k * S.d + 2 * S.k] = 0;
-        S.cur[LK_STAT_CHANGED_GLOBAL] = changed;
-        if (t >= 1 && t <= S.t_max) {
-            S.sse[t - 1] = ssum[0];
-            for (int q = 0; q < LK_NSTAT; q++) S.stats[(int64_t)(t - 1) * LK_NSTAT + q] = S.cur[q];
-        }
-        for (int q = 0; q < LK_NSTAT; q++) S.cur[q] = 0;
+        if (t >= 1 && t <= S.t_max) S.sse[t - 1] = ss;
         *S.iter = t + 1;
         if (changed == 0) *S.done = 1;
+    }
+    const int64_t chg0 = __shfl_sync(LK_FULL_MASK, changed, 0);  // (warp 0: thread 0's load)
+    if (tid < LK_NSTAT) {
+        // the iteration's counters (the global changed count in its slot) into
+        // the stats row, then cleared for the next iteration
+        const int64_t v = tid == LK_STAT_CHANGED_GLOBAL ? chg0 : curv;
+        if (t >= 1 && t <= S.t_max) S.stats[(int64_t)(t - 1) * LK_NSTAT + tid] = v;
+        S.cur[tid] = 0;
     }
     // s_half is rebuilt by k_half_sep's atomicMin: start from +inf
     // (gate off: s = 0 never prunes)
     for (int j = tid; j < S.k; j += blockDim.x) S.s_half[j] = S.sgate ? INFINITY : 0.f;
-    // group drifts (Yinyang): max drift over each group's members (shared-memory
-    // maxima when the groups fit, global atomics otherwise)
     if (S.gdrift) {
-        if (S.t_groups <= 1024) {
-            for (int j = tid; j < S.k; j += blockDim.x)
-                atomicMax(reinterpret_cast<int*>(sg + S.group_of[j]), __float_as_int(__ldcg(S.drift + j)));
+        if (sg_ok) {
             __syncthreads();
             for (int g = tid; g < S.t_groups; g += blockDim.x) S.gdrift[g] = sg[g];
+            if (S.lazy)
+                for (int g = tid; g < S.t_groups; g += blockDim.x)
+                    S.dgcum[g] = __fadd_ru(g == tid ? dgc : __ldcg(S.dgcum + g), sg[g]);
+            if (S.lazy && tid == 0) S.scal[4] = __fadd_ru(__ldcg(S.scal + 4), smax[0]);
         } else {
             __syncthreads();
             for (int g = tid; g < S.t_groups; g += blockDim.x) S.gdrift[g] = 0.f;
             __syncthreads();
             for (int j = tid; j < S.k; j += blockDim.x) atomic_max_pos(S.gdrift + S.group_of[j], __ldcg(S.drift + j));
-        }
-        if (S.lazy) {
-            // cumulative group and global drifts of the lazy bound encoding
-            __syncthreads();
-            for (int g = tid; g < S.t_groups; g += blockDim.x)
-                S.dgcum[g] = __fadd_ru(S.dgcum[g], S.gdrift[g]);
-            if (tid == 0) S.scal[4] = __fadd_ru(S.scal[4], S.scal[1]);
+            if (S.lazy) {
+                __syncthreads();
+                for (int g = tid; g < S.t_groups; g += blockDim.x)
+                    S.dgcum[g] = __fadd_ru(S.dgcum[g], S.gdrift[g]);
+                if (tid == 0) S.scal[4] = __fadd_ru(S.scal[4], smax[0]);
+            }
         }
     }
 }
