@@ -334,6 +334,7 @@ struct TcArgs {
     int fast;             // centered top-2: index-free chains + searched columns
     int spin;             // pipeline waits poll (test_wait) instead of suspending
     int dbg;              // timing probe only (wrong labels): 1 = no epilogue work, 2 = no MMAs
+    int kouter;           // K-outer MMA order when the centroid tiles fit the TMEM buffers
     const int64_t* rowcount;  // device row count (overrides m when non-null)
     int n_ct;             // centroid tiles
     int n_kc;             // K chunks
@@ -402,6 +403,11 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                              : (int)((n_rt + gridDim.x - 1) / gridDim.x);
     uint32_t crank = 0;
     if (CL > 1) asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    // K-outer order (d > 32, exactly NBUF centroid tiles: k <= 256): the row
+    // tile's A chunk is consumed by both centroid tiles back to back (an L2 hit
+    // the second time), instead of the whole row tile's A twice (cfg4: 800 KB
+    // per CTA, re-read from DRAM)
+    const bool kouter = !ARES && A.kouter && A.n_ct == NBUF && A.n_kc > 1;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < SM::STAGES; s++) {
@@ -460,8 +466,10 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                     tma_load_2d(&map_ahi, afull, abuf, 0, (int)(rt * BM));
                     tma_load_2d(&map_alo, afull, abuf + SM::A_BYTES, 0, (int)(rt * BM));
                 }
-                for (int ct = 0; ct < A.n_ct; ct++) {
-                    for (int kc = 0; kc < A.n_kc; kc++) {
+                for (int uo = 0; uo < (kouter ? A.n_kc : A.n_ct); uo++) {
+                    for (int ui = 0; ui < (kouter ? A.n_ct : A.n_kc); ui++) {
+                        const int ct = kouter ? ui : uo;
+                        const int kc = kouter ? uo : ui;
                         mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* st = smem + stage * SM::STAGE_BYTES;
                         mbar_expect_tx(&full[stage], SM::STAGE_BYTES);
@@ -509,12 +517,19 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                     mbar_wait(afull, it & 1);
                     tc_fence_after();
                 }
-                for (int ct = 0; ct < A.n_ct; ct++) {
-                    mbar_wait_k(&tempty[acc], acc_phase ^ 1, A.spin);
-                    tc_fence_after();
-                    const uint32_t tmem_d = tmem_base + acc * NACC * BN;
-                    const uint32_t tmem_x = tmem_d + ((SPLIT && !ORD) ? BN : 0);
-                    for (int kc = 0; kc < A.n_kc; kc++) {
+                // K-outer: both centroid tiles' accumulators stay live across the
+                // K loop (buffers 0 and 1), so each A chunk is used twice in a row
+                for (int uo = 0; uo < (kouter ? A.n_kc : A.n_ct); uo++) {
+                    if (!kouter || uo == 0) {
+                        for (int b = 0; b < (kouter ? NBUF : 1); b++)
+                            mbar_wait_k(&tempty[kouter ? b : acc], acc_phase ^ 1, A.spin);
+                        tc_fence_after();
+                    }
+                    for (int ui = 0; ui < (kouter ? A.n_ct : A.n_kc); ui++) {
+                        const int ct = kouter ? ui : uo;
+                        const int kc = kouter ? uo : ui;
+                        const uint32_t tmem_d = tmem_base + (kouter ? ct : acc) * NACC * BN;
+                        const uint32_t tmem_x = tmem_d + ((SPLIT && !ORD) ? BN : 0);
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
                         uint8_t* st = smem + stage * SM::STAGE_BYTES;
@@ -558,8 +573,13 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                         else mma_commit(&empty[stage]);
                         if (++stage == SM::STAGES) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit(&tfull[acc]);
-                    if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+                    if (!kouter) {
+                        mma_commit(&tfull[acc]);
+                        if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+                    } else if (uo == A.n_kc - 1) {
+                        for (int b = 0; b < NBUF; b++) mma_commit(&tfull[b]);
+                        acc_phase ^= 1;  // (acc stays 0: the row tile used every buffer)
+                    }
                 }
                 if (ARES) mma_commit(aempty);  // the resident A is free once these MMAs finish
             }
@@ -1698,6 +1718,8 @@ static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo
     A.fast = knob_fast;
     A.spin = knob_spin;
     static const int knob_dbg = env_int("LK_TC_DBG", 0);
+    static const int knob_kouter = env_int("LK_TC_KOUTER", 1);
+    A.kouter = knob_kouter;
     A.dbg = (MODE == kTop2 && A.center) ? knob_dbg : 0;  // (iteration >= 2 only)
     A.n_kc = (S.d + KC - 1) / KC;
     int smem = Smem<BN, ARES>::TOTAL;
