@@ -444,6 +444,7 @@ def run_ours(args):
                              "rescanned": [r["work"] for r in recs],
                              "rechecked": [r["flagged"] for r in recs],
                              "candidate_rows": [r["candidate"] for r in recs],
+                             "overflow_rows": [r["overflow"] for r in recs],
                              "group_rows": [r["ywl"] for r in recs],
                              "group_scans": [r["pairs"] for r in recs],
                              "group_dists": [r["group_dists"] for r in recs],

@@ -753,7 +753,7 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             }
             {
                 ProfScope p(c, 9, st);
-                s = lkh::launch_assign_simt(S, S.ovf, stat + LK_STAT_OVERFLOW, stat, n, c->sms, st);
+                s = lkh::launch_assign_short(S, S.ovf, stat + LK_STAT_OVERFLOW, stat, n, c->sms, st);
                 if (s != LK_OK) return s;
             }
             c->launches += 4;

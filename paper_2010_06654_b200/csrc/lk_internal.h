@@ -9,6 +9,10 @@ namespace lkh {
 lk_status launch_assign_simt(const lk::DevState& S, const int32_t* rowlist,
                              const int64_t* rowcount, int64_t* stat, int64_t max_rows, int sms,
                              cudaStream_t st);
+// a short device-counted row list (d <= 32: one warp per row)
+lk_status launch_assign_short(const lk::DevState& S, const int32_t* rowlist,
+                              const int64_t* rowcount, int64_t* stat, int64_t max_rows, int sms,
+                              cudaStream_t st);
 // qscale_inline: also add the refinement deltas of the rows it moves
 lk_status launch_recheck(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
                          cudaStream_t st, const double* qscale_inline = nullptr);

@@ -939,6 +939,88 @@ static int grid_for(int64_t work_items, int per_block, int max_blocks) {
     return (int)b;
 }
 
+// A short row list (the tensor-core pass's candidate overflow: ~0.003% of the
+// rows) with d <= 32: one warp per row, lane L scans centroids L, L + 32, ...
+// with k_assign_reg's arithmetic (difference form, fmaf chain in dimension
+// order, first minimum kept), then a (value, index) warp merge and the same
+// certification; a block-per-256-rows scan would leave all but a few SMs idle.
+template <int DP>
+__global__ void __launch_bounds__(kThreads) k_assign_warp(DevState S, const int32_t* rowlist,
+                                                          const int64_t* rowcount, int64_t* stat) {
+    if (*S.done) return;
+    const int64_t m = *rowcount;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t e = gw; e < m; e += nw) {
+        const int64_t row = rowlist[e];
+        const float* xp = S.X32 + row * S.ldx;
+        float x[DP];
+        float xn2 = 0.f;
+#pragma unroll
+        for (int z = 0; z < DP; z++) {
+            x[z] = z < S.d ? __ldg(xp + z) : 0.f;
+            xn2 = fmaf(x[z], x[z], xn2);
+        }
+        float b1 = INFINITY, b2 = INFINITY;
+        int j1 = 0;
+        for (int j = lane; j < S.k; j += 32) {
+            const float* cp = S.C32 + (int64_t)j * S.ldc;
+            float c[DP];
+            if (DP >= 4 && (S.ldc & 3) == 0) {
+                // the lane's centroid row as float4 (rows are zero-padded to ldc)
+#pragma unroll
+                for (int z = 0; z < DP; z += 4) {
+                    const float4 v = (z < S.ldc) ? __ldg(reinterpret_cast<const float4*>(cp + z))
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+                    c[z] = v.x; c[z + 1] = v.y; c[z + 2] = v.z; c[z + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int z = 0; z < DP; z++) c[z] = z < S.d ? __ldg(cp + z) : 0.f;
+            }
+            float acc = 0.f;
+#pragma unroll
+            for (int z = 0; z < DP; z++) {
+                const float t = x[z] - (z < S.d ? c[z] : 0.f);
+                acc = fmaf(t, t, acc);
+            }
+            top2_push(acc, j, b1, j1, b2);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ob1 = __shfl_xor_sync(LK_FULL_MASK, b1, o), ob2 = __shfl_xor_sync(LK_FULL_MASK, b2, o);
+            const int oj1 = __shfl_xor_sync(LK_FULL_MASK, j1, o);
+            if (ob1 < b1 || (ob1 == b1 && oj1 < j1)) {
+                b2 = fminf(b1, ob2);
+                b1 = ob1;
+                j1 = oj1;
+            } else {
+                b2 = fminf(b2, ob1);
+            }
+        }
+        if (lane == 0) {
+            float U1, L2;
+            simt_bounds(S, b1, j1, b2, sqrtf(xn2), U1, L2);
+            if (L2 > U1) {
+                const int old = S.labels[row];
+                S.labels[row] = j1;
+                if (S.strategy != LK_STRAT_LLOYD) {
+                    S.ub[row] = store_ub(S, U1, j1);
+                    write_lb_all(S, row, fmaxf(L2, 0.0f));
+                }
+                if (old != j1) {
+                    const unsigned long long p = atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), 1ull);
+                    S.moved[p] = make_int2((int)row, old);
+                }
+            } else {
+                const unsigned long long p = atomicAdd((unsigned long long*)(stat + LK_STAT_FLAGGED), 1ull);
+                S.flagged[p] = (int)row;
+            }
+        }
+    }
+}
+
 template <int DP, int RPT>
 static lk_status launch_reg(const DevState& S, const int32_t* rowlist, const int64_t* rowcount,
                             int64_t* stat, int64_t max_rows, int sms, cudaStream_t st) {
@@ -948,6 +1030,21 @@ static lk_status launch_reg(const DevState& S, const int32_t* rowlist, const int
     size_t smem = (size_t)tile_k * DP * 4;
     int grid = grid_for(max_rows, kThreads * RPT, sms * 6);
     k_assign_reg<DP, RPT><<<grid, kThreads, smem, st>>>(S, rowlist, rowcount, stat, tile_k);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+// A short device-counted row list (the candidate overflow), warp per row for d <= 32.
+lk_status launch_assign_short(const DevState& S, const int32_t* rowlist, const int64_t* rowcount,
+                              int64_t* stat, int64_t max_rows, int sms, cudaStream_t st) {
+    const int d = S.d;
+    if (d > 32) return launch_assign_simt(S, rowlist, rowcount, stat, max_rows, sms, st);
+    const int grid = grid_for(max_rows, kThreads / 32, sms * 4);
+    if (d <= 2) k_assign_warp<2><<<grid, kThreads, 0, st>>>(S, rowlist, rowcount, stat);
+    else if (d <= 4) k_assign_warp<4><<<grid, kThreads, 0, st>>>(S, rowlist, rowcount, stat);
+    else if (d <= 8) k_assign_warp<8><<<grid, kThreads, 0, st>>>(S, rowlist, rowcount, stat);
+    else if (d <= 16) k_assign_warp<16><<<grid, kThreads, 0, st>>>(S, rowlist, rowcount, stat);
+    else k_assign_warp<32><<<grid, kThreads, 0, st>>>(S, rowlist, rowcount, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
