@@ -254,6 +254,37 @@ __global__ void __launch_bounds__(kThreads) k_recheck_fp64(DevState S, int64_t* 
 // 16 lanes per ambiguous row (two rows per warp): lane i computes candidate
 // slot i exactly (fp64, numpy's pairwise order), a 16-lane (value, index)
 // top-2 merge picks the winner.
+// numpy's pairwise leaf (pw_leaf) for len <= 32 with the row and the centroid
+// in registers (compile-time indices): the same association and roundings.
+__device__ __forceinline__ double pw_leaf32r(const float (&x)[32], const double (&c)[32], int len) {
+    auto t2 = [&](int z) {
+        const double t = __dsub_rn((double)x[z], c[z]);
+        return __dmul_rn(t, t);
+    };
+    if (len < 8) {
+        double res = 0.0;
+#pragma unroll
+        for (int z = 0; z < 8; z++)
+            if (z < len) res = __dadd_rn(res, t2(z));
+        return res;
+    }
+    const int main_end = len - (len % 8);
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = t2(j);
+#pragma unroll
+    for (int i = 1; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            if (8 * i < main_end) r[j] = __dadd_rn(r[j], t2(8 * i + j));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int z = 8; z < 32; z++)
+        if (z >= main_end && z < len) res = __dadd_rn(res, t2(z));
+    return res;
+}
+
 template <int kL>  // lanes per row; lane i takes candidate slots i, i + kL, ...
 __global__ void __launch_bounds__(kThreads) k_recheck_cand(DevState S, int64_t* stat) {
     if (*S.done) return;
@@ -273,7 +304,35 @@ __global__ void __launch_bounds__(kThreads) k_recheck_cand(DevState S, int64_t* 
         const bool over_row = ok && (cnt < 1 || cnt > LK_MAX_CAND);
         double b1 = INFINITY, b2 = INFINITY;
         int j1 = 0x7fffffff;
-        if (ok && !over_row) {
+        // d <= 32, fp32 rows, even d: the row and each candidate in registers
+        // (vector loads: a thread reads whole rows, no 8x sector amplification)
+        const bool regs = kL == 1 && S.d <= 32 && !S.X64 && (S.d & 1) == 0 && S.pw_len == 3 &&
+                          (S.ldx & 3) == 0;
+        if (ok && !over_row && regs) {
+            float xr[32];
+            const float4* xp = reinterpret_cast<const float4*>(S.X32 + row * S.ldx);
+#pragma unroll
+            for (int z4 = 0; z4 < 8; z4++) {
+                const float4 v = 4 * z4 < S.d ? __ldg(xp + z4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                xr[4 * z4] = v.x; xr[4 * z4 + 1] = v.y; xr[4 * z4 + 2] = v.z; xr[4 * z4 + 3] = v.w;
+            }
+#pragma unroll
+            for (int z = 0; z < 32; z++)
+                if (z >= S.d) xr[z] = 0.f;
+            for (int i = 0; i < cnt; i++) {
+                const int j = S.cand_slots[e * LK_MAX_CAND + i];
+                const double2* cp = reinterpret_cast<const double2*>(S.C64 + (int64_t)j * S.d);
+                double c[32];
+#pragma unroll
+                for (int z2 = 0; z2 < 16; z2++) {
+                    const double2 v = 2 * z2 < S.d ? __ldg(cp + z2) : make_double2(0.0, 0.0);
+                    c[2 * z2] = v.x;
+                    c[2 * z2 + 1] = v.y;
+                }
+                const double dd = __dsqrt_rn(pw_leaf32r(xr, c, S.d));
+                merge_top2(b1, j1, b2, dd, j, INFINITY);
+            }
+        } else if (ok && !over_row) {
             for (int i = sub; i < cnt; i += kL) {
                 const int j = S.cand_slots[e * LK_MAX_CAND + i];
                 const double* cp = S.C64 + (int64_t)j * S.d;
