@@ -443,6 +443,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     LK_CUDA_CHECK(cudaMemcpy(S.pw_prog, prog.data(), prog.size() * 4, cudaMemcpyHostToDevice));
     LK_CUDA_CHECK(cudaMemset(S.done, 0, 16));
     S.lazy = L.size[B_GLB] > 0 ? 1 : 0;
+    S.hlog_inline = (S.lazy && S.hlog != nullptr && S.hlog_cap > 0) ? 1 : 0;
     {
         const char* e = getenv("LK_SGATE");  // A/B knob for the centroid-separation gate
         S.sgate = e ? (atoi(e) != 0) : 1;
@@ -696,7 +697,7 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
                     if (s != LK_OK) return s;
                 }
                 c->launches += 1;
-                if (S.hlog) {
+                if (S.hlog && !S.hlog_inline) {
                     ProfScope p(c, 3, st);
                     s = lkh::launch_log_history(S, c->sms, st);
                     if (s != LK_OK) return s;

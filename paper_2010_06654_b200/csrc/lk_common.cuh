@@ -56,6 +56,7 @@ struct DevState {
     int2* hlog;             // [hlog_cap] label-history log: (row, new label) of moved rows
     int64_t* hlog_off;      // [t_max + 1] log offsets per iteration (-1: overflow)
     int64_t hlog_cap;
+    int32_t hlog_inline;    // the fused Yinyang path writes the log itself (no k_log_history)
     double* sse;            // [t_max]
     int32_t* pw_prog;       // numpy pairwise-sum program for the fp64 recheck
     int32_t pw_len;

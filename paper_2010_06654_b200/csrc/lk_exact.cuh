@@ -222,6 +222,11 @@ __device__ __forceinline__ void recheck_row_block(const DevState& S, int64_t* st
             if (qscale_inline) {
                 refine_move(S, qscale_inline, row, old, j1);
                 atomicAdd((unsigned long long*)(S.delta + (int64_t)S.k * S.d + 2 * S.k), 1ull);
+                if (S.hlog_inline) {  // (the fused path logs its own moves)
+                    const int t = *S.iter;
+                    const int64_t hb = (t >= 1 && t <= S.t_max) ? S.hlog_off[t - 1] : -1;
+                    if (hb >= 0 && hb + (int64_t)p < S.hlog_cap) S.hlog[hb + p] = make_int2((int)row, j1);
+                }
             }
         }
     }

@@ -721,6 +721,13 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
         S.scal[3] = __int_as_float(xa);
         S.delta[(int64_t)S.k * S.d + 2 * S.k] = 0;
         if (t >= 1 && t <= S.t_max) S.sse[t - 1] = ss;
+        if (S.hlog_inline && t >= 1 && t <= S.t_max) {
+            // close the iteration's label-history segment (k_log_history's job on
+            // the other paths); curv = this thread's cur[LK_STAT_CHANGED] (slot 0)
+            const int64_t base = __ldcg(S.hlog_off + (t - 1));
+            const int64_t mlog = curv;
+            S.hlog_off[t] = (base >= 0 && base + mlog <= S.hlog_cap) ? base + mlog : -1;
+        }
         *S.iter = t + 1;
         if (changed == 0) *S.done = 1;
     }

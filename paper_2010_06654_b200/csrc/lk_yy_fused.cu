@@ -76,6 +76,7 @@ struct Shared {
     int* boff;
     const uint32_t* ptmp;
     uint16_t* psort;
+    int64_t hbase;     // this iteration's label-history log offset (-1: not logged)
     float* rb1;
     float* rb2;
     int* rp1;
@@ -95,10 +96,13 @@ __device__ __forceinline__ void move_deltas(const DevState* __restrict__ G, cons
 template <int DP>
 __device__ __forceinline__ void commit_move(const DevState& S, const double* qscale,
                                             int64_t* stat, bool mv, int64_t row, int old,
-                                            int nw) {
+                                            int nw, int64_t hbase) {
     if (mv) move_deltas<DP>(S.self, qscale, row, old, nw);
     const int64_t pm = warp_append(mv, (unsigned long long*)(stat + LK_STAT_CHANGED));
     if (mv) S.moved[pm] = make_int2((int)row, old);
+    // label history (lloyd.py:140) as the moved-row log, written here instead of
+    // by k_log_history: slot base + position in the moved list
+    if (mv && hbase >= 0 && hbase + pm < S.hlog_cap) S.hlog[hbase + pm] = make_int2((int)row, nw);
     // the changed count rides in the all-reduce payload
     warp_count(mv, S.delta + (int64_t)S.k * S.d + 2 * S.k);
 }
@@ -266,7 +270,7 @@ __device__ __forceinline__ void drain(const DevState& S, int64_t* stat, const do
                 Q.flag[atomicAdd(sh.nflag, 1)] = q;
             }
         }
-        commit_move<DP>(S, qscale, stat, mv, i, a, bestJ);
+        commit_move<DP>(S, qscale, stat, mv, i, a, bestJ, sh.hbase);
     }
     __syncthreads();
 
@@ -317,7 +321,12 @@ __global__ void __launch_bounds__(kThreads, (DP <= 4 ? 3 : 2)) k_yy_fused(DevSta
     float* rb2 = rb1 + pcap;
     int* rp1 = reinterpret_cast<int*>(rb2 + pcap);
     const float dm = S.scal[4];
-    const Shared sh{dg, dm, goff, bcnt, boff, ptmp, psort, rb1, rb2, rp1, &s_nflag};
+    int64_t hbase = -1;
+    if (S.hlog_inline) {
+        const int t = *S.iter;
+        if (t >= 1 && t <= S.t_max) hbase = S.hlog_off[t - 1];
+    }
+    const Shared sh{dg, dm, goff, bcnt, boff, ptmp, psort, hbase, rb1, rb2, rp1, &s_nflag};
 
     if (threadIdx.x < T) {
         dg[threadIdx.x] = S.dgcum[threadIdx.x];
