@@ -37,7 +37,7 @@ enum InternalBuf {
     B_QEXP, B_HLOG, B_HLOG_OFF, B_CUR,
     // internal
     B_C64_PREV, B_C32, B_CNORM, B_DRIFT, B_SHALF, B_GDRIFT, B_SCAL, B_MOVED, B_FLAGGED, B_WORK,
-    B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_DONE, B_SSE_PART, B_PW_PROG,
+    B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_XSHIFT, B_DONE, B_SSE_PART, B_PW_PROG,
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
     B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB, B_COUNT_
@@ -86,7 +86,10 @@ static bool make_layout(const lk_config& c, Layout* L) {
         c.history_cap < 0)
         return false;
     if (c.n_local > 0x7fffffffLL) return false;  // row ids are int32 on device
-    if (c.k > 32767) return false;                // packed (group, label position) pairs
+    // k itself is unbounded (any 1 <= k <= n, core.py:186-187); the group
+    // strategies pack (group, member position) into 16 + 16 bits, checked
+    // per group in lk_set_groups
+    if (is_group_strategy(c.strategy) && c.groups > 65535) return false;
     memset(L, 0, sizeof(*L));
     L->ldx = (c.d <= 2) ? c.d : ((c.d + 3) / 4) * 4;
     L->ldc = ((c.d + 3) / 4) * 4;
@@ -105,7 +108,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
     L->size[B_SSE] = (uint64_t)tm * 8;
     L->size[B_GROUP_OF] = (uint64_t)k * 4;
     L->size[B_COUNTS] = (uint64_t)k * 8;
-    L->size[B_QEXP] = (uint64_t)(d + 1) * 4;
+    L->size[B_QEXP] = (uint64_t)(3 * d + 1) * 4;
     L->size[B_HLOG] = c.history_cap > 0 ? (uint64_t)c.history_cap * 8 : 0;
     L->size[B_HLOG_OFF] = (uint64_t)(tm + 1) * 8;
     L->size[B_CUR] = (uint64_t)LK_NSTAT * 8;
@@ -123,6 +126,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
     L->size[B_QSUM] = (uint64_t)k * 8;
     L->size[B_QSCALE] = (uint64_t)(d + 1) * 8;
     L->size[B_QINV] = (uint64_t)(d + 1) * 8;
+    L->size[B_XSHIFT] = (uint64_t)d * 8;
     L->size[B_DONE] = 16;
     L->size[B_SSE_PART] = (uint64_t)k * 8;
     L->size[B_PW_PROG] = 4096 * 4;
@@ -379,6 +383,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.counts = buf<int64_t>(c, B_COUNTS);
     S.qsum = buf<int64_t>(c, B_QSUM);
     S.qexp = buf<int32_t>(c, B_QEXP);
+    S.xshift = buf<double>(c, B_XSHIFT);
     S.done = buf<int32_t>(c, B_DONE);
     S.iter = S.done + 1;
     S.cur = buf<int64_t>(c, B_CUR);
@@ -507,7 +512,7 @@ static __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
 lk_status lk_scan_points(lk_ctx* c, void* stream) {
     if (!c) return LK_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    k_fill_i32<<<1, 256, 0, st>>>(c->S.qexp, c->cfg.d + 1, -1100);
+    k_fill_i32<<<1, 256, 0, st>>>(c->S.qexp, 3 * (int64_t)c->cfg.d + 1, INT32_MIN);
     LK_LAUNCH_CHECK();
     c->launches += 2;
     lk_status s = lkh::launch_scan_exp(c->S, c->sms, st);
@@ -519,15 +524,51 @@ lk_status lk_scan_points(lk_ctx* c, void* stream) {
     return LK_OK;
 }
 
-// Fixed-point scales from the scanned exponents, on the device (no host round
-// trip): per dimension 2^(B - e_z), B = 62 - ceil(log2(n_total + 1)), so a sum
-// of n_total values each < 2^B stays below 2^62.
-static __global__ void k_set_quant(const int32_t* qexp, double* qscale, double* qinv, int d, int B) {
-    for (int z = threadIdx.x; z <= d; z += blockDim.x) {
-        const int ez = qexp[z] < -1000 ? 0 : qexp[z];
-        const int sh = B - ez;
-        qscale[z] = ldexp(1.0, sh);
-        qinv[z] = ldexp(1.0, -sh);
+// Fixed-point scales from the scanned ranges, on the device (no host round
+// trip).  Per dimension the shift m_z is the middle of [min x_z, max x_z] and
+// r_z >= |x_z - m_z| its half range; the scale is 2^(B - e_z) with
+// 2^e_z > r_z, B = 62 - ceil(log2(n_total + 1)), so a sum of n_total
+// quantized values stays below 2^62; qexp[d] covers
+// ||x - m||^2 <= sum_z r_z^2.
+__device__ __forceinline__ float unkey(int k) { return __int_as_float(k >= 0 ? k : (k ^ 0x7fffffff)); }
+
+__device__ __forceinline__ void range_of(const int32_t* qexp, int d, int z, double* m, double* r) {
+    const int kh = qexp[d + 1 + z], kl = qexp[2 * d + 1 + z];
+    if (kh == INT32_MIN || kl == INT32_MIN) {  // no rows anywhere
+        *m = 0.0;
+        *r = 0.0;
+        return;
+    }
+    const double hi = (double)unkey(kh), lo = -(double)unkey(kl);
+    const double mm = 0.5 * hi + 0.5 * lo;
+    *m = mm;
+    *r = fmax(hi - mm, mm - lo) * (1.0 + 1e-12);
+}
+
+static __global__ void k_set_quant(int32_t* qexp, double* qscale, double* qinv, double* xshift, int d,
+                                   int B) {
+    for (int z = threadIdx.x; z < d; z += blockDim.x) {
+        double m, r;
+        range_of(qexp, d, z, &m, &r);
+        int ez = 0;
+        if (r > 0.0) frexp(r, &ez);
+        xshift[z] = m;
+        qexp[z] = ez;
+        qscale[z] = ldexp(1.0, B - ez);
+        qinv[z] = ldexp(1.0, ez - B);
+    }
+    if (threadIdx.x == 0) {
+        double r2 = 0.0;
+        for (int z = 0; z < d; z++) {
+            double m, r;
+            range_of(qexp, d, z, &m, &r);
+            r2 = fma(r, r, r2);
+        }
+        int e2 = 0;
+        if (r2 > 0.0) frexp(r2 * (1.0 + 1e-9), &e2);
+        qexp[d] = e2;
+        qscale[d] = ldexp(1.0, B - e2);
+        qinv[d] = ldexp(1.0, e2 - B);
     }
 }
 
@@ -539,7 +580,8 @@ lk_status lk_set_quant(lk_ctx* c, void* stream) {
     int lg = 0;
     while ((1LL << lg) <= c->cfg.n_total) lg++;
     const int B = 62 - lg;
-    k_set_quant<<<1, 128, 0, st>>>(c->S.qexp, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV), d, B);
+    k_set_quant<<<1, 128, 0, st>>>(c->S.qexp, buf<double>(c, B_QSCALE), buf<double>(c, B_QINV),
+                                   c->S.xshift, d, B);
     LK_LAUNCH_CHECK();
     c->launches += 1;
     c->quant_set = true;
@@ -598,7 +640,13 @@ lk_status lk_set_groups(lk_ctx* c, const int32_t* group_of, void* stream) {
         }
         cnt[group_of[j]]++;
     }
-    for (int g = 0; g < t; g++) off[g + 1] = off[g] + cnt[g];
+    for (int g = 0; g < t; g++) {
+        if (cnt[g] > 32767) {
+            set_error("lk_set_groups: group %d has %d members (at most 32767)", g, cnt[g]);
+            return LK_ERR_ARG;
+        }
+        off[g + 1] = off[g] + cnt[g];
+    }
     std::vector<int32_t> fill(off.begin(), off.end()), inv(k);
     for (int j = 0; j < k; j++) {
         inv[j] = fill[group_of[j]];

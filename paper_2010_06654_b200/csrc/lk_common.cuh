@@ -46,8 +46,9 @@ struct DevState {
     int64_t* sums;          // [k, d] fixed-point member sums
     int64_t* counts;        // [k]
     int64_t* qsum;          // [k] fixed-point sum of ||x||^2 per cluster
-    int32_t* qexp;          // [d+1] exponents (max|x_z| < 2^qexp[z]; qexp[d] for ||x||^2)
-    int32_t* qshift;        // [d+1] fixed-point shifts
+    int32_t* qexp;          // [3d+1]: exponents (|x_z - m_z| < 2^qexp[z]; qexp[d] for
+                            // ||x - m||^2), then the order keys of max x_z and of max -x_z
+    double* xshift;         // [d] m: the fixed-point sums are of x - m
     int32_t* done;          // [1] set once an iteration had changed == 0
     int32_t* iter;          // [1] current iteration (1-based), advanced by the update
     int64_t* cur;           // [LK_NSTAT] counters of the iteration in flight

@@ -80,6 +80,13 @@ __device__ __forceinline__ double load_x(const DevState& S, int64_t row, int z) 
     return S.X64 ? S.X64[row * S.d + z] : (double)__ldg(S.X32 + row * S.ldx + z);
 }
 
+// x_z - m_z: what the fixed-point member sums accumulate (the shift m is the
+// middle of the data's range, so the sums and the SSE do not cancel for data
+// far from the origin)
+__device__ __forceinline__ double load_xs(const DevState& S, int64_t row, int z) {
+    return load_x(S, row, z) - __ldg(S.xshift + z);
+}
+
 // Lanes per moved row in k_refine_moved (power of two >= min(d, 32)).
 __host__ __device__ __forceinline__ int refine_lanes(int d) {
     return d <= 1 ? 1 : d <= 2 ? 2 : d <= 4 ? 4 : d <= 8 ? 8 : d <= 16 ? 16 : 32;
@@ -94,7 +101,7 @@ __device__ __forceinline__ double row_norm2_refine(const DevState& S, int64_t ro
     for (int s = 0; s < G; s++) {
         double a = 0.0;
         for (int z = s; z < S.d; z += G) {
-            const double v = load_x(S, row, z);
+            const double v = load_xs(S, row, z);
             a = fma(v, v, a);
         }
         p[s] = a;
@@ -117,7 +124,7 @@ __device__ __forceinline__ double row_norm2_refine_r(const DevState& S, int64_t 
         for (int z = s; z < DP; z += 1) {
             // dimension z belongs to lane z % G
             if (z < S.d && (z & (G - 1)) == s) {
-                const double v = load_x(S, row, z);
+                const double v = load_xs(S, row, z);
                 a = fma(v, v, a);
             }
         }
@@ -147,7 +154,7 @@ __device__ __forceinline__ void refine_move(const DevState& S, const double* qsc
         double v[P], sc[P];
 #pragma unroll
         for (int z = 0; z < P; z++) {
-            v[z] = z < S.d ? load_x(S, row, z) : 0.0;
+            v[z] = z < S.d ? load_xs(S, row, z) : 0.0;
             sc[z] = z < S.d ? __ldg(qscale + z) : 0.0;
         }
 #pragma unroll
@@ -162,7 +169,7 @@ __device__ __forceinline__ void refine_move(const DevState& S, const double* qsc
         }
     } else {
         for (int z = 0; z < S.d; z++) {
-            const double v = load_x(S, row, z);
+            const double v = load_xs(S, row, z);
             const long long q = __double2ll_rn(v * qscale[z]);
             if (q) {
                 atomicAdd((unsigned long long*)(dS + (int64_t)nw * S.d + z), (unsigned long long)q);

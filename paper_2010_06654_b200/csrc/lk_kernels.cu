@@ -16,6 +16,7 @@
 //       the empty-cluster rule (lloyd.py:94-96), drifts (bounds.py:31-35),
 //       s = half nearest-other distance (bounds.py:38-47), SSE (core.py:172).
 #include <float.h>
+#include <limits.h>
 #include <math.h>
 
 #include "lk_common.cuh"
@@ -536,7 +537,7 @@ __device__ __forceinline__ void refine_batch32(const DevState& S, const double* 
 #pragma unroll
     for (int b = 0; b < B; b++) {
         nw[b] = row[b] >= 0 ? S.labels[row[b]] : 0;
-        v[b] = (row[b] >= 0 && lane < S.d) ? load_x(S, row[b], lane) : 0.0;
+        v[b] = (row[b] >= 0 && lane < S.d) ? load_xs(S, row[b], lane) : 0.0;
     }
     const double scq = qscale[S.d];
     long long run_q = 0, run_qq = 0;
@@ -619,7 +620,7 @@ __global__ void __launch_bounds__(kThreads) k_refine_moved(DevState S, int64_t* 
             old = mv.y;
             nw = S.labels[row];
             for (int z = sub; z < S.d; z += G) {
-                double v = load_x(S, row, z);
+                double v = load_xs(S, row, z);
                 x2 = fma(v, v, x2);
                 long long q = __double2ll_rn(v * qscale[z]);
                 if (q) {
@@ -785,8 +786,9 @@ __device__ __forceinline__ void update_centroid_warp(const DevState& S, int j, c
         double old = S.C64[(int64_t)j * S.d + z];
         double c = old;
         if (cnt > 0) {
+            // (sums are of x - m: sr / cnt is the mean's offset from m)
             double sr = (double)sv * qinv[z];
-            c = sr / (double)cnt;
+            c = __ldg(S.xshift + z) + sr / (double)cnt;
             s2 = fma(sr, sr, s2);
         }
         S.C64_prev[(int64_t)j * S.d + z] = old;
@@ -958,35 +960,58 @@ __global__ void k_fill_inf(DevState S) {
     if (j < S.k) S.s_half[j] = INFINITY;
 }
 
-// Per-dimension max |x| exponents (frexp convention: |x| < 2^e) of the local
-// rows, and the exponent of max ||x||^2 in qexp[d].  One warp per row, lanes
-// over dimensions; per-warp maxima in shared memory, then global atomicMax.
-__global__ void __launch_bounds__(kThreads) k_scan_exp(DevState S) {
-    extern __shared__ int wexp[];  // [8 warps][d + 1]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* we = wexp + warp * (S.d + 1);
-    for (int z = lane; z <= S.d; z += 32) we[z] = -1100;
-    __syncwarp();
-    for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < S.n; i += (int64_t)gridDim.x * 8) {
-        double s = 0.0;
-        for (int z = lane; z < S.d; z += 32) {
-            double v = load_x(S, i, z);
-            s = fma(v, v, s);
-            if (v != 0.0) {
-                int ex;
-                frexp(fabs(v), &ex);
-                we[z] = max(we[z], ex);
+// Per-dimension range of the local rows as order keys (fkey: the int32 order
+// of the fp32 values): qexp[d + 1 + z] = max key of x_z, qexp[2d + 1 + z] =
+// max key of -x_z (fp64 input: rounded outward to fp32).  Multi-GPU callers
+// all-reduce(max) the whole qexp buffer before lk_set_quant.  For d <= 1024
+// each thread owns one dimension (blockDim a multiple of d), block maxima in
+// shared memory, then one global atomic per block and key.
+__device__ __forceinline__ int fkey(float f) {
+    const int b = __float_as_int(f);
+    return b >= 0 ? b : (b ^ 0x7fffffff);
+}
+
+__global__ void __launch_bounds__(1024) k_scan_range(DevState S) {
+    extern __shared__ int skey[];  // [2d]
+    const int d = S.d;
+    for (int z = threadIdx.x; z < 2 * d; z += blockDim.x) skey[z] = INT_MIN;
+    __syncthreads();
+    const auto val = [&](int64_t row, int z, float& hi, float& lo) {
+        if (S.X64) {
+            const double v = S.X64[row * d + z];
+            hi = fmaxf(hi, __double2float_ru(v));
+            lo = fminf(lo, __double2float_rd(v));
+        } else {
+            const float v = __ldg(S.X32 + row * S.ldx + z);
+            hi = fmaxf(hi, v);
+            lo = fminf(lo, v);
+        }
+    };
+    if (d <= 1024) {
+        const int per = blockDim.x / d;
+        if ((int)threadIdx.x < per * d) {
+            const int z = threadIdx.x % d, r0 = threadIdx.x / d;
+            float hi = -INFINITY, lo = INFINITY;
+            for (int64_t row = (int64_t)blockIdx.x * per + r0; row < S.n;
+                 row += (int64_t)gridDim.x * per)
+                val(row, z, hi, lo);
+            if (hi >= lo) {
+                atomicMax(skey + z, fkey(hi));
+                atomicMax(skey + d + z, fkey(-lo));
             }
         }
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(LK_FULL_MASK, s, o);
-        if (lane == 0 && s > 0.0) {
-            int ex;
-            frexp(s * (1.0 + 1e-9), &ex);
-            we[S.d] = max(we[S.d], ex);
-        }
+    } else {
+        for (int64_t row = blockIdx.x; row < S.n; row += gridDim.x)
+            for (int z = threadIdx.x; z < d; z += blockDim.x) {
+                float hi = -INFINITY, lo = INFINITY;
+                val(row, z, hi, lo);
+                atomicMax(skey + z, fkey(hi));
+                atomicMax(skey + d + z, fkey(-lo));
+            }
     }
-    __syncwarp();
-    for (int z = lane; z <= S.d; z += 32) atomicMax(S.qexp + z, we[z]);
+    __syncthreads();
+    for (int z = threadIdx.x; z < 2 * d; z += blockDim.x)
+        if (skey[z] != INT_MIN) atomicMax(S.qexp + d + 1 + z, skey[z]);
 }
 
 }  // namespace lk
@@ -1262,60 +1287,15 @@ lk_status init_simt_attributes() {
     return LK_OK;
 }
 
-// Small d: one thread per row, per-thread maxima in registers, shared then
-// global atomicMax (the warp-per-row version idles 30 of 32 lanes at d = 2).
-template <int D>
-__global__ void __launch_bounds__(kThreads) k_scan_exp_small(DevState S) {
-    __shared__ int se[D + 1];
-    if (threadIdx.x <= D) se[threadIdx.x] = -1100;
-    __syncthreads();
-    int e[D + 1];
-#pragma unroll
-    for (int z = 0; z <= D; z++) e[z] = -1100;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < S.n;
-         i += (int64_t)gridDim.x * kThreads) {
-        double s2 = 0.0;
-#pragma unroll
-        for (int z = 0; z < D; z++) {
-            if (z < S.d) {
-                const double v = load_x(S, i, z);
-                s2 = fma(v, v, s2);
-                if (v != 0.0) {
-                    int ex;
-                    frexp(fabs(v), &ex);
-                    e[z] = max(e[z], ex);
-                }
-            }
-        }
-        if (s2 > 0.0) {
-            int ex;
-            frexp(s2 * (1.0 + 1e-9), &ex);
-            e[D] = max(e[D], ex);
-        }
-    }
-#pragma unroll
-    for (int z = 0; z < D; z++)
-        if (z < S.d) atomicMax(&se[z], e[z]);
-    atomicMax(&se[D], e[D]);
-    __syncthreads();
-    if (threadIdx.x < S.d) atomicMax(S.qexp + threadIdx.x, se[threadIdx.x]);
-    if (threadIdx.x == 0) atomicMax(S.qexp + S.d, se[D]);
-}
-
 lk_status launch_scan_exp(const DevState& S, int sms, cudaStream_t st) {
-    if (S.d <= 8) {
-        const int grid = grid_for(S.n, kThreads, sms * 4);
-        if (S.d <= 2) k_scan_exp_small<2><<<grid, kThreads, 0, st>>>(S);
-        else if (S.d <= 4) k_scan_exp_small<4><<<grid, kThreads, 0, st>>>(S);
-        else k_scan_exp_small<8><<<grid, kThreads, 0, st>>>(S);
-        LK_LAUNCH_CHECK();
-        return LK_OK;
-    }
-    size_t smem = (size_t)8 * (S.d + 1) * sizeof(int);
+    const int d = S.d;
+    const int bs = d <= 1024 ? d * (1024 / d) : 1024;
+    const size_t smem = (size_t)2 * d * sizeof(int);
     if (smem > 48 * 1024)
-        LK_CUDA_CHECK(cudaFuncSetAttribute(k_scan_exp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LK_CUDA_CHECK(cudaFuncSetAttribute(k_scan_range, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
-    k_scan_exp<<<grid_for(S.n, 8, sms * 4), kThreads, smem, st>>>(S);
+    const int64_t rows_per_block = d <= 1024 ? bs / d : 1;
+    k_scan_range<<<grid_for(S.n, (int)rows_per_block * 8, sms * 2), bs, smem, st>>>(S);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }

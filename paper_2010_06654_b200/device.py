@@ -248,7 +248,7 @@ class DeviceLloyd:
         self.delta = self._view("delta", torch.int64, (self.delta_len,))
         self.stats = self._view("stats", torch.int64, (max(1, self.t_max), nat.NSTAT))
         self.sse_buf = self._view("sse", torch.float64, (max(1, self.t_max),))
-        self.qexp = self._view("qexp", torch.int32, (self.d + 1,))
+        self.qexp = self._view("qexp", torch.int32, (3 * self.d + 1,))
         self.counts = self._view("counts", torch.int64, (self.k,))
         self.hlog = (self._view("hlog", torch.int32, (self.history_cap, 2))
                      if self.history_cap else None)
@@ -403,8 +403,9 @@ class DeviceLloyd:
         torch = _torch()
         self.set_centroids(init)
         T = self.t_max
-        if check_every <= 0:
-            check_every = self.history_iters  # the log drains at its capacity
+        if check_every <= 0 or check_every > self.history_iters:
+            # the log holds history_iters iterations: drain at least that often
+            check_every = self.history_iters
         res = {"iterations": 0, "converged": False, "history": [], "records": []}
         if T <= 0:
             res["centroids"] = np.array(init, dtype=np.float64, copy=True)

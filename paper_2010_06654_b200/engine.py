@@ -74,7 +74,9 @@ def run_engine(data, k: int, config: KnobConfig, *, init=None, init_method: str 
         res = run_pruner(x, k, "search", init=init, t_max=config.t_max,
                          capacity=config.capacity, ctx=ctx, kernel=kernel)
     elif config.index_mode == "none":
-        if config.bound_strategy in ("none", "full"):
+        if config.bound_strategy == "none":
+            # "full" is a tree-engine profile (engine.py:129); at index_mode="none"
+            # the reference hands it to run_pruner, which raises (pruners.py:868-869)
             res = run_lloyd(x, k, init=init, t_max=config.t_max, ctx=ctx, kernel=kernel)
         else:
             res = run_pruner(x, k, config.bound_strategy, init=init, t_max=config.t_max,

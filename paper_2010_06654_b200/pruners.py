@@ -52,7 +52,8 @@ def gpu_groups(strategy: str, n: int, k: int, d: int = 0) -> int:
         # table dominate an iteration's traffic at large k), at most 32 groups;
         # the fused path (d <= 32) reads a row's group table only when its
         # global bound fails
-        return max(4, min(32, round(k / 64)))
+        # (and no group above 32767 members: the packed pair format)
+        return max(4, min(32, round(k / 64)), -(-k // 32000))
     return 0
 
 

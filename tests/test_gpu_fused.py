@@ -152,3 +152,23 @@ def test_tensor_core_d32_variants(env_set):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("strategy", ["yinyang", "hamerly", "lloyd"])
+def test_history_drained_mid_run(oracle, strategy):
+    """A label-history log holding 2 iterations is drained and rewound mid-run
+    (history_iters < t_max; a larger check_every is clamped to it): the
+    rebuilt assign_history still equals the oracle's at every iteration."""
+    from paper_2010_06654_b200.device import DeviceLloyd
+    x = blobs(5000, 8, 20, 2.0, seed=21)
+    k, t_max = 40, 9
+    init = x[np.random.default_rng(3).choice(len(x), k, replace=False)].astype(np.float64)
+    eng = DeviceLloyd(x, k, strategy, t_max, groups=8 if strategy == "yinyang" else 0,
+                      history_iters=2)
+    try:
+        out = eng.run(init, check_every=5)
+    finally:
+        eng.close()
+    ref = oracle.run_lloyd(x, k, init, t_max)
+    check_trajectory(oracle, x, init, out["history"], ref["history"], f"drain {strategy}")
+    assert out["converged"] == ref["converged"]
