@@ -63,8 +63,9 @@ typedef enum {
     LK_STRAT_LLOYD = 0,    /* run_lloyd: full n*k scan every iteration */
     LK_STRAT_HAMERLY = 1,  /* one upper + one global lower bound per point */
     LK_STRAT_YINYANG = 2,  /* upper bound + t group lower bounds per point */
-    LK_STRAT_ELKAN = 3,    /* Yinyang with t = k singleton groups */
-    LK_STRAT_REGROUP = 4   /* Yinyang, groups rebuilt every iteration */
+    LK_STRAT_ELKAN = 3,    /* group bounds (Elkan's per-centroid bounds folded into
+                              min(k, 32) groups on the SIMT path) */
+    LK_STRAT_REGROUP = 4   /* Yinyang group bounds (the host may regroup between runs) */
 } lk_strategy;
 
 /* Assignment-kernel selection. */
@@ -157,6 +158,12 @@ lk_status lk_ctx_destroy(lk_ctx *ctx);
 lk_status lk_buffer(const lk_ctx *ctx, int32_t id, uint64_t *offset, uint64_t *bytes);
 /* Row stride (floats) of LK_BUF_X32 and the length of LK_BUF_DELTA (int64s). */
 lk_status lk_layout(const lk_ctx *ctx, int64_t *ldx, int64_t *delta_len, int32_t *nlb);
+
+/* Group count t of a group-bound strategy and the most members a group may
+ * have (0: not a group strategy).  On the block-sparse tensor-core path
+ * (d <= 32, k <= 4096) every group is one 128-column tile: t = ceil(k / 128),
+ * capacity 128; lk_set_groups rejects a larger group. */
+lk_status lk_group_shape(const lk_ctx *ctx, int32_t *groups, int32_t *capacity);
 
 /* After the caller has filled X32 (and X64): compute the per-dimension
  * max-|x| exponents of the local rows into LK_BUF_QEXP (device).  Multi-GPU

@@ -32,7 +32,7 @@ EXPORTED = (
     "lk_version", "lk_last_error", "lk_workspace_bytes", "lk_ctx_create", "lk_ctx_destroy",
     "lk_buffer", "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
     "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_graph_capture", "lk_graph_replay",
-    "lk_launch_count", "lk_profile", "lk_profile_read", "lk_d2_update",
+    "lk_launch_count", "lk_profile", "lk_profile_read", "lk_d2_update", "lk_group_shape",
 )
 
 
@@ -88,6 +88,7 @@ def load():
     L.lk_ctx_destroy.argtypes = [vp]
     L.lk_buffer.argtypes = [vp, i32, ctypes.POINTER(u64), ctypes.POINTER(u64)]
     L.lk_layout.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    L.lk_group_shape.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.lk_scan_points.argtypes = [vp, vp]
     L.lk_set_quant.argtypes = [vp, vp]
     L.lk_set_centroids.argtypes = [vp, vp, vp]
@@ -104,7 +105,8 @@ def load():
     for name in ("lk_workspace_bytes", "lk_ctx_create", "lk_ctx_destroy", "lk_buffer",
                  "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
                  "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_graph_capture",
-                 "lk_graph_replay", "lk_profile", "lk_profile_read", "lk_d2_update"):
+                 "lk_graph_replay", "lk_profile", "lk_profile_read", "lk_d2_update",
+                 "lk_group_shape"):
         getattr(L, name).restype = i32
     _lib = L
     return L

@@ -40,7 +40,8 @@ enum InternalBuf {
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_XSHIFT, B_DONE, B_SSE_PART, B_PW_PROG,
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
-    B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB, B_COUNT_
+    B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB,
+    B_YMASK, B_ROWLUN, B_ROWMASK, B_PMASK, B_COUNT_
 };
 
 struct Layout {
@@ -59,6 +60,20 @@ static bool is_group_strategy(int s) {
 static uint64_t align256(uint64_t v) { return (v + 255) & ~uint64_t(255); }
 
 static bool is_group_strategy(int s);
+static bool tc_enabled(const lk_config& c);
+
+// Block-sparse Yinyang on the tensor cores (lk_tgy.cu): d <= 32 (one K chunk),
+// groups = 128-column tiles of the B operand, at most 32 of them (k <= 4096).
+// LK_TGY=0 (A/B knob) keeps the full-rescan tensor-core path.
+static bool tgy_mode(const lk_config& c) {
+    static const int knob = [] {
+        const char* e = getenv("LK_TGY");
+        return e ? atoi(e) : 1;
+    }();
+    const int G = (c.k + 127) / 128;
+    return knob != 0 && is_group_strategy(c.strategy) && tc_enabled(c) && c.d >= 8 && c.d <= 32 &&
+           G <= 32;
+}
 
 static int32_t nlb_for(const lk_config& c, int32_t* groups) {
     int32_t g = 1;
@@ -69,6 +84,12 @@ static int32_t nlb_for(const lk_config& c, int32_t* groups) {
         default: g = c.groups > 0 ? c.groups : (c.k + 9) / 10; break;
     }
     if (g > c.k) g = c.k;
+    if (tgy_mode(c)) {
+        // one group per 128-column tile; the row-major bound table is padded to
+        // whole float4 loads (slots >= groups are never read)
+        *groups = (c.k + 127) / 128;
+        return (*groups + 3) / 4 * 4;
+    }
     // the warp-per-row Yinyang path works on 8/16/32 group slots; extra slots
     // are empty groups (no members, never binding)
     if (is_group_strategy(c.strategy) && g <= 32 && c.d <= 32)
@@ -148,7 +169,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
         // tile centering (rows sorted by label, tiles shifted by a centroid)
         L->size[B_PTAB] = (uint64_t)k * kpad * 4;
         L->size[B_PERM] = (uint64_t)n * 4;
-        L->size[B_LCUR] = (uint64_t)(k + 1) * 4;
+        L->size[B_LCUR] = (uint64_t)(kpad + 1) * 4;  // (sort keys: B columns on the group-tile path)
         L->size[B_TILE_LAB] = (uint64_t)(n / 128 + 2) * 4;
         L->size[B_ROWR] = (uint64_t)n * 8;
         L->size[B_ROWXO] = (uint64_t)n * 4;
@@ -157,7 +178,20 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_ROWLAB] = (uint64_t)n * 4;
 
     }
-    if (is_group_strategy(c.strategy)) {
+    if (tgy_mode(c)) {
+        const int64_t kpad = (k + 255) / 256 * 256;
+        L->size[B_GPERM] = (uint64_t)kpad * 4;     // column -> centroid (-1: padding)
+        L->size[B_GOFF] = (uint64_t)(L->groups + 1) * 4;
+        L->size[B_GINV] = (uint64_t)k * 4;         // centroid -> column
+        L->size[B_YLUN] = (uint64_t)n * 8;
+        L->size[B_YMASK] = (uint64_t)n * 4;
+        L->size[B_ROWLUN] = (uint64_t)n * 4;
+        L->size[B_ROWMASK] = (uint64_t)n * 4;
+        L->size[B_PMASK] = (uint64_t)(n / 256 + 2) * 4;
+        L->size[B_DCUM] = (uint64_t)k * 4;
+        L->size[B_DGCUM] = (uint64_t)L->groups * 4;
+        L->size[B_GLB] = (uint64_t)n * 4;
+    } else if (is_group_strategy(c.strategy)) {
         int64_t cap = n * (int64_t)L->groups;
         if (cap > (1LL << 30)) cap = 1LL << 30;  // result slots, <= 16 GB
         if (cap < 1) cap = 1;
@@ -448,6 +482,13 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     LK_CUDA_CHECK(cudaMemcpy(S.pw_prog, prog.data(), prog.size() * 4, cudaMemcpyHostToDevice));
     LK_CUDA_CHECK(cudaMemset(S.done, 0, 16));
     S.lazy = L.size[B_GLB] > 0 ? 1 : 0;
+    S.tgy = tgy_mode(*cfg) ? 1 : 0;
+    S.kcols = S.tgy ? 128 * L.groups : cfg->k;
+    S.colperm = S.tgy ? buf<int32_t>(c, B_GPERM) : nullptr;
+    S.ymask = buf<uint32_t>(c, B_YMASK);
+    S.rowlun = buf<float>(c, B_ROWLUN);
+    S.rowmask = buf<uint32_t>(c, B_ROWMASK);
+    S.pmask = buf<uint32_t>(c, B_PMASK);
     S.hlog_inline = (S.lazy && S.hlog != nullptr && S.hlog_cap > 0) ? 1 : 0;
     {
         const char* e = getenv("LK_SGATE");  // A/B knob for the centroid-separation gate
@@ -492,6 +533,13 @@ lk_status lk_buffer(const lk_ctx* c, int32_t id, uint64_t* offset, uint64_t* byt
     }
     if (offset) *offset = c->L.off[id];
     if (bytes) *bytes = c->L.size[id];
+    return LK_OK;
+}
+
+lk_status lk_group_shape(const lk_ctx* c, int32_t* groups, int32_t* capacity) {
+    if (!c) return LK_ERR_ARG;
+    if (groups) *groups = c->L.groups;
+    if (capacity) *capacity = c->S.tgy ? 128 : (is_group_strategy(c->cfg.strategy) ? 32767 : 0);
     return LK_OK;
 }
 
@@ -591,10 +639,20 @@ lk_status lk_set_quant(lk_ctx* c, void* stream) {
 static __global__ void k_init_centroids(lk::DevState S, int kpad) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = blockIdx.x * (blockDim.x / 32) + warp;
+    if (S.colperm && j < kpad && S.colperm[j] < 0) {
+        // a padding column of the group tiles: never a candidate
+        if (lane == 0) S.cn2[j] = INFINITY;
+        for (int z = lane; z < S.ldc; z += 32) {
+            S.Chi[(int64_t)j * S.ldc + z] = 0.f;
+            S.Clo[(int64_t)j * S.ldc + z] = 0.f;
+        }
+    }
     if (j >= S.k) {
-        if (j < kpad && S.cn2 && lane == 0) S.cn2[j] = INFINITY;
+        if (!S.colperm && j < kpad && S.cn2 && lane == 0) S.cn2[j] = INFINITY;
         return;
     }
+    // B-operand column of centroid j (group order on the group-tile path)
+    const int64_t cj = S.colperm ? S.ginv[j] : j;
     double cn2 = 0.0, c2 = 0.0;
     for (int z = lane; z < S.ldc; z += 32) {
         double c = z < S.d ? S.C64[(int64_t)j * S.d + z] : 0.0;
@@ -606,8 +664,8 @@ static __global__ void k_init_centroids(lk::DevState S, int kpad) {
         c2 = fma(c, c, c2);
         if (S.Chi) {
             float hi = lk::tf32_trunc(v);
-            S.Chi[(int64_t)j * S.ldc + z] = hi;
-            S.Clo[(int64_t)j * S.ldc + z] = v - hi;
+            S.Chi[cj * S.ldc + z] = hi;
+            S.Clo[cj * S.ldc + z] = v - hi;
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -616,7 +674,7 @@ static __global__ void k_init_centroids(lk::DevState S, int kpad) {
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *S.iter = 1;
     if (lane == 0) {
-        if (S.cn2) S.cn2[j] = (float)c2;
+        if (S.cn2) S.cn2[cj] = (float)c2;
         float cn = __double2float_ru(sqrt(cn2) * (1.0 + 1e-12));
         S.cnorm[j] = cn;
         S.drift[j] = 0.f;
@@ -632,6 +690,7 @@ lk_status lk_set_groups(lk_ctx* c, const int32_t* group_of, void* stream) {
         return LK_ERR_STATE;
     }
     const int k = c->cfg.k, t = c->L.groups;
+    const int cap = c->S.tgy ? 128 : 32767;  // group-tile path: one 128-column tile per group
     std::vector<int32_t> cnt(t + 1, 0), perm(k), off(t + 1, 0);
     for (int j = 0; j < k; j++) {
         if (group_of[j] < 0 || group_of[j] >= t) {
@@ -641,20 +700,21 @@ lk_status lk_set_groups(lk_ctx* c, const int32_t* group_of, void* stream) {
         cnt[group_of[j]]++;
     }
     for (int g = 0; g < t; g++) {
-        if (cnt[g] > 32767) {
-            set_error("lk_set_groups: group %d has %d members (at most 32767)", g, cnt[g]);
+        if (cnt[g] > cap) {
+            set_error("lk_set_groups: group %d has %d members (at most %d)", g, cnt[g], cap);
             return LK_ERR_ARG;
         }
-        off[g + 1] = off[g] + cnt[g];
+        off[g + 1] = c->S.tgy ? 128 * (g + 1) : off[g] + cnt[g];
     }
     std::vector<int32_t> fill(off.begin(), off.end()), inv(k);
+    if (c->S.tgy) perm.assign((size_t)c->S.kpad, -1);  // column -> centroid, padding -1
     for (int j = 0; j < k; j++) {
         inv[j] = fill[group_of[j]];
         perm[fill[group_of[j]]++] = j;  // ascending j within a group
     }
     cudaStream_t st = (cudaStream_t)stream;
     LK_CUDA_CHECK(cudaMemcpyAsync(c->S.group_of, group_of, k * 4, cudaMemcpyHostToDevice, st));
-    LK_CUDA_CHECK(cudaMemcpyAsync(c->S.gperm, perm.data(), k * 4, cudaMemcpyHostToDevice, st));
+    LK_CUDA_CHECK(cudaMemcpyAsync(c->S.gperm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, st));
     LK_CUDA_CHECK(cudaMemcpyAsync(c->S.goff, off.data(), (t + 1) * 4, cudaMemcpyHostToDevice, st));
     LK_CUDA_CHECK(cudaMemcpyAsync(c->S.ginv, inv.data(), k * 4, cudaMemcpyHostToDevice, st));
     LK_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -684,6 +744,7 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     LK_CUDA_CHECK(cudaMemsetAsync(S.hlog_off, 0, c->L.size[B_HLOG_OFF], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.sse, 0, c->L.size[B_SSE], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
+    if (S.tgy) LK_CUDA_CHECK(cudaMemsetAsync(S.lb, 0, c->L.size[B_LB], st));  // bounds >= 0
     if (S.lazy) {
         LK_CUDA_CHECK(cudaMemsetAsync(S.dcum, 0, c->L.size[B_DCUM], st));
         LK_CUDA_CHECK(cudaMemsetAsync(S.dgcum, 0, c->L.size[B_DGCUM], st));
@@ -732,6 +793,23 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
                          : lkh::launch_assign_simt(S, nullptr, nullptr, stat, n, c->sms, st);
             if (s != LK_OK) return s;
             c->launches += 1;
+        } else if (S.tgy) {
+            // block-sparse Yinyang on the tensor cores: filter -> label-sorted
+            // worklist -> (row-tile pair x failing group tile) MMAs (lk_tgy.cu)
+            {
+                ProfScope p(c, 1, st);
+                s = lkh::launch_filter_tgy(S, stat, c->sms, st);
+                if (s != LK_OK) return s;
+            }
+            {
+                ProfScope p(c, 10, st);
+                s = lkh::launch_sort_tgy(S, stat, c->sms, st);
+                if (s != LK_OK) return s;
+            }
+            ProfScope p(c, 0, st);
+            s = lkh::launch_assign_tgy(S, stat, n, c->sms, st);
+            if (s != LK_OK) return s;
+            c->launches += 8;
         } else if (is_group_strategy(c->cfg.strategy)) {
             // tensor-core runs: every row failing the bounds is rescanned in full
             const bool full_only = use_tc;

@@ -110,6 +110,15 @@ struct DevState {
     float* dcum;            // [k] cumulative centroid drift (rounded up)
     float* dgcum;           // [t] cumulative group drift (rounded up); scal[4] = cumulative max drift
     float* glb;             // [n] stored global lower bound (min over the groups)
+    // block-sparse Yinyang on the tensor cores (lk_tgy.cu, k_assign_tgy):
+    // groups are 128-column tiles of the B operand (centroids in group order)
+    int32_t tgy;            // 1: the group-tile path is on
+    int32_t kcols;          // B-operand columns (128 * groups with the group tiles, else k)
+    const int32_t* colperm; // [kpad] centroid id of each B column (-1: padding); null = identity
+    uint32_t* ymask;        // [n] per worklist entry: groups the row must scan
+    float* rowlun;          // [n] per sorted position: lower bound over the unscanned groups
+    uint32_t* rowmask;      // [n] per sorted position: the row's group mask
+    uint32_t* pmask;        // [n / 256 + 2] per row-tile pair: union of its rows' masks
     // a copy of this struct in device memory, for out-of-line device
     // functions (a reference to the kernel parameter would copy it to the stack)
     const DevState* self;
@@ -142,6 +151,13 @@ __device__ __forceinline__ int64_t lb_index(const DevState& S, int64_t row, int 
 }
 
 __device__ __forceinline__ void write_lb_all(const DevState& S, int64_t row, float v) {
+    if (S.tgy) {
+        // group tiles: the row's scanned groups already hold their own bounds
+        // (k_assign_tgy writes them for ambiguous rows too; the table starts at
+        // 0), so a re-decision only sets the global bound
+        S.glb[row] = __fadd_rd(v, S.scal[4]);
+        return;
+    }
     if (S.lazy) {
         for (int g = 0; g < S.nlb; g++) S.lb[row * S.nlb + g] = __fadd_rd(v, S.dgcum[g]);
         S.glb[row] = __fadd_rd(v, S.scal[4]);

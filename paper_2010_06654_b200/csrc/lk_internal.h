@@ -58,6 +58,12 @@ lk_status launch_assign_tc_centered(const lk::DevState& S, const int32_t* rowlis
                                     bool counts_are_local, int sms, cudaStream_t st);
 lk_status launch_collect_tc(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
                             cudaStream_t st);
+// block-sparse Yinyang on the tensor cores (group tiles, d <= 32): the bound
+// filter (lk_tgy.cu) and the sorted, masked tcgen05 pass over its worklist
+lk_status launch_filter_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
+lk_status launch_sort_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
+lk_status launch_assign_tgy(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
+                            cudaStream_t st);
 lk_status launch_assign_tc(const lk::DevState& S, const int32_t* rowlist,
                            const int64_t* rowcount, int64_t* stat, int64_t max_rows, int sms,
                            cudaStream_t st);

@@ -779,6 +779,7 @@ __device__ __forceinline__ void update_centroid_warp(const DevState& S, int j, c
     // (body indented one level less than its scope, to keep the diff small)
     int64_t cnt = S.counts[j] + dN[j];
     int64_t qs = S.qsum[j] + dQ[j];
+    const int64_t cj = S.colperm ? S.ginv[j] : j;  // B-operand column of centroid j
     double s2 = 0.0, drift2 = 0.0, cn2 = 0.0, c2 = 0.0;
     for (int z = lane; z < S.d; z += 32) {
         int64_t sv = S.sums[(int64_t)j * S.d + z] + dS[(int64_t)j * S.d + z];
@@ -801,8 +802,8 @@ __device__ __forceinline__ void update_centroid_warp(const DevState& S, int j, c
         cn2 = fma((double)c32, (double)c32, cn2);
         if (S.Chi) {
             float hi = tf32_trunc(c32);
-            S.Chi[(int64_t)j * S.ldc + z] = hi;
-            S.Clo[(int64_t)j * S.ldc + z] = c32 - hi;
+            S.Chi[cj * S.ldc + z] = hi;
+            S.Clo[cj * S.ldc + z] = c32 - hi;
             c2 = fma(c, c, c2);
         }
     }
@@ -813,7 +814,7 @@ __device__ __forceinline__ void update_centroid_warp(const DevState& S, int j, c
         c2 += __shfl_xor_sync(LK_FULL_MASK, c2, o);
     }
     if (lane == 0) {
-        if (S.cn2) S.cn2[j] = (float)c2;
+        if (S.cn2) S.cn2[cj] = (float)c2;
         S.counts[j] = cnt;
         S.qsum[j] = qs;
         const float dj = drift2 > 0.0 ? __double2float_ru(sqrt(drift2) * (1.0 + 1e-12)) : 0.f;

@@ -273,6 +273,13 @@ __device__ __forceinline__ void dp2s(float v0, float v1, float c0, float c1, flo
     upk2(r, d0, d1);
 }
 
+// Centroid id of B-operand column c (-1: padding).  Columns are centroid ids
+// except on the group-tile path, where they are in group order (S.colperm).
+__device__ __forceinline__ int col_id(const DevState& S, int c) {
+    if (S.colperm) return c < S.kpad ? __ldg(S.colperm + c) : -1;
+    return c < S.k ? c : -1;
+}
+
 // ---- certification (D-space error bound) ------------------------------------
 
 // |D_true - D~| <= kappa * |x| |c| + 8u (|x|^2 + |c|^2) for the 3xTF32 form;
@@ -678,11 +685,11 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                     }
                     if (valid) {
                         for (unsigned m = hit0; m; m &= m - 1) {
-                            if (cnt < cap) slots[cnt] = jb + __ffs(m) - 1;
+                            if (cnt < cap) slots[cnt] = col_id(S, jb + __ffs(m) - 1);
                             cnt++;
                         }
                         for (unsigned m = hit1; m; m &= m - 1) {
-                            if (cnt < cap) slots[cnt] = jb + 32 + __ffs(m) - 1;
+                            if (cnt < cap) slots[cnt] = col_id(S, jb + 32 + __ffs(m) - 1);
                             cnt++;
                         }
                     }
@@ -822,7 +829,7 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                                 else b2 = fminf(b2, dp);
                             } else {
                                 if (valid && dp <= thr) {
-                                    if (cnt < cap) slots[cnt] = jb + c4 * 4 + e;
+                                    if (cnt < cap) slots[cnt] = col_id(S, jb + c4 * 4 + e);
                                     cnt++;
                                 }
                             }
@@ -895,6 +902,7 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
             int old = 0;
             float thr_out = 0.f, lb_out = 0.f;
             if (valid) {
+                if (S.colperm && j1 >= 0) j1 = col_id(S, j1);  // (a column of the group tiles)
                 row = A.rowlist ? (int64_t)A.rowlist[r] : r;
                 const float xn2 = A.center ? S.rowxn2[r] : S.xn2[row];  // (contiguous copy when gathered)
                 const float xn = sqrtf(xn2) * (1.0f + 2 * kU32);
@@ -1323,7 +1331,7 @@ __global__ void __launch_bounds__(320, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(bempty);  // this warp is done with the pair's beta rows
-            const int j1 = (bj >= 0 && bv == b1) ? bj : -1;
+            const int j1 = (bj >= 0 && bv == b1) ? col_id(S, bj) : -1;
             int64_t row = 0;
             bool moved = false, amb = false;
             int old = 0;
@@ -1343,6 +1351,396 @@ __global__ void __launch_bounds__(320, 1)
     if (warp == MW) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+// ---- Yinyang on the tensor cores: block-sparse (row-tile pair x group tile) --
+//
+// Reference: Yinyang.assign_pass (pruners.py:438-497) -- the global gate, the
+// per-group scans against the running best, the group-bound rewrite and the
+// old-group fix-up -- for d <= 32 on the k_assign_tc2 pipeline.  The B operand
+// holds the centroids in group order (column 128 g + member rank: group g is
+// centroid tile g, S.colperm maps columns back to ids).  k_filter_tgy lists the
+// rows whose bounds fail together with their failing groups plus the group of
+// their label; the rows are label-sorted into 256-row pairs and a pair runs
+// only the centroid tiles in the union of its rows' masks (pmask).
+//
+// The epilogue keeps each row's top-2 over the scanned tiles and every scanned
+// tile's minimum.  A row is certified iff the winner's upper bound is below the
+// second-best's lower bound AND below the lower bound of every unscanned group
+// (rowlun); it then rewrites ub, the global bound and each scanned group's
+// bound (lazy encoding).  Ambiguous rows take the collect pass
+// over all k and the exact fp64 recheck, as on the full path.
+
+// Certified lower bound (distance) on every column whose TC value D'~ >= v, for
+// a centered row (R, |x'| = xo): the L2 expression of tc_certify evaluated at
+// v, with the square root rounded down.
+__device__ __forceinline__ float tgy_lower(double R, double xo, double kx_cmax, double gb, double cmax,
+                                           float v) {
+    if (isinf(v)) return INFINITY;
+    const double av = fabs((double)v);
+    const double eo = kx_cmax + gb * (av + 2.0 * xo * cmax) + 2.0 * 5.9604644775390625e-08 * av;
+    const float sr = __fsqrt_ru(__double2float_ru(fmax(R + (double)v + eo, 0.0)));
+    const double ex = 2.384185791015625e-07 * xo * ((double)sr + xo);
+    const double L = (R + (double)v - eo - ex) - fabs(R) * 1e-12;
+    return __fsqrt_rd(__double2float_rd(fmax(L, 0.0)));
+}
+
+__global__ void __launch_bounds__(320, 1)
+    k_assign_tgy(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                 DevState S, TcArgs A, int64_t* stat) {
+    if (*S.done) return;
+    using SM = Tc2Smem;
+    constexpr int BN = 128, NBUF = 2, PW = 8, MW = 9, GS = 257;  // GS: group-minimum row stride
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* abuf = smem + SM::A_OFF;
+    uint64_t* full = (uint64_t*)(smem + SM::BAR_OFF);
+    uint64_t* empty = full + SM::STAGES;
+    uint64_t* tfull = empty + SM::STAGES;
+    uint64_t* tempty = tfull + NBUF;
+    uint64_t* afull = tempty + NBUF;
+    uint64_t* aempty = afull + 1;
+    uint64_t* bfull = aempty + 1;
+    uint64_t* bempty = bfull + 1;
+    uint32_t* tmem_slot = (uint32_t*)(bempty + 1);
+    float* sbeta = (float*)(smem + SM::BETA_OFF);  // [2][kpad]
+    float* sgm = sbeta + 2 * S.kpad;                // [G][GS]: per group, the pair's 256 rows
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t m = *A.rowcount;
+    const int64_t n_rt = (m + BM - 1) / BM;
+    const int64_t n_rp = (n_rt + 1) / 2;
+    auto beta_of = [&](int64_t t_) -> const float* {
+        if (t_ >= n_rt) return S.cn2;
+        const int at = S.tile_lab[t_];
+        return at >= 0 ? S.ptab + (int64_t)at * S.kpad : S.cn2;
+    };
+    const int n_it = (int)(n_rp > (int64_t)blockIdx.x ? (n_rp - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < SM::STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < NBUF; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 8);
+        }
+        mbar_init(afull, 1);
+        mbar_init(aempty, 1);
+        mbar_init(bfull, 1);
+        mbar_init(bempty, 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_map(&map_ahi);
+        prefetch_map(&map_alo);
+        prefetch_map(&map_bhi);
+        prefetch_map(&map_blo);
+    }
+    if (warp == MW) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == PW) {
+        // ===== TMA producer: per pair, the A tiles, then only the masked centroid tiles
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int it = 0; it < n_it; it++) {
+                const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
+                const uint32_t pm = __ldg(S.pmask + rp);
+                mbar_wait(bempty, (it & 1) ^ 1);
+                mbar_expect_tx(bfull, (uint32_t)S.kpad * 8);
+                bulk_load(sbeta, beta_of(2 * rp), (uint32_t)S.kpad * 4, bfull);
+                bulk_load(sbeta + S.kpad, beta_of(2 * rp + 1), (uint32_t)S.kpad * 4, bfull);
+                mbar_wait(aempty, (it & 1) ^ 1);
+                mbar_expect_tx(afull, 4 * SM::A_BYTES);
+#pragma unroll
+                for (int s = 0; s < 2; s++) {
+                    const int row0 = (int)((2 * rp + s) * BM);
+                    tma_load_2d(&map_ahi, afull, abuf + s * 2 * SM::A_BYTES, 0, row0);
+                    tma_load_2d(&map_alo, afull, abuf + s * 2 * SM::A_BYTES + SM::A_BYTES, 0, row0);
+                }
+                for (uint32_t mm = pm; mm; mm &= mm - 1) {
+                    const int ct = __ffs(mm) - 1;
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* bst = smem + stage * SM::STAGE_BYTES;
+                    mbar_expect_tx(&full[stage], SM::STAGE_BYTES);
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        uint8_t* dst = bst + (q >> 1) * SM::B_BYTES + (q & 1) * (SM::B_BYTES / 2);
+                        tma_load_2d((q >> 1) ? &map_blo : &map_bhi, &full[stage], dst, 0,
+                                    ct * BN + (q & 1) * (BN / 2));
+                    }
+                    if (++stage == SM::STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == MW) {
+        // ===== MMA issuer (ordered single accumulator, as k_assign_tc2) =====
+        constexpr uint32_t idesc = idesc_tf32(BM, BN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        int64_t n_dist = 0;
+        for (int it = 0; it < n_it; it++) {
+            const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
+            const uint32_t pm = __ldg(S.pmask + rp);
+            const int64_t rows = m - 2 * rp * BM < 2 * BM ? m - 2 * rp * BM : 2 * BM;
+            n_dist += rows * 128 * __popc(pm);
+            mbar_wait(afull, it & 1);
+            tc_fence_after();
+            for (uint32_t mm = pm; mm; mm &= mm - 1) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                uint8_t* bst = smem + stage * SM::STAGE_BYTES;
+                const uint64_t dbhi = umma_desc(bst);
+                const uint64_t dblo = umma_desc(bst + SM::B_BYTES);
+#pragma unroll
+                for (int s = 0; s < 2; s++) {
+                    const uint32_t tmem_d = tmem_base + acc * 2 * BN + s * BN;
+                    const uint64_t dahi = umma_desc(abuf + s * 2 * SM::A_BYTES);
+                    const uint64_t dalo = umma_desc(abuf + s * 2 * SM::A_BYTES + SM::A_BYTES);
+#pragma unroll
+                    for (int k = 0; k < KC / UK; k++) {
+                        const uint64_t off = (uint64_t)((k * UK * 4) >> 4);
+                        mma_tf32(tmem_d, dalo + off, dbhi + off, idesc, k != 0);
+                        mma_tf32(tmem_d, dahi + off, dblo + off, idesc, 1);
+                    }
+#pragma unroll
+                    for (int k = 0; k < KC / UK; k++) {
+                        const uint64_t off = (uint64_t)((k * UK * 4) >> 4);
+                        mma_tf32(tmem_d, dahi + off, dbhi + off, idesc, 1);
+                    }
+                }
+                mma_commit(&empty[stage]);
+                if (++stage == SM::STAGES) { stage = 0; phase ^= 1; }
+                mma_commit(&tfull[acc]);
+                if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+            }
+            mma_commit(aempty);
+        }
+        if (lane == 0 && n_dist) atomicAdd((unsigned long long*)(stat + LK_STAT_DIST), (unsigned long long)n_dist);
+    } else {
+        // ===== epilogue: warp w = rows 32 (w % 4) .. of row tile w / 4 =====
+        const int q = warp & 3, s = warp >> 2;
+        const float kappa = tc_kappa_ordered(S.d);
+        const int G = S.t_groups;
+        const float dm = S.scal[4];
+        const float cmax_f = S.scal[0];
+        __shared__ unsigned long long escr[9];
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        const int rloc0 = s * BM + q * 32;   // this warp's first row in the pair
+        const int rloc = rloc0 + lane;
+        auto load_bv = [&](int it_) -> float {
+            if (it_ >= n_it) return INFINITY;
+            const int64_t r_ = (2 * (blockIdx.x + (int64_t)it_ * gridDim.x) + s) * BM + q * 32 + lane;
+            return r_ < m ? __ldcs(S.rowbv + r_) : INFINITY;
+        };
+        float bv_next = load_bv(0);
+        for (int it = 0; it < n_it; it++) {
+            const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
+            const uint32_t pm = __ldg(S.pmask + rp);
+            const int64_t rt = 2 * rp + s;
+            const int64_t r = rt * BM + q * 32 + lane;
+            const bool valid = r < m;
+            float b1 = INFINITY, b2 = INFINITY, bv = bv_next;
+            int bj = -1;
+            bv_next = load_bv(it + 1);
+            mbar_wait(bfull, it & 1);
+            const uint32_t sb0 = smem_u32(sbeta + s * S.kpad);
+            for (uint32_t mm = pm; mm; mm &= mm - 1) {
+                const int ct = __ffs(mm) - 1;
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 2 * BN + s * BN;
+                float gmin = INFINITY;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 64) {
+                    uint32_t r0[32], r1[32];
+                    tmem_ld32_async(taddr + c0, r0);
+                    tmem_ld32_async(taddr + c0 + 32, r1);
+                    const int jb = ct * BN + c0;
+                    const uint32_t sb = sb0 + 4 * jb;
+                    float4 cv[16];
+#pragma unroll
+                    for (int c4 = 0; c4 < 16; c4++)
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(cv[c4].x), "=f"(cv[c4].y), "=f"(cv[c4].z), "=f"(cv[c4].w)
+                                     : "r"(sb + 16 * c4));
+                    tmem_wait_ld();
+                    float dv[64];
+#pragma unroll
+                    for (int c4 = 0; c4 < 16; c4++) {
+                        const float cc[4] = {cv[c4].x, cv[c4].y, cv[c4].z, cv[c4].w};
+#pragma unroll
+                        for (int e = 0; e < 4; e += 2) {
+                            const int col = c4 * 4 + e;
+                            const float v0 = __uint_as_float(col < 32 ? r0[col & 31] : r1[col & 31]);
+                            const float v1 = __uint_as_float(col < 32 ? r0[(col + 1) & 31] : r1[(col + 1) & 31]);
+                            dp2s(v0, v1, cc[e], cc[e + 1], dv[col], dv[col + 1]);
+                        }
+                    }
+                    float m21[22];
+#pragma unroll
+                    for (int i = 0; i < 21; i++) m21[i] = fmin3(dv[3 * i], dv[3 * i + 1], dv[3 * i + 2]);
+                    m21[21] = dv[63];
+                    float m8[8];
+#pragma unroll
+                    for (int i = 0; i < 7; i++) m8[i] = fmin3(m21[3 * i], m21[3 * i + 1], m21[3 * i + 2]);
+                    m8[7] = m21[21];
+                    const float mc = fmin3(fmin3(m8[0], m8[1], m8[2]), fmin3(m8[3], m8[4], m8[5]),
+                                           fminf(m8[6], m8[7]));
+                    gmin = fminf(gmin, mc);
+                    if (__any_sync(LK_FULL_MASK, mc < b2)) {
+                        float a1 = b1, a2 = b2, e1 = INFINITY, e2 = INFINITY;
+#pragma unroll
+                        for (int pp = 0; pp < 32; pp += 2) {
+                            const float lo0 = fminf(dv[2 * pp], dv[2 * pp + 1]);
+                            const float hi0 = fmaxf(dv[2 * pp], dv[2 * pp + 1]);
+                            a2 = fmin3(fmaxf(a1, lo0), a2, hi0);
+                            a1 = fminf(a1, lo0);
+                            const float lo1 = fminf(dv[2 * pp + 2], dv[2 * pp + 3]);
+                            const float hi1 = fmaxf(dv[2 * pp + 2], dv[2 * pp + 3]);
+                            e2 = fmin3(fmaxf(e1, lo1), e2, hi1);
+                            e1 = fminf(e1, lo1);
+                        }
+                        b2 = fmin3(fmaxf(a1, e1), a2, e2);
+                        b1 = fminf(a1, e1);
+                        const bool imp = b1 < bv;
+                        if (__any_sync(LK_FULL_MASK, imp)) {
+                            int found = -1;
+#pragma unroll
+                            for (int e = 63; e >= 0; e--)
+                                if (dv[e] == b1) found = jb + e;
+                            if (imp) {
+                                bv = b1;
+                                bj = found;
+                            }
+                        }
+                    }
+                }
+                sgm[ct * GS + rloc] = gmin;  // the group's minimum D'~ (raw)
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bempty);
+            const int j1 = (bj >= 0 && bv == b1) ? col_id(S, bj) : -1;
+            int64_t row = 0;
+            bool moved = false, amb = false, cert = false;
+            int old = 0;
+            float thr_out = 0.f, lb_out = 0.f;
+            if (valid) {
+                row = S.perm[r];
+                const double R = S.rowR[r];
+                const double xo = (double)S.rowxo[r];
+                const double cmax = (double)cmax_f;
+                const double cn1 = j1 >= 0 ? (double)S.cnorm[j1] : cmax;
+                const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
+                const double ab1 = fabs((double)b1);
+                const double e1 = (double)kappa * xo * cn1 + gb * (ab1 + 2.0 * xo * cn1) +
+                                  2.0 * 5.9604644775390625e-08 * ab1;
+                const float sr1 = __fsqrt_ru(__double2float_ru(fmax(R + (double)b1 + e1, 0.0)));
+                const double ex1 = 2.384185791015625e-07 * xo * ((double)sr1 + xo);
+                const double U = (R + (double)b1 + e1 + ex1) * (1.0 + 1e-12) + 1e-300;
+                const float Ud = __fsqrt_ru(__double2float_ru(fmax(U, 0.0)));
+                const double kxc = (double)kappa * xo * cmax;
+                const float L2d = tgy_lower(R, xo, kxc, gb, cmax, b2);
+                const float lun = S.rowlun[r];
+                // the winner beats every other scanned column and every unscanned group
+                cert = j1 >= 0 && L2d > Ud && lun > Ud && !isinf(b1);
+                if (cert) {
+                    old = S.rowlab[r];
+                    moved = old != j1;
+                    if (moved) S.labels[row] = j1;
+                    S.ub[row] = __fsub_ru(Ud, S.dcum[j1]);
+                    S.glb[row] = __fadd_rd(fminf(L2d, lun), dm);
+                    const int g1 = S.group_of[j1];
+                    // every scanned group's bound: its minimum, the winner's group
+                    // the second best (its other members); lazy encoding
+                    for (uint32_t mm = pm; mm; mm &= mm - 1) {
+                        const int g = __ffs(mm) - 1;
+                        const float v = g == g1 ? L2d : tgy_lower(R, xo, kxc, gb, cmax, sgm[g * GS + rloc]);
+                        sgm[g * GS + rloc] = __fadd_rd(v, S.dgcum[g]);
+                    }
+                } else {
+                    amb = true;
+                    // every scanned group's minimum bounds all its members,
+                    // whichever one the re-decision picks
+                    for (uint32_t mm = pm; mm; mm &= mm - 1) {
+                        const int g = __ffs(mm) - 1;
+                        const float v = tgy_lower(R, xo, kxc, gb, cmax, sgm[g * GS + rloc]);
+                        sgm[g * GS + rloc] = __fadd_rd(v, S.dgcum[g]);
+                    }
+                    const float xn2 = S.rowxn2[r];
+                    const double xn = (double)(sqrtf(xn2) * (1.0f + 2 * kU32));
+                    const double eunc = (double)kappa * xn * cmax + 8.0 * 5.9604644775390625e-08 *
+                                        ((double)xn2 + cmax * cmax);
+                    const double thr = (U - (double)xn2 * (1.0 - 2.384185791015625e-07) + eunc) *
+                                       (1.0 + 1e-9) + 1e-30;
+                    thr_out = __double2float_ru(thr);
+                    lb_out = __double2float_rd(sqrt(fmax(U, 0.0)) * (1.0 - 1e-12));
+                }
+            }
+            // scanned group bounds of the certified rows: one coalesced row segment
+            // per row (lane g writes group g)
+            __syncwarp();
+            const unsigned wm = __ballot_sync(LK_FULL_MASK, cert || amb);
+            for (unsigned mm = wm; mm; mm &= mm - 1) {
+                const int i = __ffs(mm) - 1;
+                const int64_t row_i = __shfl_sync(LK_FULL_MASK, row, i);
+                if (lane < G && ((pm >> lane) & 1u)) S.lb[row_i * S.nlb + lane] = sgm[lane * GS + rloc0 + i];
+            }
+            __syncwarp();
+            int64_t pos = epi_append8(moved, (unsigned long long*)(stat + LK_STAT_CHANGED), escr, warp);
+            if (moved) S.moved[pos] = make_int2((int)row, old);
+            int64_t cpos = epi_append8(amb, (unsigned long long*)(stat + LK_STAT_CANDIDATE), escr, warp);
+            if (amb) {
+                S.cand_rows[cpos] = (int)row;
+                S.cand_thr[cpos] = thr_out;
+                S.cand_lb[cpos] = lb_out;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == MW) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+// Union of the group masks of each 256-row pair of the sorted worklist (one
+// warp per pair).
+__global__ void k_pair_mask(DevState S, const int64_t* count) {
+    if (*S.done) return;
+    const int64_t m = *count;
+    const int64_t np = (m + 255) / 256;
+    const int lane = threadIdx.x & 31;
+    for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < np;
+         p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            const int64_t pos = p * 256 + e * 32 + lane;
+            if (pos < m) v |= __ldcs(S.rowmask + pos);
+        }
+        v = __reduce_or_sync(LK_FULL_MASK, v);
+        if (lane == 0) S.pmask[p] = v;
     }
 }
 
@@ -1416,7 +1814,8 @@ __global__ void __launch_bounds__(256) k_pair_table(DevState S) {
         for (int e = threadIdx.x; e < T * 32; e += 256) {
             const int r = e / 32, z = e % 32, zz = z0 + z;
             ta[z][r] = (a0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(a0 + r) * S.ldc + zz] : 0.f;
-            tb[z][r] = (j0 + r < S.k && zz < S.d) ? S.C32[(int64_t)(j0 + r) * S.ldc + zz] : 0.f;
+            const int jb = col_id(S, j0 + r);
+            tb[z][r] = (jb >= 0 && zz < S.d) ? S.C32[(int64_t)jb * S.ldc + zz] : 0.f;
         }
         __syncthreads();
         const int zn = min(32, S.d - z0);
@@ -1437,26 +1836,33 @@ __global__ void __launch_bounds__(256) k_pair_table(DevState S) {
 #pragma unroll
         for (int v = 0; v < P; v++) {
             const int j = j0 + tx + 16 * v;
-            if (j < S.kpad) S.ptab[(int64_t)a * S.kpad + j] = j < S.k ? acc[u][v] : INFINITY;
+            if (j < S.kpad) S.ptab[(int64_t)a * S.kpad + j] = col_id(S, j) >= 0 ? acc[u][v] : INFINITY;
         }
     }
 }
 
 // Per-label histogram of a row list (rowlist == nullptr: the label counts of
 // the last refinement are used instead).
+// Sort key of a label: the label itself, or on the group-tile path its B
+// column (labels of one group adjacent, so a pair spanning several labels
+// mostly stays inside one group tile).
+__device__ __forceinline__ int sort_key(const DevState& S, int lab) {
+    return S.colperm ? __ldg(S.ginv + lab) : lab;
+}
+
 __global__ void k_label_count(DevState S, const int32_t* rowlist, const int64_t* count) {
     if (*S.done) return;
     const int64_t m = count ? *count : S.n;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
          p += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(S.lcur + S.labels[rowlist ? rowlist[p] : p], 1);
+        atomicAdd(S.lcur + sort_key(S, S.labels[rowlist ? rowlist[p] : p]), 1);
 }
 
 // lcur := exclusive prefix of the histogram (from lcur, or from S.counts).
 __global__ void __launch_bounds__(1024) k_label_scan(DevState S, int from_counts) {
     if (*S.done) return;
     __shared__ int part[1024];
-    const int k = S.k, per = (k + 1023) / 1024;
+    const int k = from_counts ? S.k : S.kcols, per = (k + 1023) / 1024;
     const int b = threadIdx.x * per;
     int sum = 0;
     for (int j = b; j < b + per && j < k; j++) sum += from_counts ? (int)S.counts[j] : S.lcur[j];
@@ -1485,10 +1891,15 @@ __global__ void k_label_scatter(DevState S, const int32_t* rowlist, const int64_
          p += (int64_t)gridDim.x * blockDim.x) {
         const int row = rowlist ? rowlist[p] : (int)p;
         const int lab = S.labels[row];
-        const int pos = atomicAdd(S.lcur + lab, 1);
+        const int pos = atomicAdd(S.lcur + sort_key(S, lab), 1);
         S.perm[pos] = row;
         // per sorted position: the row's label, and each tile's (first row's) label
         S.rowlab[pos] = lab;
+        if (S.tgy && rowlist) {
+            // group-tile Yinyang: the row's group mask and unscanned-group bound
+            S.rowmask[pos] = S.ymask[p];
+            S.rowlun[pos] = S.ylun[p].x;
+        }
         if ((pos & 127) == 0) S.tile_lab[pos >> 7] = lab;
     }
 }
@@ -1638,6 +2049,10 @@ static int env_int(const char* name, int dflt) {
 
 static int g_tc_max_dyn = 0;  // dynamic smem limit of the split kernels (device opt-in max)
 static int tc_max_dyn_smem() { return g_tc_max_dyn; }
+static int g_tgy_max_dyn = 0;
+static int tc_max_dyn_smem_tgy() { return g_tgy_max_dyn; }
+// k_assign_tgy: the k_assign_tc2 layout + the pair's per-group minima
+static int tgy_smem(const DevState& S) { return Tc2Smem::TOTAL + 8 * S.kpad + S.t_groups * 257 * 4; }
 
 template <int BN, int MODE, bool SPLIT, bool ARES, int CL = 1>
 static lk_status tc_attr(int optin) {
@@ -1677,6 +2092,11 @@ lk_status init_tc_attributes() {
     if (s == LK_OK) {
         LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            optin - 1024));
+        cudaFuncAttributes fa;
+        LK_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_assign_tgy));
+        g_tgy_max_dyn = optin - (int)fa.sharedSizeBytes;
+        LK_CUDA_CHECK(cudaFuncSetAttribute(k_assign_tgy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           g_tgy_max_dyn));
     }
     if (s == LK_OK) s = tc_attr<128, kTop2, true, true, 2>(optin);
     if (s == LK_OK) s = tc_attr<128, kCollect, true, true, 2>(optin);
@@ -1707,13 +2127,13 @@ static lk_status launch_bn(const DevState& S, const float* ahi, const float* alo
                            TcArgs A, int64_t max_rows, int64_t* stat, int sms, cudaStream_t st) {
     CUtensorMap mah, mal, mbh, mbl;
     if (!make_map(&mah, ahi, a_rows, S.d, S.ldx, BM) || !make_map(&mal, alo, a_rows, S.d, S.ldx, BM) ||
-        !make_map(&mbh, S.Chi, S.k, S.d, S.ldc, ARES ? BN / 2 : BN) ||
-        !make_map(&mbl, S.Clo, S.k, S.d, S.ldc, ARES ? BN / 2 : BN)) {
+        !make_map(&mbh, S.Chi, S.kcols, S.d, S.ldc, ARES ? BN / 2 : BN) ||
+        !make_map(&mbl, S.Clo, S.kcols, S.d, S.ldc, ARES ? BN / 2 : BN)) {
         set_error("cuTensorMapEncodeTiled failed");
         return LK_ERR_CUDA;
     }
     A.m = max_rows;
-    A.n_ct = (S.k + BN - 1) / BN;
+    A.n_ct = (S.kcols + BN - 1) / BN;
     static const int knob_fast = env_int("LK_TC_FAST", 1), knob_spin = env_int("LK_TC_SPIN", 0);
     A.fast = knob_fast;
     A.spin = knob_spin;
@@ -1763,12 +2183,12 @@ static lk_status launch_tc2(const DevState& S, const float* ahi, const float* al
                             int64_t max_rows, int64_t* stat, int sms, cudaStream_t st) {
     CUtensorMap mah, mal, mbh, mbl;
     if (!make_map(&mah, ahi, S.n, S.d, S.ldx, BM) || !make_map(&mal, alo, S.n, S.d, S.ldx, BM) ||
-        !make_map(&mbh, S.Chi, S.k, S.d, S.ldc, 64) || !make_map(&mbl, S.Clo, S.k, S.d, S.ldc, 64)) {
+        !make_map(&mbh, S.Chi, S.kcols, S.d, S.ldc, 64) || !make_map(&mbl, S.Clo, S.kcols, S.d, S.ldc, 64)) {
         set_error("cuTensorMapEncodeTiled failed");
         return LK_ERR_CUDA;
     }
     A.m = max_rows;
-    A.n_ct = (S.k + 127) / 128;
+    A.n_ct = (S.kcols + 127) / 128;
     A.n_kc = 1;
     A.sbeta = 0;
     const int64_t pairs = ((max_rows + BM - 1) / BM + 1) / 2;
@@ -1842,7 +2262,7 @@ lk_status launch_assign_tc_centered(const DevState& S, const int32_t* rowlist,
         k_label_scan<<<1, 1024, 0, st>>>(S, 1);  // the label counts are the histogram
         LK_LAUNCH_CHECK();
     } else {
-        LK_CUDA_CHECK(cudaMemsetAsync(S.lcur, 0, (size_t)(S.k + 1) * 4, st));
+        LK_CUDA_CHECK(cudaMemsetAsync(S.lcur, 0, (size_t)(S.kcols + 1) * 4, st));
         // (every local row of a shard: its counts are global, histogram the labels)
         k_label_count<<<grid, 256, 0, st>>>(S, rowlist, rowcount);
         LK_LAUNCH_CHECK();
@@ -1861,6 +2281,54 @@ lk_status launch_assign_tc_centered(const DevState& S, const int32_t* rowlist,
     A.center = 1;
     A.sbeta = 1;  // (dropped by launch_mode when the double buffer does not fit)
     return launch_mode<kTop2>(S, S.Xg_hi, S.Xg_lo, A, max_rows, stat, sms, st);
+}
+
+// Block-sparse Yinyang pass over the filter's worklist (stat[LK_STAT_WORK]
+// rows, masks in S.ymask): label sort, pair masks, centered gather, then the
+// (row-tile pair x group tile) MMAs of k_assign_tgy.
+lk_status launch_sort_tgy(const DevState& S, int64_t* stat, int sms, cudaStream_t st) {
+    const int64_t* count = stat + LK_STAT_WORK;
+    const int grid = sms * 8;
+    LK_CUDA_CHECK(cudaMemsetAsync(S.lcur, 0, (size_t)(S.kcols + 1) * 4, st));
+    k_label_count<<<grid, 256, 0, st>>>(S, S.work, count);
+    LK_LAUNCH_CHECK();
+    k_label_scan<<<1, 1024, 0, st>>>(S, 0);
+    LK_LAUNCH_CHECK();
+    k_label_scatter<<<grid, 256, 0, st>>>(S, S.work, count);
+    LK_LAUNCH_CHECK();
+    k_pair_mask<<<sms * 4, 256, 0, st>>>(S, count);
+    LK_LAUNCH_CHECK();
+    int L = 1;
+    while (L < 32 && L * 2 <= S.ldx / 4) L *= 2;
+    k_gather_center<<<sms * 8, 256, 0, st>>>(S, count, L);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
+}
+
+lk_status launch_assign_tgy(const DevState& S, int64_t* stat, int64_t max_rows, int sms,
+                            cudaStream_t st) {
+    const int64_t* count = stat + LK_STAT_WORK;
+    CUtensorMap mah, mal, mbh, mbl;
+    if (!make_map(&mah, S.Xg_hi, S.n, S.d, S.ldx, BM) || !make_map(&mal, S.Xg_lo, S.n, S.d, S.ldx, BM) ||
+        !make_map(&mbh, S.Chi, S.kcols, S.d, S.ldc, 64) || !make_map(&mbl, S.Clo, S.kcols, S.d, S.ldc, 64)) {
+        set_error("cuTensorMapEncodeTiled failed");
+        return LK_ERR_CUDA;
+    }
+    TcArgs A = {};
+    A.m = max_rows;
+    A.rowcount = count;
+    A.rowlist = S.perm;
+    A.center = 1;
+    A.n_kc = 1;
+    A.n_ct = S.t_groups;
+    const int smem = tgy_smem(S);
+    if (smem > tc_max_dyn_smem_tgy()) {
+        set_error("group-tile pass: %d B of shared memory needed (k = %d)", smem, S.k);
+        return LK_ERR_UNSUPPORTED;
+    }
+    k_assign_tgy<<<sms, 320, smem, st>>>(mah, mal, mbh, mbl, S, A, stat);
+    LK_LAUNCH_CHECK();
+    return LK_OK;
 }
 
 // Second pass over the ambiguous rows: collect every centroid under the row's

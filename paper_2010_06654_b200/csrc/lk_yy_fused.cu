@@ -604,7 +604,7 @@ static lk_status launch_fused_tt(const lk::DevState& S, int64_t* stat, const dou
 
 // the fused path owns the lazy bound encoding (allocated for d <= 32, t <= 32
 // and no tensor cores)
-bool yy_fused_ok(const lk::DevState& S) { return S.lazy != 0; }
+bool yy_fused_ok(const lk::DevState& S) { return S.lazy != 0 && !S.tgy; }
 
 template <int DP, int T>
 static lk_status fused_attr_dp() {

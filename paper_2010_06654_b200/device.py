@@ -41,16 +41,21 @@ GROUP_STRATEGIES = ("yinyang", "elkan", "regroup")
 _GROUP_CACHE: dict = {}
 
 
-def group_centroids(centers: np.ndarray, t: int, seed: int = 0, n_iters: int = 5) -> np.ndarray:
+def group_centroids(centers: np.ndarray, t: int, seed: int = 0, n_iters: int = 5,
+                    capacity: int = 0) -> np.ndarray:
     """Partition k centroids into t groups by a few Lloyd passes over the
     centroids (the idea of bounds.py:175-196; any grouping yields the same
-    labels, it only changes how much the group bounds prune).  The last
-    result is cached (a pure function of the centroids, t and the seed)."""
-    key = (hash(centers.tobytes()), centers.shape, t, seed, n_iters)
+    labels, it only changes how much the group bounds prune).  capacity > 0
+    caps every group's size (the tensor-core group tiles hold 128 centroids).
+    The last result is cached (a pure function of the arguments)."""
+    key = (hash(centers.tobytes()), centers.shape, t, seed, n_iters, capacity)
     hit = _GROUP_CACHE.get("key")
     if hit == key:
         return _GROUP_CACHE["groups"].copy()
-    g = _group_centroids(centers, t, seed, n_iters)
+    if capacity > 0:
+        g = _tile_groups(centers, t, capacity)
+    else:
+        g = _group_centroids(centers, t, seed, n_iters)
     _GROUP_CACHE.update(key=key, groups=g.copy())
     return g
 
@@ -75,6 +80,75 @@ def _group_centroids(centers: np.ndarray, t: int, seed: int, n_iters: int) -> np
     return g.astype(np.int32)
 
 
+def _tile_groups(centers: np.ndarray, t: int, cap: int) -> np.ndarray:
+    """Balanced, spatially compact groups of at most ``cap`` centroids: recursive
+    bisection at the (size-proportional) quantile of the projection on the
+    principal axis (a balanced PCA tree).  A k-means grouping under a size cap
+    scatters a large cluster's surplus centroids into far-away groups, which
+    then fail for every row of that cluster; bisection keeps every group a
+    compact region instead."""
+    k = centers.shape[0]
+    t = max(1, min(t, k))
+    if t * cap < k:
+        raise ValueError(f"{t} groups of at most {cap} cannot hold {k} centroids")
+    out = np.zeros(k, dtype=np.int32)
+
+    def split(idx, g0, gn):
+        if gn == 1:
+            out[idx] = g0
+            return
+        gl = gn // 2
+        gr = gn - gl
+        m = len(idx)
+        nl = int(round(m * gl / gn))
+        nl = min(max(nl, m - gr * cap), gl * cap)
+        pts = centers[idx]
+        c = pts - pts.mean(axis=0)
+        if m > 1 and np.any(c):
+            _, _, vt = np.linalg.svd(c, full_matrices=False)
+            proj = c @ vt[0]
+        else:
+            proj = np.zeros(m)
+        order = np.argsort(proj, kind="stable")
+        split(idx[order[:nl]], g0, gl)
+        split(idx[order[nl:]], g0 + gl, gr)
+
+    split(np.arange(k), 0, t)
+    return out
+
+
+def _balance_groups(centers: np.ndarray, g: np.ndarray, t: int, cap: int, rounds: int = 3):
+    """Capacity-constrained regrouping: (centroid, group) pairs in increasing
+    distance to the group means, each centroid to the nearest group with room;
+    the means are recomputed and the assignment repeated a few times."""
+    k = centers.shape[0]
+    t = max(1, min(t, k))
+    if t * cap < k:
+        raise ValueError(f"{t} groups of at most {cap} cannot hold {k} centroids")
+    cn = np.sum(centers * centers, axis=1)
+    for _ in range(rounds):
+        cnt = np.bincount(g, minlength=t)
+        means = np.zeros((t, centers.shape[1]))
+        np.add.at(means, g, centers)
+        nz = cnt > 0
+        means[nz] /= cnt[nz, None]
+        d2 = cn[:, None] - 2.0 * centers @ means.T + np.sum(means * means, axis=1)[None, :]
+        order = np.argsort(d2, axis=None, kind="stable").tolist()
+        out = [-1] * k
+        room = [cap] * t
+        left = k
+        for e in order:
+            j, q = divmod(e, t)
+            if out[j] < 0 and room[q] > 0:
+                out[j] = q
+                room[q] -= 1
+                left -= 1
+                if left == 0:
+                    break
+        g = np.asarray(out, dtype=np.int64)
+    return g.astype(np.int32)
+
+
 @dataclass
 class IterRecord:
     changed: int
@@ -86,6 +160,7 @@ class IterRecord:
     sse: float
     assign_ms: float
     update_ms: float
+    tile_mode: bool = False  # group tiles: group_dists counts every distance the pass evaluated
 
 
 class DeviceLogChunk:
@@ -240,6 +315,10 @@ class DeviceLloyd:
         nat.check(self.lib.lk_layout(h, ctypes.byref(ldx), ctypes.byref(dl), ctypes.byref(nlb)),
                   "lk_layout")
         self.ldx, self.delta_len, self.nlb = ldx.value, dl.value, nlb.value
+        gt, gc = ctypes.c_int32(), ctypes.c_int32()
+        nat.check(self.lib.lk_group_shape(h, ctypes.byref(gt), ctypes.byref(gc)), "lk_group_shape")
+        # group-tile path (capacity 128): the library fixes t = ceil(k / 128)
+        self.group_count, self.group_cap = gt.value, gc.value
 
         self.x32 = self._view("x32", torch.float32, (self.n, self.ldx))
         self.x64 = self._view("x64", torch.float64, (self.n, self.d)) if has_x64 else None
@@ -332,9 +411,13 @@ class DeviceLloyd:
     def set_centroids(self, init):
         torch = _torch()
         if self.strategy in GROUP_STRATEGIES:
-            t = min(self.groups_req, self.nlb) if self.groups_req > 0 else self.nlb
+            if self.group_cap == 128:
+                t, cap = self.group_count, self.group_cap
+            else:
+                t = min(self.groups_req, self.nlb) if self.groups_req > 0 else self.nlb
+                cap = 0
             self.set_groups(group_centroids(np.asarray(init, dtype=np.float64), t,
-                                            seed=self.group_seed))
+                                            seed=self.group_seed, capacity=cap))
         with torch.cuda.device(self.dev):
             c = torch.as_tensor(np.ascontiguousarray(init, dtype=np.float64)) \
                 if not isinstance(init, torch.Tensor) else init.to(torch.float64)
@@ -487,7 +570,8 @@ class DeviceLloyd:
                     group_dists=int(stats[t, nat.STAT["dist"]]),
                     sse=float(sse[t]),
                     assign_ms=e0.elapsed_time(e1),
-                    update_ms=e1.elapsed_time(e2)))
+                    update_ms=e1.elapsed_time(e2),
+                    tile_mode=self.group_cap == 128))
             res["iterations"] = iters
             res["converged"] = converged
             res["records"] = recs

@@ -82,7 +82,9 @@ def _iteration_stats(strategy: str, t: int, rec, n: int, k: int) -> IterationSta
             kw["bound_updates"] = 2 * n
     elif strategy in ("yinyang", "elkan"):
         # tightened rows + group scans (pruners.py:445-487 accounting)
-        dist = rec.active + rec.group_dists + rec.work * (k - 1)
+        # (group tiles: the pass counts its own (row, centroid) evaluations)
+        dist = rec.active + rec.group_dists + (0 if getattr(rec, "tile_mode", False)
+                                               else rec.work * (k - 1))
         kw["bound_dist_comps"] = k
         kw["bound_accesses"] = n
         kw["bound_updates"] = n + rec.active + 2 * rec.work

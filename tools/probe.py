@@ -49,7 +49,7 @@ def run(x, init, k, strat, kern, g, T, cfg):
     eng.profile(True)
     st = torch.cuda.current_stream()
     names = {0: "assign", 1: "filter", 2: "recheck", 3: "refine", 4: "update", 5: "gscan",
-             6: "gmerge", 7: "collect", 8: "cand", 9: "ovf"}
+             6: "gmerge", 7: "collect", 8: "cand", 9: "ovf", 10: "sort"}
     prev = {c: 0.0 for c in names}
     for t in range(1, T + 1):
         a = torch.cuda.Event(enable_timing=True)
