@@ -41,7 +41,7 @@ enum InternalBuf {
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
     B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB,
-    B_YMASK, B_ROWLUN, B_ROWMASK, B_PMASK, B_COUNT_
+    B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_COUNT_
 };
 
 struct Layout {
@@ -185,9 +185,9 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_GINV] = (uint64_t)k * 4;         // centroid -> column
         L->size[B_YLUN] = (uint64_t)n * 8;
         L->size[B_YMASK] = (uint64_t)n * 4;
-        L->size[B_ROWLUN] = (uint64_t)n * 4;
-        L->size[B_ROWMASK] = (uint64_t)n * 4;
+        L->size[B_TMETA] = (uint64_t)n * sizeof(lk::TgyMeta);
         L->size[B_PMASK] = (uint64_t)(n / 256 + 2) * 4;
+        L->size[B_SHIST] = (uint64_t)1536 * kpad * 4;  // (<= 1536 sort blocks)
         L->size[B_DCUM] = (uint64_t)k * 4;
         L->size[B_DGCUM] = (uint64_t)L->groups * 4;
         L->size[B_GLB] = (uint64_t)n * 4;
@@ -486,9 +486,9 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.kcols = S.tgy ? 128 * L.groups : cfg->k;
     S.colperm = S.tgy ? buf<int32_t>(c, B_GPERM) : nullptr;
     S.ymask = buf<uint32_t>(c, B_YMASK);
-    S.rowlun = buf<float>(c, B_ROWLUN);
-    S.rowmask = buf<uint32_t>(c, B_ROWMASK);
     S.pmask = buf<uint32_t>(c, B_PMASK);
+    S.shist = buf<int32_t>(c, B_SHIST);
+    S.tmeta = buf<lk::TgyMeta>(c, B_TMETA);
     S.hlog_inline = (S.lazy && S.hlog != nullptr && S.hlog_cap > 0) ? 1 : 0;
     {
         const char* e = getenv("LK_SGATE");  // A/B knob for the centroid-separation gate

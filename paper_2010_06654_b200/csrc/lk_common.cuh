@@ -16,6 +16,19 @@ namespace lk {
 constexpr int kWarp = 32;
 constexpr float kU32 = 5.9604644775390625e-08f;  // 2^-24, fp32 unit roundoff
 
+// Per sorted position of the group-tile worklist: everything the certification
+// of k_assign_tgy needs, in one 32-byte record (one full sector per row; the
+// sort writes it at a scattered position).
+struct __align__(16) TgyMeta {
+    double R;      // ||x'||^2 + 2 x'.o (x' = x - o, o the tile's centroid)
+    float xo;      // ||x'|| rounded up
+    float bv;      // search threshold (upper bound on the TC value of the row's label column)
+    float xn2;     // ||x||^2
+    float lun;     // lower bound over the groups the row does not scan
+    int32_t row;   // global row id
+    uint32_t mask; // the row's groups to scan
+};
+
 // Everything the hot kernels need, passed by value (fits the 4 KB param space).
 struct DevState {
     int64_t n;        // local rows
@@ -116,9 +129,9 @@ struct DevState {
     int32_t kcols;          // B-operand columns (128 * groups with the group tiles, else k)
     const int32_t* colperm; // [kpad] centroid id of each B column (-1: padding); null = identity
     uint32_t* ymask;        // [n] per worklist entry: groups the row must scan
-    float* rowlun;          // [n] per sorted position: lower bound over the unscanned groups
-    uint32_t* rowmask;      // [n] per sorted position: the row's group mask
     uint32_t* pmask;        // [n / 256 + 2] per row-tile pair: union of its rows' masks
+    int32_t* shist;         // [tgy_sort_blocks, kcols] worklist sort: per-block key counts
+    struct TgyMeta* tmeta;  // [n] per sorted position of the group-tile worklist (32 B)
     // a copy of this struct in device memory, for out-of-line device
     // functions (a reference to the kernel parameter would copy it to the stack)
     const DevState* self;
@@ -131,6 +144,9 @@ struct DevState {
 __device__ __forceinline__ float store_ub(const DevState& S, float U, int label) {
     return S.lazy ? __fsub_ru(U, S.dcum[label]) : U;
 }
+
+// Blocks of the group-tile worklist sort (lk_tc.cu k_sort_*): four per SM (one wave at 64 registers).
+inline int tgy_sort_blocks(int sms) { return 4 * (sms > 0 ? sms : 148) > 1536 ? 1536 : 4 * (sms > 0 ? sms : 148); }
 
 // numpy pairwise-sum association program passed by value (k-means++ D^2
 // updates): (0, start, len) = leaf, (1, 0, 0) = add the two top values.

@@ -1386,13 +1386,32 @@ __device__ __forceinline__ float tgy_lower(double R, double xo, double kx_cmax, 
     return __fsqrt_rd(__double2float_rd(fmax(L, 0.0)));
 }
 
+// Shared memory of k_assign_tgy: the k_assign_tc2 stages and resident A, a ring
+// of per-tile beta slices (the two row tiles' 128 offsets of the staged
+// centroid tile: the producer never waits for a whole pair's epilogue), the
+// cumulative group drifts and the pair's per-group minima.
+struct TgySmem {
+    static constexpr int B_BYTES = 128 * KC * 4;
+    static constexpr int STAGE_BYTES = 2 * B_BYTES;
+    static constexpr int STAGES = 3;
+    static constexpr int NBB = 4;                        // beta ring slots
+    static constexpr int A_BYTES = BM * KC * 4;
+    static constexpr int A_OFF = STAGES * STAGE_BYTES;
+    static constexpr int BAR_OFF = A_OFF + 4 * A_BYTES;
+    static constexpr int RING_OFF = BAR_OFF + 256;
+    static constexpr int DG_OFF = RING_OFF + NBB * 1024;
+    static constexpr int GM_OFF = DG_OFF + 32 * 4;
+    static constexpr int GS = 257;                       // per-group row stride of the minima
+    static constexpr int TOTAL = GM_OFF + 1024;          // (+ G * GS * 4 at launch)
+};
+
 __global__ void __launch_bounds__(320, 1)
     k_assign_tgy(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                  const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                  DevState S, TcArgs A, int64_t* stat) {
     if (*S.done) return;
-    using SM = Tc2Smem;
-    constexpr int BN = 128, NBUF = 2, PW = 8, MW = 9, GS = 257;  // GS: group-minimum row stride
+    using SM = TgySmem;
+    constexpr int BN = 128, NBUF = 2, PW = 8, MW = 9, GS = SM::GS, NBB = SM::NBB;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* abuf = smem + SM::A_OFF;
@@ -1402,13 +1421,15 @@ __global__ void __launch_bounds__(320, 1)
     uint64_t* tempty = tfull + NBUF;
     uint64_t* afull = tempty + NBUF;
     uint64_t* aempty = afull + 1;
-    uint64_t* bfull = aempty + 1;
-    uint64_t* bempty = bfull + 1;
-    uint32_t* tmem_slot = (uint32_t*)(bempty + 1);
-    float* sbeta = (float*)(smem + SM::BETA_OFF);  // [2][kpad]
-    float* sgm = sbeta + 2 * S.kpad;                // [G][GS]: per group, the pair's 256 rows
+    uint64_t* rfull = aempty + 1;     // [NBB] beta slices staged
+    uint64_t* rempty = rfull + NBB;   // [NBB] ... and released by the 8 epilogue warps
+    uint32_t* tmem_slot = (uint32_t*)(rempty + NBB);
+    float* ring = (float*)(smem + SM::RING_OFF);  // [NBB][2][128]
+    float* sdg = (float*)(smem + SM::DG_OFF);     // [32] cumulative group drifts
+    float* sgm = (float*)(smem + SM::GM_OFF);     // [G][GS]: per group, the pair's 256 rows
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = S.t_groups;
     const int64_t m = *A.rowcount;
     const int64_t n_rt = (m + BM - 1) / BM;
     const int64_t n_rp = (n_rt + 1) / 2;
@@ -1428,16 +1449,19 @@ __global__ void __launch_bounds__(320, 1)
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 8);
         }
+        for (int b = 0; b < NBB; b++) {
+            mbar_init(&rfull[b], 1);
+            mbar_init(&rempty[b], 8);
+        }
         mbar_init(afull, 1);
         mbar_init(aempty, 1);
-        mbar_init(bfull, 1);
-        mbar_init(bempty, 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_map(&map_ahi);
         prefetch_map(&map_alo);
         prefetch_map(&map_bhi);
         prefetch_map(&map_blo);
     }
+    if (threadIdx.x < 32) sdg[threadIdx.x] = threadIdx.x < G ? S.dgcum[threadIdx.x] : 0.f;
     if (warp == MW) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
@@ -1450,17 +1474,15 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == PW) {
-        // ===== TMA producer: per pair, the A tiles, then only the masked centroid tiles
+        // ===== TMA producer: per pair the A tiles (as soon as the previous
+        // pair's MMAs are done), then per masked centroid tile its B operand
+        // and the two row tiles' beta slices
         if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
+            int stage = 0, rs = 0;
+            uint32_t phase = 0, rphase = 0;
             for (int it = 0; it < n_it; it++) {
                 const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
                 const uint32_t pm = __ldg(S.pmask + rp);
-                mbar_wait(bempty, (it & 1) ^ 1);
-                mbar_expect_tx(bfull, (uint32_t)S.kpad * 8);
-                bulk_load(sbeta, beta_of(2 * rp), (uint32_t)S.kpad * 4, bfull);
-                bulk_load(sbeta + S.kpad, beta_of(2 * rp + 1), (uint32_t)S.kpad * 4, bfull);
                 mbar_wait(aempty, (it & 1) ^ 1);
                 mbar_expect_tx(afull, 4 * SM::A_BYTES);
 #pragma unroll
@@ -1469,6 +1491,8 @@ __global__ void __launch_bounds__(320, 1)
                     tma_load_2d(&map_ahi, afull, abuf + s * 2 * SM::A_BYTES, 0, row0);
                     tma_load_2d(&map_alo, afull, abuf + s * 2 * SM::A_BYTES + SM::A_BYTES, 0, row0);
                 }
+                const float* bt0 = beta_of(2 * rp);
+                const float* bt1 = beta_of(2 * rp + 1);
                 for (uint32_t mm = pm; mm; mm &= mm - 1) {
                     const int ct = __ffs(mm) - 1;
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -1481,6 +1505,11 @@ __global__ void __launch_bounds__(320, 1)
                                     ct * BN + (q & 1) * (BN / 2));
                     }
                     if (++stage == SM::STAGES) { stage = 0; phase ^= 1; }
+                    mbar_wait(&rempty[rs], rphase ^ 1);
+                    mbar_expect_tx(&rfull[rs], 1024);
+                    bulk_load(ring + rs * 256, bt0 + ct * BN, 512, &rfull[rs]);
+                    bulk_load(ring + rs * 256 + 128, bt1 + ct * BN, 512, &rfull[rs]);
+                    if (++rs == NBB) { rs = 0; rphase ^= 1; }
                 }
             }
         }
@@ -1536,36 +1565,46 @@ __global__ void __launch_bounds__(320, 1)
         // ===== epilogue: warp w = rows 32 (w % 4) .. of row tile w / 4 =====
         const int q = warp & 3, s = warp >> 2;
         const float kappa = tc_kappa_ordered(S.d);
-        const int G = S.t_groups;
         const float dm = S.scal[4];
         const float cmax_f = S.scal[0];
-        __shared__ unsigned long long escr[9];
-        int acc = 0;
-        uint32_t acc_phase = 0;
+        int acc = 0, rs = 0;
+        uint32_t acc_phase = 0, rphase = 0;
         const int rloc0 = s * BM + q * 32;   // this warp's first row in the pair
         const int rloc = rloc0 + lane;
-        auto load_bv = [&](int it_) -> float {
-            if (it_ >= n_it) return INFINITY;
-            const int64_t r_ = (2 * (blockIdx.x + (int64_t)it_ * gridDim.x) + s) * BM + q * 32 + lane;
-            return r_ < m ? __ldcs(S.rowbv + r_) : INFINITY;
-        };
-        float bv_next = load_bv(0);
         for (int it = 0; it < n_it; it++) {
             const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
             const uint32_t pm = __ldg(S.pmask + rp);
             const int64_t rt = 2 * rp + s;
             const int64_t r = rt * BM + q * 32 + lane;
             const bool valid = r < m;
-            float b1 = INFINITY, b2 = INFINITY, bv = bv_next;
+            float b1 = INFINITY, b2 = INFINITY, bv = INFINITY;
             int bj = -1;
-            bv_next = load_bv(it + 1);
-            mbar_wait(bfull, it & 1);
-            const uint32_t sb0 = smem_u32(sbeta + s * S.kpad);
+            // the row's certification record, loaded while the tiles stream
+            int64_t row = 0;
+            double R = 0.0, xo = 0.0;
+            float lun = 0.f, xn2 = 0.f;
+            int old = 0;
+            if (valid) {
+                const int4* src = reinterpret_cast<const int4*>(S.tmeta + r);
+                int4 w[2];
+                w[0] = __ldcs(src);
+                w[1] = __ldcs(src + 1);
+                const TgyMeta& t = *reinterpret_cast<const TgyMeta*>(w);
+                row = t.row;
+                R = t.R;
+                xo = (double)t.xo;
+                lun = t.lun;
+                xn2 = t.xn2;
+                bv = t.bv;
+                old = S.labels[row];
+            }
             for (uint32_t mm = pm; mm; mm &= mm - 1) {
                 const int ct = __ffs(mm) - 1;
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
+                mbar_wait(&rfull[rs], rphase);
                 const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 2 * BN + s * BN;
+                const uint32_t sb0 = smem_u32(ring + rs * 256 + s * 128);
                 float gmin = INFINITY;
 #pragma unroll 1
                 for (int c0 = 0; c0 < BN; c0 += 64) {
@@ -1573,7 +1612,7 @@ __global__ void __launch_bounds__(320, 1)
                     tmem_ld32_async(taddr + c0, r0);
                     tmem_ld32_async(taddr + c0 + 32, r1);
                     const int jb = ct * BN + c0;
-                    const uint32_t sb = sb0 + 4 * jb;
+                    const uint32_t sb = sb0 + 4 * c0;
                     float4 cv[16];
 #pragma unroll
                     for (int c4 = 0; c4 < 16; c4++)
@@ -1635,20 +1674,17 @@ __global__ void __launch_bounds__(320, 1)
                 sgm[ct * GS + rloc] = gmin;  // the group's minimum D'~ (raw)
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (lane == 0) {
+                    mbar_arrive(&tempty[acc]);
+                    mbar_arrive(&rempty[rs]);
+                }
                 if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+                if (++rs == NBB) { rs = 0; rphase ^= 1; }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bempty);
             const int j1 = (bj >= 0 && bv == b1) ? col_id(S, bj) : -1;
-            int64_t row = 0;
             bool moved = false, amb = false, cert = false;
-            int old = 0;
             float thr_out = 0.f, lb_out = 0.f;
             if (valid) {
-                row = S.perm[r];
-                const double R = S.rowR[r];
-                const double xo = (double)S.rowxo[r];
                 const double cmax = (double)cmax_f;
                 const double cn1 = j1 >= 0 ? (double)S.cnorm[j1] : cmax;
                 const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
@@ -1661,33 +1697,24 @@ __global__ void __launch_bounds__(320, 1)
                 const float Ud = __fsqrt_ru(__double2float_ru(fmax(U, 0.0)));
                 const double kxc = (double)kappa * xo * cmax;
                 const float L2d = tgy_lower(R, xo, kxc, gb, cmax, b2);
-                const float lun = S.rowlun[r];
                 // the winner beats every other scanned column and every unscanned group
                 cert = j1 >= 0 && L2d > Ud && lun > Ud && !isinf(b1);
+                const int g1 = cert ? S.group_of[j1] : -1;
+                // every scanned group's bound (lazy encoding): its minimum bounds
+                // all its members, whichever wins; a certified row's winner group
+                // gets the second best (its other members)
+                for (uint32_t mm = pm; mm; mm &= mm - 1) {
+                    const int g = __ffs(mm) - 1;
+                    const float v = g == g1 ? L2d : tgy_lower(R, xo, kxc, gb, cmax, sgm[g * GS + rloc]);
+                    sgm[g * GS + rloc] = __fadd_rd(v, sdg[g]);
+                }
                 if (cert) {
-                    old = S.rowlab[r];
                     moved = old != j1;
                     if (moved) S.labels[row] = j1;
                     S.ub[row] = __fsub_ru(Ud, S.dcum[j1]);
                     S.glb[row] = __fadd_rd(fminf(L2d, lun), dm);
-                    const int g1 = S.group_of[j1];
-                    // every scanned group's bound: its minimum, the winner's group
-                    // the second best (its other members); lazy encoding
-                    for (uint32_t mm = pm; mm; mm &= mm - 1) {
-                        const int g = __ffs(mm) - 1;
-                        const float v = g == g1 ? L2d : tgy_lower(R, xo, kxc, gb, cmax, sgm[g * GS + rloc]);
-                        sgm[g * GS + rloc] = __fadd_rd(v, S.dgcum[g]);
-                    }
                 } else {
                     amb = true;
-                    // every scanned group's minimum bounds all its members,
-                    // whichever one the re-decision picks
-                    for (uint32_t mm = pm; mm; mm &= mm - 1) {
-                        const int g = __ffs(mm) - 1;
-                        const float v = tgy_lower(R, xo, kxc, gb, cmax, sgm[g * GS + rloc]);
-                        sgm[g * GS + rloc] = __fadd_rd(v, S.dgcum[g]);
-                    }
-                    const float xn2 = S.rowxn2[r];
                     const double xn = (double)(sqrtf(xn2) * (1.0f + 2 * kU32));
                     const double eunc = (double)kappa * xn * cmax + 8.0 * 5.9604644775390625e-08 *
                                         ((double)xn2 + cmax * cmax);
@@ -1697,19 +1724,19 @@ __global__ void __launch_bounds__(320, 1)
                     lb_out = __double2float_rd(sqrt(fmax(U, 0.0)) * (1.0 - 1e-12));
                 }
             }
-            // scanned group bounds of the certified rows: one coalesced row segment
-            // per row (lane g writes group g)
+            // scanned group bounds: one coalesced row segment per row (lane g
+            // writes group g)
             __syncwarp();
-            const unsigned wm = __ballot_sync(LK_FULL_MASK, cert || amb);
+            const unsigned wm = __ballot_sync(LK_FULL_MASK, valid);
             for (unsigned mm = wm; mm; mm &= mm - 1) {
                 const int i = __ffs(mm) - 1;
                 const int64_t row_i = __shfl_sync(LK_FULL_MASK, row, i);
                 if (lane < G && ((pm >> lane) & 1u)) S.lb[row_i * S.nlb + lane] = sgm[lane * GS + rloc0 + i];
             }
             __syncwarp();
-            int64_t pos = epi_append8(moved, (unsigned long long*)(stat + LK_STAT_CHANGED), escr, warp);
+            const int64_t pos = warp_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED));
             if (moved) S.moved[pos] = make_int2((int)row, old);
-            int64_t cpos = epi_append8(amb, (unsigned long long*)(stat + LK_STAT_CANDIDATE), escr, warp);
+            const int64_t cpos = warp_append(amb, (unsigned long long*)(stat + LK_STAT_CANDIDATE));
             if (amb) {
                 S.cand_rows[cpos] = (int)row;
                 S.cand_thr[cpos] = thr_out;
@@ -1737,7 +1764,7 @@ __global__ void k_pair_mask(DevState S, const int64_t* count) {
 #pragma unroll
         for (int e = 0; e < 8; e++) {
             const int64_t pos = p * 256 + e * 32 + lane;
-            if (pos < m) v |= __ldcs(S.rowmask + pos);
+            if (pos < m) v |= __ldcs(&S.tmeta[pos].mask);
         }
         v = __reduce_or_sync(LK_FULL_MASK, v);
         if (lane == 0) S.pmask[p] = v;
@@ -1895,12 +1922,161 @@ __global__ void k_label_scatter(DevState S, const int32_t* rowlist, const int64_
         S.perm[pos] = row;
         // per sorted position: the row's label, and each tile's (first row's) label
         S.rowlab[pos] = lab;
-        if (S.tgy && rowlist) {
-            // group-tile Yinyang: the row's group mask and unscanned-group bound
-            S.rowmask[pos] = S.ymask[p];
-            S.rowlun[pos] = S.ylun[p].x;
-        }
         if ((pos & 127) == 0) S.tile_lab[pos >> 7] = lab;
+    }
+}
+
+// Group-tile worklist sort (counting sort by B column of the label, no global
+// atomics on the hot keys): each of nb blocks histograms a contiguous chunk of
+// the worklist in shared memory, k_sort_offsets turns the [nb, keys] counts
+// into per-(block, key) bases, k_sort_scatter places the rows with shared-
+// memory cursors.  The order inside a key is arbitrary (labels are certified
+// per row, independent of the tiling).
+__device__ __forceinline__ void sort_chunk(int64_t m, int nb, int b, int64_t& p0, int64_t& p1) {
+    const int64_t per = (m + nb - 1) / nb;
+    p0 = (int64_t)b * per;
+    p1 = p0 + per < m ? p0 + per : m;
+}
+
+__global__ void __launch_bounds__(256) k_sort_hist(DevState S, const int64_t* count, int* hist) {
+    if (*S.done) return;
+    extern __shared__ int sh[];
+    const int keys = S.kcols;
+    for (int j = threadIdx.x; j < keys; j += blockDim.x) sh[j] = 0;
+    __syncthreads();
+    int64_t p0, p1;
+    sort_chunk(*count, gridDim.x, blockIdx.x, p0, p1);
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x)
+        atomicAdd(sh + sort_key(S, S.labels[S.work[p]]), 1);
+    __syncthreads();
+    int* h = hist + (int64_t)blockIdx.x * keys;
+    for (int j = threadIdx.x; j < keys; j += blockDim.x) h[j] = sh[j];
+}
+
+// per key: exclusive prefix over the blocks (in place) and the key total (lcur)
+__global__ void k_sort_offsets(DevState S, int* hist, int nb) {
+    if (*S.done) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= S.kcols) return;
+    int run = 0;
+    for (int b = 0; b < nb; b++) {
+        const int v = hist[(int64_t)b * S.kcols + j];
+        hist[(int64_t)b * S.kcols + j] = run;
+        run += v;
+    }
+    S.lcur[j] = run;
+}
+
+// The label each 128-position tile is centered on: the label of its first
+// position (the key whose [base, next base) range holds it).
+__global__ void k_tile_labels(DevState S, const int64_t* count) {
+    if (*S.done) return;
+    const int64_t m = *count;
+    const int64_t nt = (m + 127) / 128;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int p = (int)(t * 128);
+        int lo = 0, hi = S.kcols;  // first key whose base exceeds p
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(S.lcur + mid) > p) hi = mid;
+            else lo = mid + 1;
+        }
+        S.tile_lab[t] = col_id(S, lo - 1);
+    }
+}
+
+// Sort and gather in one pass: each worklist row is placed at its sorted
+// position by a shared-memory cursor (per-block bases from k_sort_offsets)
+// and written there centered on its tile's centroid and split for 3xTF32
+// (full 128-byte lines), with its certification record (one 32-byte sector).
+// L lanes per row (float4 columns).
+template <int L>
+__global__ void __launch_bounds__(256) k_sort_gather(DevState S, const int64_t* count, const int* hist) {
+    if (*S.done) return;
+    extern __shared__ int sh[];
+    const int keys = S.kcols;
+    const int* h = hist + (int64_t)blockIdx.x * keys;
+    for (int j = threadIdx.x; j < keys; j += blockDim.x) sh[j] = __ldg(S.lcur + j) + h[j];
+    __syncthreads();
+    int64_t p0, p1;
+    sort_chunk(*count, gridDim.x, blockIdx.x, p0, p1);
+    const int sub = threadIdx.x & (L - 1);
+    const int c4n = S.ldx / 4;
+    const float kap = tc_kappa_ordered(S.d);
+    const int RPB = blockDim.x / L;  // rows per block step
+    for (int64_t base = p0; base < p1; base += RPB) {
+        const int64_t p = base + threadIdx.x / L;
+        const bool ok = p < p1;
+        int row = 0, lab = 0, pos = 0, a = -1;
+        uint32_t mask = 0;
+        float lun = 0.f;
+        if (ok && sub == 0) {
+            row = __ldcs(S.work + p);
+            lab = S.labels[row];
+            mask = __ldcs(S.ymask + p);
+            lun = __ldcs(&S.ylun[p].x);
+            pos = atomicAdd(sh + sort_key(S, lab), 1);
+            a = __ldg(S.tile_lab + (pos >> 7));
+        }
+        row = __shfl_sync(LK_FULL_MASK, row, 0, L);
+        pos = __shfl_sync(LK_FULL_MASK, pos, 0, L);
+        a = __shfl_sync(LK_FULL_MASK, a, 0, L);
+        double x2 = 0.0, xo = 0.0, xx = 0.0;
+        if (ok) {
+            const float4* xp = reinterpret_cast<const float4*>(S.X32 + (int64_t)row * S.ldx);
+            const float4* op = reinterpret_cast<const float4*>(S.C32 + (int64_t)(a >= 0 ? a : 0) * S.ldc);
+            float4* hp = reinterpret_cast<float4*>(S.Xg_hi + (int64_t)pos * S.ldx);
+            float4* lp = reinterpret_cast<float4*>(S.Xg_lo + (int64_t)pos * S.ldx);
+            for (int c = sub; c < c4n; c += L) {
+                const float4 x = __ldg(xp + c);
+                const float4 o = a >= 0 ? __ldg(op + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float xv[4] = {x.x, x.y, x.z, x.w};
+                const float xs[4] = {x.x - o.x, x.y - o.y, x.z - o.z, x.w - o.w};
+                const float ov[4] = {o.x, o.y, o.z, o.w};
+                float hh[4], ll[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    hh[e] = __uint_as_float(__float_as_uint(xs[e]) & 0xFFFFE000u);
+                    ll[e] = xs[e] - hh[e];
+                    x2 = fma((double)xs[e], (double)xs[e], x2);
+                    xo = fma((double)xs[e], (double)ov[e], xo);
+                    xx = fma((double)xv[e], (double)xv[e], xx);
+                }
+                __stcs(hp + c, make_float4(hh[0], hh[1], hh[2], hh[3]));
+                __stcs(lp + c, make_float4(ll[0], ll[1], ll[2], ll[3]));
+            }
+        }
+#pragma unroll
+        for (int o = L >> 1; o > 0; o >>= 1) {
+            x2 += __shfl_xor_sync(LK_FULL_MASK, x2, o, L);
+            xo += __shfl_xor_sync(LK_FULL_MASK, xo, o, L);
+            xx += __shfl_xor_sync(LK_FULL_MASK, xx, o, L);
+        }
+        if (ok && sub == 0) {
+            TgyMeta t;
+            t.R = x2 + 2.0 * xo;
+            t.xo = __double2float_ru(sqrt(x2) * (1.0 + 1e-12));
+            t.xn2 = S.X64 ? S.xn2[row] : (float)xx;
+            float bv = INFINITY;
+            if (a >= 0 && lab == a) {
+                // upper bound on the TC value of the row's own label column (as k_gather_center)
+                const double xd = (double)t.xo, ca = (double)S.cnorm[a];
+                const double est = xd * xd - t.R;
+                const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
+                const double ea = (double)kap * xd * ca + gb * (fabs(est) + 2.0 * xd * ca) +
+                                  2.0 * 5.9604644775390625e-08 * fabs(est);
+                bv = __double2float_ru(est + 2.0 * ea + 1e-30);
+            }
+            t.bv = bv;
+            t.lun = lun;
+            t.row = row;
+            t.mask = mask;
+            const int4* src = reinterpret_cast<const int4*>(&t);
+            int4* dst = reinterpret_cast<int4*>(S.tmeta + pos);
+            __stcs(dst, src[0]);
+            __stcs(dst + 1, src[1]);
+        }
     }
 }
 
@@ -2052,7 +2228,7 @@ static int tc_max_dyn_smem() { return g_tc_max_dyn; }
 static int g_tgy_max_dyn = 0;
 static int tc_max_dyn_smem_tgy() { return g_tgy_max_dyn; }
 // k_assign_tgy: the k_assign_tc2 layout + the pair's per-group minima
-static int tgy_smem(const DevState& S) { return Tc2Smem::TOTAL + 8 * S.kpad + S.t_groups * 257 * 4; }
+static int tgy_smem(const DevState& S) { return TgySmem::TOTAL + S.t_groups * TgySmem::GS * 4; }
 
 template <int BN, int MODE, bool SPLIT, bool ARES, int CL = 1>
 static lk_status tc_attr(int optin) {
@@ -2288,19 +2464,23 @@ lk_status launch_assign_tc_centered(const DevState& S, const int32_t* rowlist,
 // (row-tile pair x group tile) MMAs of k_assign_tgy.
 lk_status launch_sort_tgy(const DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     const int64_t* count = stat + LK_STAT_WORK;
-    const int grid = sms * 8;
-    LK_CUDA_CHECK(cudaMemsetAsync(S.lcur, 0, (size_t)(S.kcols + 1) * 4, st));
-    k_label_count<<<grid, 256, 0, st>>>(S, S.work, count);
+    const int nb = tgy_sort_blocks(sms);
+    const size_t hs = (size_t)S.kcols * 4;
+    k_sort_hist<<<nb, 256, hs, st>>>(S, count, S.shist);
+    LK_LAUNCH_CHECK();
+    k_sort_offsets<<<(S.kcols + 255) / 256, 256, 0, st>>>(S, S.shist, nb);
     LK_LAUNCH_CHECK();
     k_label_scan<<<1, 1024, 0, st>>>(S, 0);
     LK_LAUNCH_CHECK();
-    k_label_scatter<<<grid, 256, 0, st>>>(S, S.work, count);
+    k_tile_labels<<<sms * 2, 256, 0, st>>>(S, count);
+    LK_LAUNCH_CHECK();
+    // (d <= 32: at most 8 float4 columns per row)
+    // four lanes per row, 8 rows of a warp in flight (the row's chain of
+    // dependent loads -- worklist, label, cursor, tile label, point -- is the
+    // limit, not the bytes); 256-thread blocks, eight per SM
+    k_sort_gather<4><<<nb, 256, hs, st>>>(S, count, S.shist);
     LK_LAUNCH_CHECK();
     k_pair_mask<<<sms * 4, 256, 0, st>>>(S, count);
-    LK_LAUNCH_CHECK();
-    int L = 1;
-    while (L < 32 && L * 2 <= S.ldx / 4) L *= 2;
-    k_gather_center<<<sms * 8, 256, 0, st>>>(S, count, L);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }

@@ -58,6 +58,22 @@ __global__ void __launch_bounds__(kThreads) k_filter_tgy(DevState S, int64_t* st
                     xr[4 * z4 + 2] = v.z;
                     xr[4 * z4 + 3] = v.w;
                 }
+                // the group table is loaded with the point (one memory round trip
+                // instead of two; most rows that fail the global gate need it)
+                float v[32];
+                const float4* lp = reinterpret_cast<const float4*>(S.lb + i * S.nlb);
+#pragma unroll
+                for (int g4 = 0; g4 < 8; g4++) {
+                    if (4 * g4 < G) {
+                        const float4 q = __ldcs(lp + g4);
+                        v[4 * g4] = q.x;
+                        v[4 * g4 + 1] = q.y;
+                        v[4 * g4 + 2] = q.z;
+                        v[4 * g4 + 3] = q.w;
+                    } else {
+                        v[4 * g4] = v[4 * g4 + 1] = v[4 * g4 + 2] = v[4 * g4 + 3] = INFINITY;
+                    }
+                }
                 const float4* cp = reinterpret_cast<const float4*>(S.C32 + (int64_t)a * S.ldc);
                 float acc = 0.f, xn2 = 0.f;
 #pragma unroll
@@ -78,21 +94,6 @@ __global__ void __launch_bounds__(kThreads) k_filter_tgy(DevState S, int64_t* st
                 const bool tight = U < u;
                 u = fminf(u, U);
                 if (!(gate > u)) {
-                    // the group table (one contiguous row, lazy encoding)
-                    float v[32];
-                    const float4* lp = reinterpret_cast<const float4*>(S.lb + i * S.nlb);
-#pragma unroll
-                    for (int g4 = 0; g4 < 8; g4++) {
-                        if (4 * g4 < G) {
-                            const float4 q = __ldcs(lp + g4);
-                            v[4 * g4] = q.x;
-                            v[4 * g4 + 1] = q.y;
-                            v[4 * g4 + 2] = q.z;
-                            v[4 * g4 + 3] = q.w;
-                        } else {
-                            v[4 * g4] = v[4 * g4 + 1] = v[4 * g4 + 2] = v[4 * g4 + 3] = INFINITY;
-                        }
-                    }
                     float gmin = INFINITY;
 #pragma unroll
                     for (int g = 0; g < 32; g++) {
