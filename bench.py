@@ -2,7 +2,10 @@
 """Benchmark of the exact Lloyd iteration on B200 (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload cfg2] [--strategy hamerly] [--kernel auto]
+                    [--workload cfg5] [--strategy yinyang] [--kernel auto]
+
+Default workload: BASELINE configs[4] = cfg5 (n=5e7, d=32, k=4096), the largest
+configuration that fits one GPU, with the group-tile Yinyang path.
 
 A "step" is one Lloyd iteration (assignment over all n points -- full scan or
 bound-pruned, labels identical to Lloyd -- plus refinement) over the whole
@@ -159,9 +162,23 @@ def cpu_sample_rate(workload: str, strategy: str, warmup: int, steps: int, budge
 
 
 def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kernel_tc: bool,
-                     groups: int = 1):
+                     groups: int = 1, tiles: bool = False):
     """Algorithmic units of one kernel class summed over the timed iterations:
-    ("flop", F) or ("byte", B).  Per-unit figures are listed in DESIGN.md."""
+    ("flop", F) or ("byte", B).  Per-unit figures are listed in DESIGN.md.
+    tiles: the block-sparse group-tile Yinyang path (d <= 32 on the tensor
+    cores), whose pass counts every (row, centroid) product it evaluates."""
+    ldx = d if d <= 2 else (d + 3) // 4 * 4
+    if tiles:
+        nlb = (groups + 3) // 4 * 4
+        if cls == 0:  # k_assign_tgy: 2*d flops per evaluated (row, centroid) pair
+            return "flop", sum(2.0 * (n * k if r["t"] == 1 else r["group_dists"]) * d for r in recs)
+        if cls == 1:  # k_filter_tgy: label/ub/glb per row; point + group-table row per
+            # row failing the global gate; worklist entry (row, mask, bound) per listed row
+            return "byte", sum(12.0 * n + r["active"] * (4.0 * ldx + 4.0 * nlb) + 16.0 * r["work"]
+                               for r in recs)
+        if cls == 10:  # sort + centered gather: worklist entry and label in, point in,
+            # hi/lo rows and the 32-byte record out, per listed row
+            return "byte", sum(r["work"] * (20.0 + 12.0 * ldx + 32.0) for r in recs)
     if cls == 7:  # tensor-core candidate pass over the ambiguous rows
         return "flop", sum(2.0 * r["candidate"] * k * d for r in recs)
     if cls == 9:  # fp32 rescan of candidate-overflow rows
@@ -200,7 +217,34 @@ def algorithmic_work(cls: int, strategy: str, n: int, d: int, k: int, recs, kern
 
 CLASS_NAMES = {0: "assign", 1: "filter", 2: "recheck_fp64", 3: "refine", 4: "update",
                5: "group_scan", 6: "group_merge", 7: "tc_collect", 8: "cand_recheck",
-               9: "ovf_rescan"}
+               9: "ovf_rescan", 10: "sort_gather"}
+
+
+def measure_tf32_tflops(reps: int = 12) -> float:
+    """Dense TF32 tensor throughput of this GPU: torch.matmul fp32 8192^3 with
+    allow_tf32 (cuBLAS), best of ``reps`` timed with CUDA events."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        nn = 8192
+        a = torch.randn(nn, nn, device="cuda")
+        b = torch.randn(nn, nn, device="cuda")
+        for _ in range(3):
+            torch.matmul(a, b)
+        best = float("inf")
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2.0 * nn ** 3 / (best / 1e3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
 
 
 def run_ours(args):
@@ -228,10 +272,16 @@ def run_ours(args):
     cfg = datasets.CONFIGS[args.workload]
     W, K = args.warmup, args.steps
     T = W + K
-    x_full = datasets.generate(args.workload)
-    init = init_random(RunContext(seed=cfg.seed_init), x_full, cfg.k)
     r0, r1 = shard_rows(cfg.n, ws, rank)
-    x = x_full[r0:r1]
+    if ws == 1:
+        x_full = datasets.generate(args.workload)
+        init = init_random(RunContext(seed=cfg.seed_init), x_full, cfg.k)
+        x = x_full
+    else:
+        # each rank generates only its own shard (and the init rows)
+        x_full = None
+        x = datasets.generate_rows(args.workload, r0, r1)
+        init = datasets.init_from_rows(args.workload)
     n, d, k = cfg.n, cfg.d, cfg.k
     strategy = args.strategy
     gpu_strat = strategy
@@ -303,20 +353,24 @@ def run_ours(args):
 
     # profiled pass over the same iterations: per-class device time
     _, _ = trajectory(True)
-    cls_ms = {c: eng.profile_read(c)[0] for c in range(10)}
+    cls_ms = {c: eng.profile_read(c)[0] for c in CLASS_NAMES}
     eng.profile(False)
     dom = max(cls_ms, key=lambda c: cls_ms[c])
     peaks = load_peaks()
-    kind, units = algorithmic_work(dom, gpu_strat, x.shape[0], d, k, recs, False, n_groups)
+    tiles = eng.group_cap == 128
+    if tiles:
+        n_groups = eng.group_count
+    kind, units = algorithmic_work(dom, gpu_strat, x.shape[0], d, k, recs, False, n_groups, tiles)
     dom_s = cls_ms[dom] / 1e3
     uses_tc = args.kernel == "tc" or (args.kernel == "auto" and d >= 32)
     if kind == "flop":
         if dom in (2, 8):
             peak, pk_src, bound = 37.0, "nominal B200 FP64 (no measured figure)", "compute-fp64"
         elif uses_tc and dom in (0, 7):
-            peak = peaks["bf16_tflops"] / 2.0 / 3.0
-            pk_src = (f"tensor TF32 = bf16_tflops/2 ({peaks['src']} {peaks['bf16_tflops']}), "
-                      "/3 for the 3xTF32 split")
+            tf32 = measure_tf32_tflops()
+            peak = tf32 / 3.0
+            pk_src = (f"measured dense TF32 {tf32:.0f} TFLOP/s (torch.matmul fp32 8192^3, "
+                      "allow_tf32, best of 12, this run) / 3 for the 3xTF32 split")
             bound = "tensor"
         else:
             peak = N_SMS * FP32_FLOP_PER_SM_CLK * peaks["sm_max_mhz"] * 1e6 / 1e12
@@ -335,14 +389,11 @@ def run_ours(args):
     tot_cls = sum(cls_ms.values()) or 1.0
     roof["share_of_step"] = cls_ms[dom] / tot_cls
     roof["class_ms_per_step"] = {CLASS_NAMES[c]: cls_ms[c] / K for c in cls_ms}
-    prof_path = os.path.join(REPO, "profiles", f"ncu_traffic_{args.workload}_{gpu_strat}.json")
-    if os.path.exists(prof_path):
-        with open(prof_path) as f:
-            tr = json.load(f).get(CLASS_NAMES[dom])
-        if tr is not None:
-            roof["traffic"] = tr
+    roof["traffic_note"] = ("null here: dram bytes of this kernel come from an ncu --set full "
+                            "capture of the same command, profiles/r02/")
     eng.close()
-    del flush
+    del eng, flush  # (the workspace is a torch tensor: free it before the e2e calls)
+    torch.cuda.empty_cache()
 
     # e2e through the public API, pinned host input
     e2e = None
@@ -377,7 +428,7 @@ def run_ours(args):
         wall = statistics.median(walls)
         its = res.iterations
         e2e = {"value": its / wall, "unit": "iterations/s",
-               "h2d_bytes_per_step": int((x_full.nbytes + ws * init.nbytes) / its),
+               "h2d_bytes_per_step": int((n * d * 4 + ws * init.nbytes) / its),
                "d2h_bytes_per_step": int((8 * n + ws * k * d * 8) / its),
                "iterations": its, "wall_s": wall, "calls": 3, "statistic": "median",
                "includes": "per rank: context+workspace setup, H2D of its pinned shard, the "
@@ -385,7 +436,7 @@ def run_ours(args):
                            "labels and the centroids D2H; wall time max over ranks"}
     if ws == 1:
         import paper_2010_06654_b200 as lk
-        xp = torch.from_numpy(x_full).pin_memory()
+        xp = torch.from_numpy(x).pin_memory()
 
         def api_call():
             if strategy == "lloyd":
@@ -403,7 +454,7 @@ def run_ours(args):
         wall = statistics.median(walls)
         its = len(res.iterations)
         e2e = {"value": its / wall, "unit": "iterations/s",
-               "h2d_bytes_per_step": int((x_full.nbytes + init.nbytes) / its),
+               "h2d_bytes_per_step": int((x.nbytes + init.nbytes) / its),
                "d2h_bytes_per_step": int((8 * n + k * d * 8 + 8 * its * (16 + 1)) / its),
                "iterations": its, "wall_s": wall, "calls": 3, "statistic": "median",
                "includes": "validation, H2D of the points from pinned memory (cached device "
@@ -428,12 +479,12 @@ def run_ours(args):
             "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": ms_max / K,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "fp32 (certified; fp64 recheck)", "data": "synthetic",
-            "config": {"workload": args.workload, "n": n, "d": d, "k": k,
-                       "strategy": strategy, "kernel": args.kernel, "groups": n_groups,
-                       "iterations": f"{W + 1}..{T} of one trajectory from random init",
-                       "l2": "flushed (256 MB write) between timed iterations",
-                       "parallelism": f"dp{ws} (row shards, int64 delta all-reduce)",
-                       "converged_in_window": converged_in_window},
+            "config": workload_config(args, cfg),
+            "strategy": f"{strategy} (GPU; kernel={args.kernel}, {n_groups} groups"
+                        + (", group tiles" if tiles else "") + ")",
+            "run": {"parallelism": f"dp{ws} (row shards, int64 delta all-reduce)",
+                    "converged_in_window": converged_in_window,
+                    "timed": "device events per iteration on the launching stream, max over ranks"},
             "effective_tflops": 2.0 * n * k * d * value / 1e12,
             "gpu_launches": int(launches),
             "roofline": roof,
@@ -469,8 +520,9 @@ def run_reference(args):
         "unit": "iterations/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 / rate if rate else None, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp64", "data": "synthetic",
-        "config": {"workload": args.workload, "n": cfg.n, "d": cfg.d, "k": cfg.k,
-                   "strategy": args.strategy},
+        "config": workload_config(args, cfg),
+        "strategy": f"{info['strategy']} (oracle C port of the reference's algorithm, fp64; "
+                    "every exact strategy returns Lloyd's labels)",
         "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": info["threads"],
                          "kind": "port",
                          "sample": f"oracle port ({info['strategy']}, fp64, {info['threads']} "
@@ -483,14 +535,24 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def workload_config(args, cfg) -> dict:
+    """The workload both arms run (identical dicts: strategy and machine details
+    are reported beside it)."""
+    return {"workload": args.workload, "n": cfg.n, "d": cfg.d, "k": cfg.k,
+            "iterations": f"{args.warmup + 1}..{args.warmup + args.steps} of one trajectory from "
+                          f"the reference's random init (seed {cfg.seed_init})",
+            "l2": "GPU arm: 256 MB L2 flush between timed iterations (outside the events)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
-    ap.add_argument("--strategy", default="yinyang", choices=["lloyd", "hamerly", "yinyang", "elkan"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--strategy", default="yinyang",
+                    choices=["lloyd", "hamerly", "yinyang", "elkan", "regroup"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc"])
     ap.add_argument("--groups", type=int, default=0, help="Yinyang group count (0 = default)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -109,6 +109,52 @@ def generate(name: str, n: int | None = None, *, with_labels: bool = False):
     return (x, lab) if with_labels else x
 
 
+def generate_rows(name: str, r0: int, r1: int) -> np.ndarray:
+    """Rows r0..r1-1 of the full config ``name`` -- bit-identical to
+    generate(name)[r0:r1] -- generating only the 1M-row chunks that overlap
+    the range (one rank's shard; no rank materializes the whole matrix)."""
+    cfg = CONFIGS[name]
+    r0, r1 = max(0, int(r0)), min(cfg.n, int(r1))
+    centres, sigma, weights = _mixture(cfg)
+    k, d = cfg.k, cfg.d
+    out = np.empty((max(0, r1 - r0), d), dtype=np.float32)
+    if r1 <= r0:
+        return out
+    if weights is None:
+        perm_rng = np.random.default_rng([cfg.seed_data, 0xFFFF])
+        order = perm_rng.permutation(cfg.n)
+    for c0 in range((r0 // CHUNK) * CHUNK, r1, CHUNK):
+        c1 = min(cfg.n, c0 + CHUNK)
+        rng = np.random.default_rng([cfg.seed_data, c0 // CHUNK])
+        if weights is None:
+            lb = (order[c0:c1] % k).astype(np.int64)
+        else:
+            lb = rng.choice(k, size=c1 - c0, p=weights)
+        noise = rng.standard_normal(size=(c1 - c0, d), dtype=np.float32)
+        blk = centres[lb].astype(np.float32) + noise * sigma[lb, None].astype(np.float32)
+        if name == "cfg4":
+            np.clip(blk, 0.0, 1.0, out=blk)
+        a0, a1 = max(c0, r0), min(c1, r1)
+        out[a0 - r0:a1 - r0] = blk[a0 - c0:a1 - c0]
+    return out
+
+
+def init_from_rows(name: str, seed: int | None = None) -> np.ndarray:
+    """init_random(RunContext(seed), generate(name), k) without the full
+    matrix: the same rng.choice draw (core.py:182-189), then only the chunks
+    holding the chosen rows."""
+    cfg = CONFIGS[name]
+    ctx = RunContext(seed=cfg.seed_init if seed is None else seed)
+    idx = ctx.rng.choice(cfg.n, size=cfg.k, replace=False)
+    out = np.empty((cfg.k, cfg.d), dtype=np.float64)
+    chunks = sorted(set(int(i) // CHUNK for i in idx))
+    for ch in chunks:
+        blk = generate_rows(name, ch * CHUNK, min(cfg.n, (ch + 1) * CHUNK))
+        sel = np.nonzero(idx // CHUNK == ch)[0]
+        out[sel] = blk[idx[sel] - ch * CHUNK]
+    return out
+
+
 def initial_centroids(name: str, x: np.ndarray, seed: int | None = None) -> np.ndarray:
     """The reference's random init on these points (fp64, [k, d])."""
     cfg = CONFIGS[name]
