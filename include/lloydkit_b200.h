@@ -203,6 +203,17 @@ lk_status lk_step_update(lk_ctx *ctx, int32_t t, void *stream);
 lk_status lk_graph_capture(lk_ctx *ctx, int32_t t, void *stream);
 lk_status lk_graph_replay(lk_ctx *ctx, void *stream);
 
+/* Debug shadow check of the stored bounds (validate_bounds, bounds.py:280-328;
+ * run_pruner calls it when ctx.debug_validate, pruners.py:896-902): every
+ * row's ub / global lower bound / group lower bounds against the exact fp64
+ * distances to the current centroids, tolerance 1e-8 + 1e-9 |ref|.
+ * decayed = 1: after lk_step_update (bounds decayed by the centroid drift, the
+ * "iter{t}:decayed" point); 0: after lk_step_assign ("iter{t}:post").
+ * out[0] = worst ub overshoot, out[1] = worst global lower-bound overshoot,
+ * out[2 + g] = worst overshoot of group g (0: no violation); nout >= 2 + the
+ * group count.  O(n k d) fp64 work; synchronizes the stream. */
+lk_status lk_validate_bounds(lk_ctx *ctx, int32_t decayed, double *out, int32_t nout, void *stream);
+
 /* Number of kernel launches issued by this context so far. */
 int64_t lk_launch_count(const lk_ctx *ctx);
 

@@ -33,6 +33,7 @@ EXPORTED = (
     "lk_buffer", "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
     "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_graph_capture", "lk_graph_replay",
     "lk_launch_count", "lk_profile", "lk_profile_read", "lk_d2_update", "lk_group_shape",
+    "lk_validate_bounds",
 )
 
 
@@ -89,6 +90,7 @@ def load():
     L.lk_buffer.argtypes = [vp, i32, ctypes.POINTER(u64), ctypes.POINTER(u64)]
     L.lk_layout.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32)]
     L.lk_group_shape.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    L.lk_validate_bounds.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double), i32, vp]
     L.lk_scan_points.argtypes = [vp, vp]
     L.lk_set_quant.argtypes = [vp, vp]
     L.lk_set_centroids.argtypes = [vp, vp, vp]
@@ -106,7 +108,7 @@ def load():
                  "lk_layout", "lk_scan_points", "lk_set_quant", "lk_set_centroids",
                  "lk_set_groups", "lk_step_assign", "lk_step_update", "lk_graph_capture",
                  "lk_graph_replay", "lk_profile", "lk_profile_read", "lk_d2_update",
-                 "lk_group_shape"):
+                 "lk_group_shape", "lk_validate_bounds"):
         getattr(L, name).restype = i32
     _lib = L
     return L

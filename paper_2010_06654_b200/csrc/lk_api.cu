@@ -41,7 +41,7 @@ enum InternalBuf {
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
     B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB,
-    B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_COUNT_
+    B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_VALID, B_CCH, B_COUNT_
 };
 
 struct Layout {
@@ -61,6 +61,20 @@ static uint64_t align256(uint64_t v) { return (v + 255) & ~uint64_t(255); }
 
 static bool is_group_strategy(int s);
 static bool tc_enabled(const lk_config& c);
+
+// Elkan's per-centroid bounds (lk_elkan.cu) while the n x k bound table stays
+// small (n * k <= 2^26: 256 MB); larger runs keep the grouped bounds.
+// LK_ELKAN=0 (A/B knob) keeps the grouped path.
+static bool elkan_mode(const lk_config& c) {
+    static const int knob = [] {
+        const char* e = getenv("LK_ELKAN");
+        return e ? atoi(e) : 1;
+    }();
+    return knob != 0 && c.strategy == LK_STRAT_ELKAN && (int64_t)c.n_local * c.k <= (1LL << 26);
+}
+
+// the strategies that keep group bounds (lk_set_groups required)
+static bool group_mode(const lk_config& c) { return is_group_strategy(c.strategy) && !elkan_mode(c); }
 
 // Block-sparse Yinyang on the tensor cores (lk_tgy.cu): d <= 32 (one K chunk),
 // groups = 128-column tiles of the B operand, at most 32 of them (k <= 4096).
@@ -84,6 +98,10 @@ static int32_t nlb_for(const lk_config& c, int32_t* groups) {
         default: g = c.groups > 0 ? c.groups : (c.k + 9) / 10; break;
     }
     if (g > c.k) g = c.k;
+    if (elkan_mode(c)) {
+        *groups = 0;  // one bound per centroid, group-major [k, n]
+        return c.k;
+    }
     if (tgy_mode(c)) {
         // one group per 128-column tile; the row-major bound table is padded to
         // whole float4 loads (slots >= groups are never read)
@@ -92,13 +110,14 @@ static int32_t nlb_for(const lk_config& c, int32_t* groups) {
     }
     // the warp-per-row Yinyang path works on 8/16/32 group slots; extra slots
     // are empty groups (no members, never binding)
-    if (is_group_strategy(c.strategy) && g <= 32 && c.d <= 32)
+    if (group_mode(c) && g <= 32 && c.d <= 32)
         g = g <= 4 ? 4 : (g <= 8 ? 8 : (g <= 16 ? 16 : 32));
     *groups = g;
     return g < 1 ? 1 : g;
 }
 
 static bool tc_enabled(const lk_config& c) {
+    if (elkan_mode(c)) return false;  // Elkan's per-centroid loop is SIMT
     return c.kernel == LK_KERNEL_TC || (c.kernel == LK_KERNEL_AUTO && c.d >= 32);
 }
 
@@ -191,7 +210,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_DCUM] = (uint64_t)k * 4;
         L->size[B_DGCUM] = (uint64_t)L->groups * 4;
         L->size[B_GLB] = (uint64_t)n * 4;
-    } else if (is_group_strategy(c.strategy)) {
+    } else if (group_mode(c)) {
         int64_t cap = n * (int64_t)L->groups;
         if (cap > (1LL << 30)) cap = 1LL << 30;  // result slots, <= 16 GB
         if (cap < 1) cap = 1;
@@ -220,6 +239,8 @@ static bool make_layout(const lk_config& c, Layout* L) {
             L->size[B_GLB] = (uint64_t)n * 4;
         }
     }
+    if (elkan_mode(c)) L->size[B_CCH] = (uint64_t)k * k * 4;  // half inter-centroid distances
+    L->size[B_VALID] = (uint64_t)(2 + (L->groups > 0 ? L->groups : 1)) * 8;  // validator output
     L->size[B_SELF] = sizeof(lk::DevState);
     uint64_t off = 0;
     for (int b = 0; b < B_COUNT_; b++) {
@@ -375,7 +396,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     c->ws = reinterpret_cast<uint8_t*>(workspace);
     c->quant_set = false;
     c->centroids_set = false;
-    c->groups_set = !is_group_strategy(cfg->strategy);
+    c->groups_set = !group_mode(*cfg);
     c->launches = 0;
     c->profile = false;
     int sms = 148;
@@ -483,6 +504,8 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     LK_CUDA_CHECK(cudaMemset(S.done, 0, 16));
     S.lazy = L.size[B_GLB] > 0 ? 1 : 0;
     S.tgy = tgy_mode(*cfg) ? 1 : 0;
+    S.elkan = elkan_mode(*cfg) ? 1 : 0;
+    S.cch = buf<float>(c, B_CCH);
     S.kcols = S.tgy ? 128 * L.groups : cfg->k;
     S.colperm = S.tgy ? buf<int32_t>(c, B_GPERM) : nullptr;
     S.ymask = buf<uint32_t>(c, B_YMASK);
@@ -539,7 +562,9 @@ lk_status lk_buffer(const lk_ctx* c, int32_t id, uint64_t* offset, uint64_t* byt
 lk_status lk_group_shape(const lk_ctx* c, int32_t* groups, int32_t* capacity) {
     if (!c) return LK_ERR_ARG;
     if (groups) *groups = c->L.groups;
-    if (capacity) *capacity = c->S.tgy ? 128 : (is_group_strategy(c->cfg.strategy) ? 32767 : 0);
+    // (Elkan's per-centroid bounds: k singleton groups, capacity 1; no lk_set_groups)
+    if (groups && c->S.elkan) *groups = c->cfg.k;
+    if (capacity) *capacity = c->S.elkan ? 1 : c->S.tgy ? 128 : (group_mode(c->cfg) ? 32767 : 0);
     return LK_OK;
 }
 
@@ -685,7 +710,7 @@ static __global__ void k_init_centroids(lk::DevState S, int kpad) {
 
 lk_status lk_set_groups(lk_ctx* c, const int32_t* group_of, void* stream) {
     if (!c || !group_of) return LK_ERR_ARG;
-    if (!is_group_strategy(c->cfg.strategy)) {
+    if (!group_mode(c->cfg)) {
         set_error("lk_set_groups: strategy %d keeps no group bounds", c->cfg.strategy);
         return LK_ERR_STATE;
     }
@@ -744,7 +769,7 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     LK_CUDA_CHECK(cudaMemsetAsync(S.hlog_off, 0, c->L.size[B_HLOG_OFF], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.sse, 0, c->L.size[B_SSE], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
-    if (S.tgy) LK_CUDA_CHECK(cudaMemsetAsync(S.lb, 0, c->L.size[B_LB], st));  // bounds >= 0
+    if (S.tgy || S.elkan) LK_CUDA_CHECK(cudaMemsetAsync(S.lb, 0, c->L.size[B_LB], st));  // bounds >= 0
     if (S.lazy) {
         LK_CUDA_CHECK(cudaMemsetAsync(S.dcum, 0, c->L.size[B_DCUM], st));
         LK_CUDA_CHECK(cudaMemsetAsync(S.dgcum, 0, c->L.size[B_DGCUM], st));
@@ -778,7 +803,13 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
     const bool use_tc = lkh::tc_supported(S);
     lk_status s;
     if (n > 0) {
-        if (t == 1 && is_group_strategy(c->cfg.strategy) && lkh::yy_masked(S) && !use_tc) {
+        if (S.elkan) {
+            // per-centroid bounds, every iteration (iteration 1 seeds them exactly)
+            ProfScope p(c, 1, st);
+            s = lkh::launch_elkan(S, stat, c->sms, st);
+            if (s != LK_OK) return s;
+            c->launches += 2;
+        } else if (t == 1 && group_mode(c->cfg) && lkh::yy_masked(S) && !use_tc) {
             // group-order full scan that also seeds exact per-group bounds
             ProfScope p(c, 0, st);
             s = lkh::launch_yy_seed(S, stat, c->sms, st);
@@ -810,7 +841,7 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             s = lkh::launch_assign_tgy(S, stat, n, c->sms, st);
             if (s != LK_OK) return s;
             c->launches += 8;
-        } else if (is_group_strategy(c->cfg.strategy)) {
+        } else if (group_mode(c->cfg)) {
             // tensor-core runs: every row failing the bounds is rescanned in full
             const bool full_only = use_tc;
             if (lkh::yy_fused_ok(S)) {
@@ -966,6 +997,18 @@ lk_status lk_graph_replay(lk_ctx* c, void* stream) {
     }
     LK_CUDA_CHECK(cudaGraphLaunch(c->graph_exec, (cudaStream_t)stream));
     return LK_OK;
+}
+
+lk_status lk_validate_bounds(lk_ctx* c, int32_t decayed, double* out, int32_t nout, void* stream) {
+    if (!c || !out) return LK_ERR_ARG;
+    const int need = 2 + (c->L.groups > 0 ? c->L.groups : 1);
+    if (nout < need) {
+        set_error("lk_validate_bounds: %d output slots, need %d", nout, need);
+        return LK_ERR_ARG;
+    }
+    for (int i = 0; i < nout; i++) out[i] = 0.0;
+    return lkh::launch_validate(c->S, decayed != 0, out, need, buf<double>(c, B_VALID),
+                                (cudaStream_t)stream);
 }
 
 int64_t lk_launch_count(const lk_ctx* c) { return c ? c->launches : 0; }

@@ -132,6 +132,9 @@ struct DevState {
     uint32_t* pmask;        // [n / 256 + 2] per row-tile pair: union of its rows' masks
     int32_t* shist;         // [tgy_sort_blocks, kcols] worklist sort: per-block key counts
     struct TgyMeta* tmeta;  // [n] per sorted position of the group-tile worklist (32 B)
+    // Elkan's per-centroid bounds (lk_elkan.cu): lb is [k, n]
+    int32_t elkan;
+    float* cch;             // [k, k] certified lower bound of 1/2 ||c_a - c_j||
     // a copy of this struct in device memory, for out-of-line device
     // functions (a reference to the kernel parameter would copy it to the stack)
     const DevState* self;

@@ -32,6 +32,10 @@ lk_status init_tc_attributes();
 lk_status init_yy_attributes();
 lk_status launch_scan_exp(const lk::DevState& S, int sms, cudaStream_t st);
 
+// debug shadow check of the stored bounds (lk_validate.cu): worst overshoot
+// per kind into host_out[0 .. nout) (ub, lb_global, lb_group[g]); synchronous
+lk_status launch_validate(const lk::DevState& S, int decayed, double* host_out, int nout,
+                          double* dev_scratch, cudaStream_t st);
 bool yy_masked(const lk::DevState& S);
 // one-kernel Yinyang iteration (lk_yy_fused.cu), d <= 32 and t <= 32
 bool yy_fused_ok(const lk::DevState& S);
@@ -60,6 +64,8 @@ lk_status launch_collect_tc(const lk::DevState& S, int64_t* stat, int64_t max_ro
                             cudaStream_t st);
 // block-sparse Yinyang on the tensor cores (group tiles, d <= 32): the bound
 // filter (lk_tgy.cu) and the sorted, masked tcgen05 pass over its worklist
+// Elkan's per-centroid bounds (lk_elkan.cu): half-distance table + assignment
+lk_status launch_elkan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_filter_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_sort_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_assign_tgy(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,

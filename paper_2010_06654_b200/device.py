@@ -161,6 +161,7 @@ class IterRecord:
     assign_ms: float
     update_ms: float
     tile_mode: bool = False  # group tiles: group_dists counts every distance the pass evaluated
+    per_centroid: bool = False  # Elkan's per-centroid bounds: group_dists counts every distance
 
 
 class DeviceLogChunk:
@@ -410,7 +411,8 @@ class DeviceLloyd:
 
     def set_centroids(self, init):
         torch = _torch()
-        if self.strategy in GROUP_STRATEGIES:
+        if self.strategy in GROUP_STRATEGIES and self.group_cap != 1:
+            # (capacity 1: Elkan's per-centroid bounds, no grouping)
             if self.group_cap == 128:
                 t, cap = self.group_count, self.group_cap
             else:
@@ -434,6 +436,20 @@ class DeviceLloyd:
             import torch.distributed as dist
             dist.all_reduce(self.delta, group=self.comm)
         nat.check(self.lib.lk_step_update(self.ctx, int(t), st), "lk_step_update")
+
+    def validate(self, decayed: bool) -> dict:
+        """Shadow check of the stored bounds against exact fp64 distances
+        (lk_validate_bounds; validate_bounds, bounds.py:280-328): the worst
+        overshoot per kind, only kinds that were violated."""
+        nout = 2 + max(1, self.group_count)
+        out = (ctypes.c_double * nout)()
+        nat.check(self.lib.lk_validate_bounds(self.ctx, int(decayed), out, nout, self.stream_handle()),
+                  "lk_validate_bounds")
+        if self.group_cap == 1:  # Elkan's per-centroid bounds (bounds.py:304-305)
+            names = ["ub", "lb_center"]
+        else:
+            names = ["ub", "lb_global"] + [f"lb_group[{g}]" for g in range(nout - 2)]
+        return {nm: float(v) for nm, v in zip(names, out) if v > 0.0}
 
     def launch_count(self) -> int:
         return int(self.lib.lk_launch_count(self.ctx))
@@ -475,9 +491,15 @@ class DeviceLloyd:
         self._bind(src, has_x64)
 
     def run(self, init, *, record_history: bool = True, check_every: int = 0,
-            use_graphs: bool = True):
+            use_graphs: bool = True, validate: bool = False):
         """Run up to t_max iterations from ``init``; stop after the first with
         changed == 0 (lloyd.py:169-171).  Returns a dict of host arrays.
+
+        validate: debug shadow check of the bounds after every assignment
+        ("iter{t}:post") and every centroid update ("iter{t+1}:decayed"), as
+        run_pruner does under ctx.debug_validate (pruners.py:896-902); eager
+        launches, one host sync per check; res["violations"] lists
+        (where, kind, worst overshoot).
 
         Iterations are launched ahead of the stop test (``check_every``):
         once an iteration reports changed == 0 the device marks the run done
@@ -489,7 +511,11 @@ class DeviceLloyd:
         if check_every <= 0 or check_every > self.history_iters:
             # the log holds history_iters iterations: drain at least that often
             check_every = self.history_iters
-        res = {"iterations": 0, "converged": False, "history": [], "records": []}
+        res = {"iterations": 0, "converged": False, "history": [], "records": [], "violations": []}
+        validate = validate and self.strategy != "lloyd"
+        if validate:
+            use_graphs = False
+            check_every = 1
         if T <= 0:
             res["centroids"] = np.array(init, dtype=np.float64, copy=True)
             res["labels"] = np.full(self.n, -1, dtype=np.int64)
@@ -517,12 +543,18 @@ class DeviceLloyd:
                 else:
                     nat.check(self.lib.lk_step_assign(self.ctx, t, self.stream_handle()),
                               "lk_step_assign")
+                    if validate:
+                        for kind, v in self.validate(False).items():
+                            res["violations"].append((f"iter{t}:post", kind, v))
                     if self.comm is not None:
                         import torch.distributed as dist
                         dist.all_reduce(self.delta, group=self.comm)
                     e1.record(stream)
                     nat.check(self.lib.lk_step_update(self.ctx, t, self.stream_handle()),
                               "lk_step_update")
+                    if validate and t < T:
+                        for kind, v in self.validate(True).items():
+                            res["violations"].append((f"iter{t + 1}:decayed", kind, v))
                 e2.record(stream)
                 chg[t - 1].copy_(self.stats[t - 1, nat.STAT["changed_global"]], non_blocking=True)
                 if t % check_every == 0 or t == T:  # (t=1 cannot converge: n rows move)
@@ -571,7 +603,7 @@ class DeviceLloyd:
                     sse=float(sse[t]),
                     assign_ms=e0.elapsed_time(e1),
                     update_ms=e1.elapsed_time(e2),
-                    tile_mode=self.group_cap == 128))
+                    tile_mode=self.group_cap == 128, per_centroid=self.group_cap == 1))
             res["iterations"] = iters
             res["converged"] = converged
             res["records"] = recs

@@ -83,8 +83,11 @@ def _iteration_stats(strategy: str, t: int, rec, n: int, k: int) -> IterationSta
     elif strategy in ("yinyang", "elkan"):
         # tightened rows + group scans (pruners.py:445-487 accounting)
         # (group tiles: the pass counts its own (row, centroid) evaluations)
-        dist = rec.active + rec.group_dists + (0 if getattr(rec, "tile_mode", False)
-                                               else rec.work * (k - 1))
+        if getattr(rec, "per_centroid", False):
+            dist = rec.group_dists  # (the Elkan kernel counts its tightens too)
+        else:
+            dist = rec.active + rec.group_dists + (0 if getattr(rec, "tile_mode", False)
+                                                   else rec.work * (k - 1))
         kw["bound_dist_comps"] = k
         kw["bound_accesses"] = n
         kw["bound_updates"] = n + rec.active + 2 * rec.work
@@ -144,7 +147,7 @@ def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: R
     init_copy = centers.copy()
     eng = _engine(x, k, strategy, t_max, kernel, device, groups, group_seed, record_history)
     try:
-        out = eng.run(centers, record_history=record_history)
+        out = eng.run(centers, record_history=record_history, validate=bool(ctx.debug_validate))
     finally:
         if _ENGINE_CACHE.get("engine") is not eng:
             eng.close()
@@ -160,8 +163,10 @@ def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: R
         c.iterations += 1
         c.wall_nanos += s.assign_nanos + s.refine_nanos
     del before
-    if ctx.debug_validate:
-        _shadow_check(ctx, x, out, label)
+    # debug mode: the device shadow check's violations, in the reference's
+    # (label, where, kind, worst overshoot) form (bounds.py:292-295)
+    for where, kind, worst in out.get("violations", []):
+        ctx.violations.append((label, where, kind, worst))
     return RunResult(
         centroids=out["centroids"],
         assign=out["labels"],
@@ -175,13 +180,6 @@ def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: R
                "candidate_rows": [r.candidate for r in out["records"]],
                "rescanned_rows": [r.work for r in out["records"]]},
     )
-
-
-def _shadow_check(ctx: RunContext, x, out, label: str):
-    """Debug mode (RunContext.debug_validate, core.py:65): the final labels must
-    be a nearest-centroid assignment of the returned run state.  Bound-level
-    shadow validation happens inside the bounded runs (pruners.py:896-902)."""
-    return None
 
 
 def run_lloyd(data, k: int, *, init=None, init_method: str = "kmeanspp", t_max: int = 10,
