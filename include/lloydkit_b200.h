@@ -63,9 +63,10 @@ typedef enum {
     LK_STRAT_LLOYD = 0,    /* run_lloyd: full n*k scan every iteration */
     LK_STRAT_HAMERLY = 1,  /* one upper + one global lower bound per point */
     LK_STRAT_YINYANG = 2,  /* upper bound + t group lower bounds per point */
-    LK_STRAT_ELKAN = 3,    /* group bounds (Elkan's per-centroid bounds folded into
-                              min(k, 32) groups on the SIMT path) */
-    LK_STRAT_REGROUP = 4   /* Yinyang group bounds (the host may regroup between runs) */
+    LK_STRAT_ELKAN = 3,    /* one lower bound per centroid while n_local * k <= 2^26
+                              (SIMT); group bounds above that */
+    LK_STRAT_REGROUP = 4   /* Yinyang with the group map rebuilt after every centroid update
+                              and the bounds remapped (<= 32 groups) */
 } lk_strategy;
 
 /* Assignment-kernel selection. */
@@ -127,6 +128,7 @@ enum {
     LK_STAT_OVERFLOW = 8,  /* ambiguous rows with > LK_MAX_CAND candidates (fp32 rescan) */
     LK_STAT_YWL = 9,       /* Yinyang rows that reached the per-group scan */
     LK_STAT_PAIRS = 10,    /* Yinyang (row, group) scans */
+    LK_STAT_REGROUPED = 11, /* Regroup: 1 if the group map was rebuilt before this iteration */
     LK_NSTAT = 16
 };
 

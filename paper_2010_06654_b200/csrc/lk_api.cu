@@ -41,7 +41,7 @@ enum InternalBuf {
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
     B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB,
-    B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_VALID, B_CCH, B_COUNT_
+    B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_VALID, B_CCH, B_RGSCR, B_RGMEANS, B_COUNT_
 };
 
 struct Layout {
@@ -85,8 +85,9 @@ static bool tgy_mode(const lk_config& c) {
         return e ? atoi(e) : 1;
     }();
     const int G = (c.k + 127) / 128;
-    return knob != 0 && is_group_strategy(c.strategy) && tc_enabled(c) && c.d >= 8 && c.d <= 32 &&
-           G <= 32;
+    // (Regroup rebuilds its groups every iteration; the tiles are fixed 128-column groups)
+    return knob != 0 && is_group_strategy(c.strategy) && c.strategy != LK_STRAT_REGROUP &&
+           tc_enabled(c) && c.d >= 8 && c.d <= 32 && G <= 32;
 }
 
 static int32_t nlb_for(const lk_config& c, int32_t* groups) {
@@ -238,6 +239,10 @@ static bool make_layout(const lk_config& c, Layout* L) {
             L->size[B_DGCUM] = (uint64_t)L->groups * 4;
             L->size[B_GLB] = (uint64_t)n * 4;
         }
+    }
+    if (c.strategy == LK_STRAT_REGROUP && group_mode(c)) {
+        L->size[B_RGSCR] = (uint64_t)(33 + k) * 4;
+        L->size[B_RGMEANS] = (uint64_t)(L->groups > 0 ? L->groups : 1) * d * 8;
     }
     if (elkan_mode(c)) L->size[B_CCH] = (uint64_t)k * k * 4;  // half inter-centroid distances
     L->size[B_VALID] = (uint64_t)(2 + (L->groups > 0 ? L->groups : 1)) * 8;  // validator output
@@ -421,10 +426,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.cnorm = buf<float>(c, B_CNORM);
     S.drift = buf<float>(c, B_DRIFT);
     S.s_half = buf<float>(c, B_SHALF);
-    S.gdrift = (cfg->strategy == LK_STRAT_YINYANG || cfg->strategy == LK_STRAT_ELKAN ||
-                cfg->strategy == LK_STRAT_REGROUP)
-                   ? buf<float>(c, B_GDRIFT)
-                   : nullptr;
+    S.gdrift = group_mode(*cfg) ? buf<float>(c, B_GDRIFT) : nullptr;  // (not Elkan's per-centroid bounds)
     S.scal = buf<float>(c, B_SCAL);
     S.group_of = buf<int32_t>(c, B_GROUP_OF);
     S.labels = buf<int32_t>(c, B_LABELS);
@@ -948,6 +950,11 @@ lk_status lk_step_update(lk_ctx* c, int32_t t, void* stream) {
     if (s == LK_OK && c->S.center) {
         s = lkh::launch_pair_table(c->S, st);  // centering offsets of the next iteration
         c->launches += 1;
+    }
+    if (s == LK_OK && c->cfg.strategy == LK_STRAT_REGROUP && group_mode(c->cfg)) {
+        // Regroup: the group map rebuilt from the new centroids, bounds remapped
+        s = lkh::launch_regroup(c->S, buf<int32_t>(c, B_RGSCR), buf<double>(c, B_RGMEANS), c->sms, st);
+        c->launches += 3;
     }
     return s;
 }

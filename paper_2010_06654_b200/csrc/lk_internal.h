@@ -66,6 +66,8 @@ lk_status launch_collect_tc(const lk::DevState& S, int64_t* stat, int64_t max_ro
 // filter (lk_tgy.cu) and the sorted, masked tcgen05 pass over its worklist
 // Elkan's per-centroid bounds (lk_elkan.cu): half-distance table + assignment
 lk_status launch_elkan(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
+// Regroup (lk_regroup.cu): the per-iteration regrouping and bound remap
+lk_status launch_regroup(const lk::DevState& S, int32_t* scr, double* means, int sms, cudaStream_t st);
 lk_status launch_filter_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_sort_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_assign_tgy(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,

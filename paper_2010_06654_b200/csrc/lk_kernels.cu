@@ -663,7 +663,7 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
     __shared__ int sarg[kThreads / 32];
     __shared__ float sg[1024];  // group drift maxima (t <= 1024)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const bool sg_ok = S.gdrift && S.t_groups <= 1024;
+    const bool sg_ok = S.gdrift && S.t_groups > 0 && S.t_groups <= 1024;
     // everything the block reads is issued up front (one dependent L2 round
     // trip instead of one per phase): the changed count, the counters of the
     // iteration, the cumulative group drifts

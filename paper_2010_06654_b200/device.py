@@ -162,6 +162,7 @@ class IterRecord:
     update_ms: float
     tile_mode: bool = False  # group tiles: group_dists counts every distance the pass evaluated
     per_centroid: bool = False  # Elkan's per-centroid bounds: group_dists counts every distance
+    regrouped: int = 0  # Regroup: the group map was rebuilt before this iteration
 
 
 class DeviceLogChunk:
@@ -603,7 +604,8 @@ class DeviceLloyd:
                     sse=float(sse[t]),
                     assign_ms=e0.elapsed_time(e1),
                     update_ms=e1.elapsed_time(e2),
-                    tile_mode=self.group_cap == 128, per_centroid=self.group_cap == 1))
+                    tile_mode=self.group_cap == 128, per_centroid=self.group_cap == 1,
+                    regrouped=int(stats[t, nat.STAT["regrouped"]])))
             res["iterations"] = iters
             res["converged"] = converged
             res["records"] = recs

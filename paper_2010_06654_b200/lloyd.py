@@ -80,7 +80,7 @@ def _iteration_stats(strategy: str, t: int, rec, n: int, k: int) -> IterationSta
         dist = n * k
         if strategy != "lloyd":
             kw["bound_updates"] = 2 * n
-    elif strategy in ("yinyang", "elkan"):
+    elif strategy in ("yinyang", "elkan", "regroup"):
         # tightened rows + group scans (pruners.py:445-487 accounting)
         # (group tiles: the pass counts its own (row, centroid) evaluations)
         if getattr(rec, "per_centroid", False):
@@ -178,7 +178,8 @@ def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: R
         label=label,
         extra={"device": "cuda", "recheck_rows": [r.flagged for r in out["records"]],
                "candidate_rows": [r.candidate for r in out["records"]],
-               "rescanned_rows": [r.work for r in out["records"]]},
+               "rescanned_rows": [r.work for r in out["records"]],
+               "regrouped": [r.regrouped for r in out["records"]]},
     )
 
 

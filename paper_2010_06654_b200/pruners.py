@@ -21,7 +21,7 @@ from .lloyd import RunResult, _prepare, run_device
 GPU_STRATEGY = {
     "hamerly": "hamerly",
     "yinyang": "yinyang",
-    "regroup": "yinyang",
+    "regroup": "regroup",
     "elkan": "elkan",
     "drake": "yinyang",
     "heap": "yinyang",
@@ -47,6 +47,9 @@ def gpu_groups(strategy: str, n: int, k: int, d: int = 0) -> int:
         if 0 < d <= 32:
             return min(k, 32)
         return k if n * k <= (1 << 26) else min(k, 64)
+    if strategy == "regroup":
+        # the device regroup pass handles <= 32 groups
+        return max(2, min(32, round(k / 64), k - 1))
     if strategy == "yinyang":
         # ~64 centroids per group (the reference's k/10 would make the n*t
         # table dominate an iteration's traffic at large k), at most 32 groups;

@@ -101,3 +101,23 @@ def test_group_tiles_off_knob():
     r = subprocess.run([sys.executable, "-c", OFF_CASE.format(repo=repo, tests=tests)], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("d,kernel", [(2, "simt"), (16, "simt"), (32, "simt"), (40, "auto")])
+def test_regroup_rebuilds_groups_and_matches_oracle(oracle, d, kernel):
+    """Regroup (pruners.py:500-504): the device rebuilds the group map after
+    every centroid update (regroup_pass, bounds.py:199-212) and remaps the
+    bounds (bounds.py:215-228); labels stay the oracle's."""
+    n, k = 20000, 240
+    # (overlapping blobs: the first iterations move the centroids far enough
+    # that the nearest-group-mean pass changes the map)
+    x = blobs(n, d, 60, seed=d + 11, spread=30.0 if d <= 32 else 6.0, sigma=2.0)
+    m = lk()
+    init = m.make_init(m.RunContext(seed=d), x, k, "random")
+    ref = oracle.run_lloyd(x, k, init, 12)
+    ctx = m.RunContext(seed=1, debug_validate=True)
+    res = m.run_pruner(x, k, "regroup", init=init, t_max=12, kernel=kernel, ctx=ctx)
+    check_trajectory(oracle, x, init, res.assign_history, ref["history"], f"regroup d={d}")
+    assert centroid_ok(res.centroids, ref["centroids"], x)
+    assert sum(res.extra["regrouped"]) > 0, res.extra["regrouped"]
+    assert ctx.violations == [], ctx.violations[:5]
