@@ -112,7 +112,10 @@ typedef enum {
     LK_BUF_QEXP = 11,      /* int32  [d + 1]         fixed-point exponents */
     LK_BUF_HLOG = 12,      /* int32x2 [history_cap]  (row, new label) of every moved row */
     LK_BUF_HLOG_OFF = 13,  /* int64  [t_max + 1]     log offset of each iteration (-1 overflow) */
-    LK_NBUF = 14
+    LK_BUF_TSTAMP = 14,    /* uint64 [t_max + 1, 2]  device clock (ns, %globaltimer): [t][0] update
+                              start, [t][1] update end of iteration t; [0][1] iteration 1's
+                              start (assign phase t = [t][0] - [t-1][1], also under graph replay) */
+    LK_NBUF = 15
 } lk_buffer_id;
 
 /* Per-iteration counters (LK_BUF_STATS rows). */

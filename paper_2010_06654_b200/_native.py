@@ -22,7 +22,8 @@ STRAT_IDS = {"lloyd": 0, "hamerly": 1, "yinyang": 2, "elkan": 3, "regroup": 4}
 KERNEL_IDS = {"auto": 0, "simt": 1, "tc": 2}
 
 BUF = {"x32": 0, "x64": 1, "c64": 2, "labels": 3, "ub": 4, "lb": 5, "delta": 6, "stats": 7,
-       "sse": 8, "group_of": 9, "counts": 10, "qexp": 11, "hlog": 12, "hlog_off": 13}
+       "sse": 8, "group_of": 9, "counts": 10, "qexp": 11, "hlog": 12, "hlog_off": 13,
+       "tstamp": 14}
 NSTAT = 16
 STAT = {"changed": 0, "flagged": 1, "active": 2, "work": 3, "dist": 4, "bound_upd": 5,
         "candidate": 6, "changed_global": 7, "overflow": 8, "ywl": 9, "pairs": 10,

@@ -34,7 +34,7 @@ namespace {
 
 enum InternalBuf {
     B_X32 = 0, B_X64, B_C64, B_LABELS, B_UB, B_LB, B_DELTA, B_STATS, B_SSE, B_GROUP_OF, B_COUNTS,
-    B_QEXP, B_HLOG, B_HLOG_OFF, B_CUR,
+    B_QEXP, B_HLOG, B_HLOG_OFF, B_TSTAMP, B_CUR,
     // internal
     B_C64_PREV, B_C32, B_CNORM, B_DRIFT, B_SHALF, B_GDRIFT, B_SCAL, B_MOVED, B_FLAGGED, B_WORK,
     B_SUMS, B_QSUM, B_QSCALE, B_QINV, B_XSHIFT, B_DONE, B_SSE_PART, B_PW_PROG,
@@ -153,6 +153,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
     L->size[B_HLOG] = c.history_cap > 0 ? (uint64_t)c.history_cap * 8 : 0;
     L->size[B_HLOG_OFF] = (uint64_t)(tm + 1) * 8;
     L->size[B_CUR] = (uint64_t)LK_NSTAT * 8;
+    L->size[B_TSTAMP] = (uint64_t)(tm + 1) * 2 * 8;
     L->size[B_C64_PREV] = (uint64_t)k * d * 8;
     L->size[B_C32] = (uint64_t)k * L->ldc * 4;
     L->size[B_CNORM] = (uint64_t)k * 4;
@@ -447,6 +448,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.t_max = cfg->t_max;
     S.hlog = buf<int2>(c, B_HLOG);
     S.hlog_off = buf<int64_t>(c, B_HLOG_OFF);
+    S.tstamp = buf<uint64_t>(c, B_TSTAMP);
     S.hlog_cap = cfg->history_cap;
     S.stats = buf<int64_t>(c, B_STATS);
     S.sse = buf<double>(c, B_SSE);
@@ -769,6 +771,7 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     LK_CUDA_CHECK(cudaMemsetAsync(S.stats, 0, c->L.size[B_STATS], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.cur, 0, c->L.size[B_CUR], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.hlog_off, 0, c->L.size[B_HLOG_OFF], st));
+    LK_CUDA_CHECK(cudaMemsetAsync(S.tstamp, 0xff, c->L.size[B_TSTAMP], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.sse, 0, c->L.size[B_SSE], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
     if (S.tgy || S.elkan) LK_CUDA_CHECK(cudaMemsetAsync(S.lb, 0, c->L.size[B_LB], st));  // bounds >= 0
@@ -782,6 +785,17 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     c->launches += 1;
     c->centroids_set = true;
     return LK_OK;
+}
+
+// Device-clock stamp of iteration 1's start (tstamp[0][1]); the update kernel
+// stamps every iteration's update start / end (tstamp[t][0..1]), so the
+// assign / refine split survives CUDA-graph replay.
+static __global__ void k_stamp_start(lk::DevState S) {
+    if (threadIdx.x == 0) {
+        uint64_t g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        S.tstamp[1] = g;
+    }
 }
 
 lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
@@ -804,6 +818,13 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
     const int64_t n = c->cfg.n_local;
     const bool use_tc = lkh::tc_supported(S);
     lk_status s;
+    if (t == 1) {
+        // the iteration's start on the device clock (later iterations start
+        // where the previous update ended: lk_step_update stamps it)
+        k_stamp_start<<<1, 32, 0, st>>>(S);
+        LK_LAUNCH_CHECK();
+        c->launches += 1;
+    }
     if (n > 0) {
         if (S.elkan) {
             // per-centroid bounds, every iteration (iteration 1 seeds them exactly)

@@ -66,6 +66,8 @@ struct DevState {
     int32_t* iter;          // [1] current iteration (1-based), advanced by the update
     int64_t* cur;           // [LK_NSTAT] counters of the iteration in flight
     int64_t* stats;         // [t_max, LK_NSTAT]
+    uint64_t* tstamp;       // [t_max + 1][2] device clock (ns): [t][0] update start, [t][1] update end
+                            // of iteration t; [0][1] the start of iteration 1
     int32_t t_max;
     int2* hlog;             // [hlog_cap] label-history log: (row, new label) of moved rows
     int64_t* hlog_off;      // [t_max + 1] log offsets per iteration (-1: overflow)
@@ -183,6 +185,12 @@ __device__ __forceinline__ void write_lb_all(const DevState& S, int64_t row, flo
         return;
     }
     for (int g = 0; g < S.nlb; g++) S.lb[(int64_t)g * S.n + row] = v;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    return g;
 }
 
 __device__ __forceinline__ float tf32_trunc(float x) {

@@ -722,6 +722,7 @@ __device__ __forceinline__ void update_global_block(const DevState& S, const dou
         S.scal[3] = __int_as_float(xa);
         S.delta[(int64_t)S.k * S.d + 2 * S.k] = 0;
         if (t >= 1 && t <= S.t_max) S.sse[t - 1] = ss;
+        if (t >= 1 && t <= S.t_max) S.tstamp[2 * t + 1] = globaltimer_ns();  // the update's end
         if (S.hlog_inline && t >= 1 && t <= S.t_max) {
             // close the iteration's label-history segment (k_log_history's job on
             // the other paths); curv = this thread's cur[LK_STAT_CHANGED] (slot 0)
@@ -836,6 +837,12 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
     pdl_wait();
     pdl_trigger();
     if (*S.done) return;
+    if (threadIdx.x == 0) {
+        // the update phase's start on the device clock (earliest block)
+        const int t = *S.iter;
+        if (t >= 1 && t <= S.t_max)
+            atomicMin(reinterpret_cast<unsigned long long*>(S.tstamp + 2 * t), globaltimer_ns());
+    }
     const int warp = threadIdx.x >> 5;
     const int j = blockIdx.x * (kThreads / 32) + warp;
     update_centroid_warp(S, j, qinv, sse_part);

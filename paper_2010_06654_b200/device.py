@@ -334,6 +334,7 @@ class DeviceLloyd:
         self.hlog = (self._view("hlog", torch.int32, (self.history_cap, 2))
                      if self.history_cap else None)
         self.hlog_off = self._view("hlog_off", torch.int64, (max(1, self.t_max) + 1,))
+        self.tstamp = self._view("tstamp", torch.int64, (max(1, self.t_max) + 1, 2))
         if strategy != "lloyd":
             self.ub = self._view("ub", torch.float32, (self.n,))
             self.lb = self._view("lb", torch.float32, (self.nlb, self.n))
@@ -465,18 +466,42 @@ class DeviceLloyd:
         return ms.value, nl.value
 
     def capture(self, t: int) -> bool:
-        """Capture one iteration t >= 2 (assign + update) as a CUDA graph owned
-        by the native context (lk_graph_capture).  The iteration index lives
-        on the device, so the graph replays every later iteration.  Single
-        process only: with a communicator the all-reduce stays outside."""
-        if t < 2 or self.comm is not None:
+        """Capture one iteration t >= 2 as a CUDA graph; the iteration index
+        lives on the device, so the graph replays every later iteration.
+
+        Single process: assign + update captured natively (lk_graph_capture).
+        With a communicator: a torch CUDA graph of lk_step_assign, the
+        all-reduce of the delta payload (NCCL is stream-capturable) and
+        lk_step_update -- one launch per iteration and no host sync.  A
+        backend that cannot be captured (gloo) returns False: eager steps."""
+        if t < 2:
             return False
-        nat.check(self.lib.lk_graph_capture(self.ctx, int(t), self.stream_handle()),
-                  "lk_graph_capture")
+        if self.comm is None:
+            nat.check(self.lib.lk_graph_capture(self.ctx, int(t), self.stream_handle()),
+                      "lk_graph_capture")
+            self.graph_ready = True
+            return True
+        import torch.distributed as dist
+        if dist.get_backend(self.comm) != "nccl":
+            return False
+        torch = _torch()
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.graph(g, stream=side):
+            st = ctypes.c_void_p(side.cuda_stream)
+            nat.check(self.lib.lk_step_assign(self.ctx, int(t), st), "lk_step_assign")
+            dist.all_reduce(self.delta, group=self.comm)
+            nat.check(self.lib.lk_step_update(self.ctx, int(t), st), "lk_step_update")
+        self._torch_graph = g
         self.graph_ready = True
         return True
 
     def replay(self):
+        g = getattr(self, "_torch_graph", None)
+        if g is not None:
+            g.replay()
+            return
         nat.check(self.lib.lk_graph_replay(self.ctx, self.stream_handle()), "lk_graph_replay")
 
     def rebind(self, data):
@@ -576,6 +601,8 @@ class DeviceLloyd:
             h_stats = torch.empty(tuple(self.stats[:iters].shape), dtype=self.stats.dtype, pin_memory=True)
             h_sse = torch.empty(tuple(self.sse_buf[:iters].shape), dtype=self.sse_buf.dtype, pin_memory=True)
             h_c64 = torch.empty(tuple(self.c64.shape), dtype=self.c64.dtype, pin_memory=True)
+            h_ts = torch.empty((iters + 1, 2), dtype=torch.int64, pin_memory=True)
+            h_ts.copy_(self.tstamp[: iters + 1], non_blocking=True)
             lab = torch.empty(self.n, dtype=torch.int64, pin_memory=True)
             h_stats.copy_(self.stats[:iters], non_blocking=True)
             h_sse.copy_(self.sse_buf[:iters], non_blocking=True)
@@ -591,9 +618,17 @@ class DeviceLloyd:
                 g = st_t.to("cpu").numpy()
                 g[:, nat.STAT["changed_global"]] = stats[:, nat.STAT["changed_global"]]
                 stats = g
+            # assign / refine split from the device-clock stamps of the library
+            # (valid under graph replay); host events where a stamp is missing
+            ts = h_ts.numpy().astype(np.uint64)
             recs = []
             for t in range(iters):
                 e0, e1, e2 = ev[t]
+                s_prev, u0, u1 = ts[t, 1], ts[t + 1, 0], ts[t + 1, 1]
+                if max(s_prev, u0, u1) < np.uint64(1 << 63) and s_prev <= u0 <= u1:
+                    a_ms, u_ms = float(u0 - s_prev) / 1e6, float(u1 - u0) / 1e6
+                else:
+                    a_ms, u_ms = e0.elapsed_time(e1), e1.elapsed_time(e2)
                 recs.append(IterRecord(
                     changed=int(stats[t, nat.STAT["changed_global"]]),
                     flagged=int(stats[t, nat.STAT["flagged"]]),
@@ -602,8 +637,8 @@ class DeviceLloyd:
                     work=int(stats[t, nat.STAT["work"]]),
                     group_dists=int(stats[t, nat.STAT["dist"]]),
                     sse=float(sse[t]),
-                    assign_ms=e0.elapsed_time(e1),
-                    update_ms=e1.elapsed_time(e2),
+                    assign_ms=a_ms,
+                    update_ms=u_ms,
                     tile_mode=self.group_cap == 128, per_centroid=self.group_cap == 1,
                     regrouped=int(stats[t, nat.STAT["regrouped"]])))
             res["iterations"] = iters

@@ -61,24 +61,41 @@ class ShardedLloyd:
         self._all_reduce(q, dist.ReduceOp.MAX)
         self.engine.set_quant()
 
-    def run(self, init, t_max: int) -> ShardedResult:
+    def run(self, init, t_max: int, check_every: int = 8, use_graphs: bool = True) -> ShardedResult:
+        """Iterations 1..t_max without a host sync per iteration: the engine
+        stops itself once an iteration's global changed count is 0 (later
+        iterations are device no-ops, their all-reduced deltas are zero), and
+        the host reads the counters every ``check_every`` iterations and once
+        at the end.  From iteration 2 on an engine that can capture one
+        iteration (assign + all-reduce + update) as a CUDA graph replays it."""
         import torch.distributed as dist
         eng = self.engine
         eng.set_centroids(init)
-        changed, sse = [], []
-        converged = False
         it = 0
+        converged = False
+        changed_all = []
+        graphs = False
+        checked = 0
         for t in range(1, t_max + 1):
-            delta = eng.assign(t)
-            self._all_reduce(delta, dist.ReduceOp.SUM)
-            eng.update(t)
-            it = t
-            c = eng.changed_global(t)
-            changed.append(c)
-            sse.append(eng.sse(t))
-            if c == 0:
-                converged = True
-                break
+            if t == 2 and use_graphs and hasattr(eng, "capture"):
+                graphs = eng.capture(t)
+            if graphs:
+                eng.replay()
+            else:
+                delta = eng.assign(t)
+                self._all_reduce(delta, dist.ReduceOp.SUM)
+                eng.update(t)
+            if t % check_every == 0 or t == t_max:
+                chg = eng.changed_range(checked, t)  # one host sync
+                changed_all.extend(chg)
+                z = [i for i, c in enumerate(chg) if c == 0]
+                if z:
+                    it = checked + z[0] + 1
+                    converged = True
+                    break
+                checked = it = t
+        changed = changed_all[:it]
+        sse = eng.sse_range(0, it)
         return ShardedResult(iterations=it, converged=converged, centroids=eng.centroids(),
                              local_labels=eng.labels(), changed=changed, sse=sse)
 
@@ -123,12 +140,19 @@ class DeviceEngine:
         nat.check(self.dev.lib.lk_step_update(self.dev.ctx, int(t), self.dev.stream_handle()),
                   "lk_step_update")
 
-    def changed_global(self, t):
-        from . import _native as nat
-        return int(self.dev.stats[t - 1, nat.STAT["changed_global"]].item())
+    def capture(self, t):
+        return self.dev.capture(t)
 
-    def sse(self, t):
-        return float(self.dev.sse_buf[t - 1].item())
+    def replay(self):
+        self.dev.replay()
+
+    def changed_range(self, t0, t1):
+        """Global changed counts of iterations t0+1..t1 (one device->host copy)."""
+        from . import _native as nat
+        return [int(v) for v in self.dev.stats[t0:t1, nat.STAT["changed_global"]].to("cpu").tolist()]
+
+    def sse_range(self, t0, t1):
+        return [float(v) for v in self.dev.sse_buf[t0:t1].to("cpu").tolist()]
 
     def centroids(self):
         return self.dev.c64.to("cpu").numpy().copy()

@@ -52,6 +52,8 @@ class CpuFixedPointEngine:
         self.inv = np.ldexp(1.0, e - B)
 
     def set_centroids(self, init):
+        self._done = False
+        self._chg, self._sses = [], []
         self.c = np.array(init, dtype=np.float64, copy=True)
         self.labels_ = np.full(self.n, -1, dtype=np.int64)
         self.sums = np.zeros((self.k, self.d), dtype=np.int64)
@@ -60,6 +62,9 @@ class CpuFixedPointEngine:
 
     def assign(self, t):
         from oracle import oracle as O
+        if self._done:  # (the device's no-op iterations after convergence)
+            self._delta = torch.zeros(self.k * self.d + 2 * self.k + 8, dtype=torch.int64)
+            return self._delta
         new = O.assign_full(self.x, self.c, nthreads=1)[0] if self.n else np.empty(0, np.int64)
         moved = np.nonzero(new != self.labels_)[0]
         q = np.rint(self.x[moved] * self.scale[None, : self.d]).astype(np.int64)
@@ -78,6 +83,10 @@ class CpuFixedPointEngine:
         return self._delta
 
     def update(self, t):
+        if self._done:
+            self._chg.append(0)
+            self._sses.append(self._sse)
+            return
         kd, k = self.k * self.d, self.k
         dl = self._delta.numpy()
         self.sums += dl[:kd].reshape(self.k, self.d)
@@ -89,12 +98,15 @@ class CpuFixedPointEngine:
         sr = self.sums * self.inv[None, : self.d]
         self._sse = float(np.sum(np.where(nz, self.qs * self.inv[self.d]
                                           - np.sum(sr * sr, axis=1) / np.maximum(self.cnt, 1), 0)))
+        self._chg.append(self._changed)
+        self._sses.append(self._sse)
+        self._done = self._changed == 0
 
-    def changed_global(self, t):
-        return self._changed
+    def changed_range(self, t0, t1):
+        return list(self._chg[t0:t1])
 
-    def sse(self, t):
-        return self._sse
+    def sse_range(self, t0, t1):
+        return list(self._sses[t0:t1])
 
     def centroids(self):
         return self.c.copy()

@@ -30,25 +30,33 @@ def _case():
     return x, init
 
 
-def _rank(rank, world, port, strategy, out):
+def _rank(rank, world, port, strategy, out, backend="gloo"):
     import torch
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # gloo: every rank on the box's one GPU (host-staged exchange); nccl: one
+    # GPU per rank
+    dev = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2010_06654_b200.device import DeviceLloyd
     from paper_2010_06654_b200.distributed import (DeviceEngine, ShardedLloyd, gather_labels,
                                                    shard_rows)
     x, init = _case()
     r0, r1 = shard_rows(len(x), world, rank)
-    dev = DeviceLloyd(x[r0:r1], 64, strategy, 40, n_total=len(x), record_history=False,
-                      groups=7 if strategy == "yinyang" else 0)
-    drv = ShardedLloyd(DeviceEngine(dev))
+    eng = DeviceLloyd(x[r0:r1], 64, strategy, 40, n_total=len(x), record_history=False,
+                      groups=7 if strategy == "yinyang" else 0, comm=dist.group.WORLD)
+    drv = ShardedLloyd(DeviceEngine(eng), group=dist.group.WORLD)
     drv.bind()
     res = drv.run(init, 40)
     labels = gather_labels(res.local_labels)
     np.savez(out + f".r{rank}.npz", centroids=res.centroids, labels=labels,
-             iters=res.iterations, changed=np.array(res.changed))
+             iters=res.iterations, changed=np.array(res.changed),
+             graphed=bool(getattr(eng, "graph_ready", False)))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -69,3 +77,41 @@ def test_two_ranks_on_device_match_one_rank(tmp_path, oracle, strategy):
     assert a0["changed"].tolist() == ref["changed"].tolist()
     assert np.all(np.abs(a0["centroids"] - ref["centroids"])
                   <= 1e-5 * np.abs(ref["centroids"]) + 1e-9 * np.abs(x).max())
+
+
+def _check_against(out, ref_out, oracle, world):
+    parts = [np.load(out + f".r{r}.npz") for r in range(world)]
+    b = np.load(ref_out + ".r0.npz")
+    for p in parts:
+        assert np.array_equal(p["centroids"], b["centroids"])
+    assert np.array_equal(parts[0]["labels"], b["labels"])
+    assert int(parts[0]["iters"]) == int(b["iters"])
+    x, init = _case()
+    ref = oracle.run_lloyd(x, 64, init, 40)
+    assert int(parts[0]["iters"]) == ref["iterations"]
+    assert parts[0]["changed"].tolist() == ref["changed"].tolist()
+    return parts
+
+
+@pytest.mark.parametrize("strategy", ["lloyd", "yinyang"])
+def test_nccl_graph_captured_protocol_single_gpu(tmp_path, oracle, strategy):
+    """One rank over NCCL on the box's GPU: the iteration (assign, NCCL
+    all-reduce of the delta payload, update) is captured as one CUDA graph and
+    replayed without a host sync per iteration; the result equals the gloo
+    (eager) protocol bit for bit and the oracle's trajectory."""
+    out_n, out_g = str(tmp_path / "nccl"), str(tmp_path / "gloo")
+    mp.spawn(_rank, args=(1, _free_port(), strategy, out_n, "nccl"), nprocs=1, join=True)
+    mp.spawn(_rank, args=(1, _free_port(), strategy, out_g, "gloo"), nprocs=1, join=True)
+    parts = _check_against(out_n, out_g, oracle, 1)
+    assert bool(parts[0]["graphed"]), "the NCCL iteration was not graph-captured"
+
+
+@pytest.mark.skipif(not __import__("torch").cuda.is_available()
+                    or __import__("torch").cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs (one NCCL rank per GPU)")
+@pytest.mark.parametrize("strategy", ["lloyd", "hamerly", "yinyang"])
+def test_two_nccl_ranks_match_one_rank(tmp_path, oracle, strategy):
+    out2, out1 = str(tmp_path / "n2"), str(tmp_path / "n1")
+    mp.spawn(_rank, args=(2, _free_port(), strategy, out2, "nccl"), nprocs=2, join=True)
+    mp.spawn(_rank, args=(1, _free_port(), strategy, out1, "gloo"), nprocs=1, join=True)
+    _check_against(out2, out1, oracle, 2)
