@@ -11,6 +11,8 @@ bit-identical across strategies and GPU counts).
 
 from __future__ import annotations
 
+import threading
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -106,6 +108,9 @@ def _iteration_stats(strategy: str, t: int, rec, n: int, k: int) -> IterationSta
 # graph) per process, reused by the next call with the same shapes -- like an
 # FFT plan.  Every call still uploads its own points and init.
 _ENGINE_CACHE: dict = {}
+# The cached context is shared state: concurrent calls from several threads
+# take turns (the numpy reference is reentrant; a device context is not).
+_ENGINE_LOCK = threading.RLock()
 
 
 def _engine(x, k, strategy, t_max, kernel, device, groups, group_seed, record_history):
@@ -145,12 +150,15 @@ def run_device(x, k: int, centers: np.ndarray, strategy: str, t_max: int, ctx: R
     """Shared body of run_lloyd / run_pruner / run_engine on one GPU."""
     n = x.shape[0]
     init_copy = centers.copy()
-    eng = _engine(x, k, strategy, t_max, kernel, device, groups, group_seed, record_history)
-    try:
-        out = eng.run(centers, record_history=record_history, validate=bool(ctx.debug_validate))
-    finally:
-        if _ENGINE_CACHE.get("engine") is not eng:
-            eng.close()
+    with _ENGINE_LOCK:
+        eng = _engine(x, k, strategy, t_max, kernel, device, groups, group_seed, record_history)
+        try:
+            # (the label history keeps its own device copy of the log: safe to
+            # read after the context is reused)
+            out = eng.run(centers, record_history=record_history, validate=bool(ctx.debug_validate))
+        finally:
+            if _ENGINE_CACHE.get("engine") is not eng:
+                eng.close()
     stats = [_iteration_stats(strategy, t + 1, r, n, k) for t, r in enumerate(out["records"])]
     before = ctx.counters.copy()
     for s in stats:
