@@ -207,7 +207,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_YLUN] = (uint64_t)n * 8;
         L->size[B_YMASK] = (uint64_t)n * 4;
         L->size[B_TMETA] = (uint64_t)n * sizeof(lk::TgyMeta);
-        L->size[B_PMASK] = (uint64_t)(n / 256 + 2) * 4;
+        L->size[B_PMASK] = (uint64_t)(n / 128 + 4) * 4;  // per 128-row tile
         L->size[B_SHIST] = (uint64_t)1536 * kpad * 4;  // (<= 1536 sort blocks)
         L->size[B_DCUM] = (uint64_t)k * 4;
         L->size[B_DGCUM] = (uint64_t)L->groups * 4;

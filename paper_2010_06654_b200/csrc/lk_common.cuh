@@ -131,7 +131,7 @@ struct DevState {
     int32_t kcols;          // B-operand columns (128 * groups with the group tiles, else k)
     const int32_t* colperm; // [kpad] centroid id of each B column (-1: padding); null = identity
     uint32_t* ymask;        // [n] per worklist entry: groups the row must scan
-    uint32_t* pmask;        // [n / 256 + 2] per row-tile pair: union of its rows' masks
+    uint32_t* pmask;        // [n / 128 + 4] per 128-row tile: union of its rows' masks
     int32_t* shist;         // [tgy_sort_blocks, kcols] worklist sort: per-block key counts
     struct TgyMeta* tmeta;  // [n] per sorted position of the group-tile worklist (32 B)
     // Elkan's per-centroid bounds (lk_elkan.cu): lb is [k, n]
@@ -150,8 +150,8 @@ __device__ __forceinline__ float store_ub(const DevState& S, float U, int label)
     return S.lazy ? __fsub_ru(U, S.dcum[label]) : U;
 }
 
-// Blocks of the group-tile worklist sort (lk_tc.cu k_sort_*): four per SM (one wave at 64 registers).
-inline int tgy_sort_blocks(int sms) { return 4 * (sms > 0 ? sms : 148) > 1536 ? 1536 : 4 * (sms > 0 ? sms : 148); }
+// Blocks of the group-tile worklist sort (lk_tc.cu k_sort_*): three per SM (one wave at 72 registers).
+inline int tgy_sort_blocks(int sms) { return 3 * (sms > 0 ? sms : 148) > 1536 ? 1536 : 3 * (sms > 0 ? sms : 148); }
 
 // numpy pairwise-sum association program passed by value (k-means++ D^2
 // updates): (0, start, len) = leaf, (1, 0, 0) = add the two top values.

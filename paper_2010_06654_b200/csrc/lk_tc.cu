@@ -1405,6 +1405,19 @@ struct TgySmem {
     static constexpr int TOTAL = GM_OFF + 1024;          // (+ G * GS * 4 at launch)
 };
 
+// A pair's centroid tiles run starting from the group of its first row tile's
+// label (then in increasing group order, wrapping): rows mostly belong to that
+// group, so their running top-2 is tight after the first tile and the exact
+// update of later chunks rarely triggers.  All three roles derive the same
+// order from the same loads.
+__device__ __forceinline__ int tgy_rot(const DevState& S, int64_t rt) {
+    const int a = __ldg(S.tile_lab + rt);
+    return a >= 0 ? __ldg(S.group_of + a) : 0;
+}
+__device__ __forceinline__ uint32_t rotr32(uint32_t m, int r) {
+    return r ? (m >> r) | (m << (32 - r)) : m;
+}
+
 __global__ void __launch_bounds__(320, 1)
     k_assign_tgy(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                  const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -1482,7 +1495,7 @@ __global__ void __launch_bounds__(320, 1)
             uint32_t phase = 0, rphase = 0;
             for (int it = 0; it < n_it; it++) {
                 const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
-                const uint32_t pm = __ldg(S.pmask + rp);
+                const uint32_t pm = __ldg(S.pmask + 2 * rp) | __ldg(S.pmask + 2 * rp + 1);
                 mbar_wait(aempty, (it & 1) ^ 1);
                 mbar_expect_tx(afull, 4 * SM::A_BYTES);
 #pragma unroll
@@ -1493,8 +1506,9 @@ __global__ void __launch_bounds__(320, 1)
                 }
                 const float* bt0 = beta_of(2 * rp);
                 const float* bt1 = beta_of(2 * rp + 1);
-                for (uint32_t mm = pm; mm; mm &= mm - 1) {
-                    const int ct = __ffs(mm) - 1;
+                const int g0 = tgy_rot(S, 2 * rp);
+                for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
+                    const int ct = (__ffs(mm) - 1 + g0) & 31;
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* bst = smem + stage * SM::STAGE_BYTES;
                     mbar_expect_tx(&full[stage], SM::STAGE_BYTES);
@@ -1523,12 +1537,16 @@ __global__ void __launch_bounds__(320, 1)
         int64_t n_dist = 0;
         for (int it = 0; it < n_it; it++) {
             const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
-            const uint32_t pm = __ldg(S.pmask + rp);
-            const int64_t rows = m - 2 * rp * BM < 2 * BM ? m - 2 * rp * BM : 2 * BM;
-            n_dist += rows * 128 * __popc(pm);
+            // each row tile runs only the centroid tiles of its own mask
+            const uint32_t m0 = __ldg(S.pmask + 2 * rp), m1 = __ldg(S.pmask + 2 * rp + 1);
+            const uint32_t pm = m0 | m1;
+            const int64_t r0n = m - 2 * rp * BM < BM ? m - 2 * rp * BM : BM;
+            const int64_t r1n = m - (2 * rp + 1) * BM < BM ? (m - (2 * rp + 1) * BM > 0 ? m - (2 * rp + 1) * BM : 0) : BM;
+            n_dist += 128 * (r0n * __popc(m0) + r1n * __popc(m1));
             mbar_wait(afull, it & 1);
             tc_fence_after();
-            for (uint32_t mm = pm; mm; mm &= mm - 1) {
+            const int g0 = tgy_rot(S, 2 * rp);
+            for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 mbar_wait(&full[stage], phase);
@@ -1536,8 +1554,10 @@ __global__ void __launch_bounds__(320, 1)
                 uint8_t* bst = smem + stage * SM::STAGE_BYTES;
                 const uint64_t dbhi = umma_desc(bst);
                 const uint64_t dblo = umma_desc(bst + SM::B_BYTES);
+                const int ct = (__ffs(mm) - 1 + g0) & 31;
 #pragma unroll
                 for (int s = 0; s < 2; s++) {
+                    if (!((((s ? m1 : m0)) >> ct) & 1u)) continue;  // (warp-uniform)
                     const uint32_t tmem_d = tmem_base + acc * 2 * BN + s * BN;
                     const uint64_t dahi = umma_desc(abuf + s * 2 * SM::A_BYTES);
                     const uint64_t dalo = umma_desc(abuf + s * 2 * SM::A_BYTES + SM::A_BYTES);
@@ -1573,7 +1593,10 @@ __global__ void __launch_bounds__(320, 1)
         const int rloc = rloc0 + lane;
         for (int it = 0; it < n_it; it++) {
             const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
-            const uint32_t pm = __ldg(S.pmask + rp);
+            // the pair's tiles stream in for the union of the two row tiles'
+            // masks; this row tile evaluates only its own (ms)
+            const uint32_t ms = __ldg(S.pmask + 2 * rp + s);
+            const uint32_t pm = __ldg(S.pmask + 2 * rp) | __ldg(S.pmask + 2 * rp + 1);
             const int64_t rt = 2 * rp + s;
             const int64_t r = rt * BM + q * 32 + lane;
             const bool valid = r < m;
@@ -1598,16 +1621,18 @@ __global__ void __launch_bounds__(320, 1)
                 bv = t.bv;
                 old = S.labels[row];
             }
-            for (uint32_t mm = pm; mm; mm &= mm - 1) {
-                const int ct = __ffs(mm) - 1;
+            const int g0 = tgy_rot(S, 2 * rp);
+            for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
+                const int ct = (__ffs(mm) - 1 + g0) & 31;
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
                 mbar_wait(&rfull[rs], rphase);
                 const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 2 * BN + s * BN;
                 const uint32_t sb0 = smem_u32(ring + rs * 256 + s * 128);
                 float gmin = INFINITY;
+                const bool mine = (ms >> ct) & 1u;  // (warp-uniform)
 #pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 64) {
+                for (int c0 = 0; c0 < (mine ? BN : 0); c0 += 64) {
                     uint32_t r0[32], r1[32];
                     tmem_ld32_async(taddr + c0, r0);
                     tmem_ld32_async(taddr + c0 + 32, r1);
@@ -1671,7 +1696,8 @@ __global__ void __launch_bounds__(320, 1)
                         }
                     }
                 }
-                sgm[ct * GS + rloc] = gmin;  // the group's minimum D'~ (raw)
+                if (mine)  // the group's minimum D'~ (raw)
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(sgm + ct * GS + rloc)), "f"(gmin) : "memory");
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
@@ -1703,10 +1729,13 @@ __global__ void __launch_bounds__(320, 1)
                 // every scanned group's bound (lazy encoding): its minimum bounds
                 // all its members, whichever wins; a certified row's winner group
                 // gets the second best (its other members)
-                for (uint32_t mm = pm; mm; mm &= mm - 1) {
+                for (uint32_t mm = ms; mm; mm &= mm - 1) {
                     const int g = __ffs(mm) - 1;
-                    const float v = g == g1 ? L2d : tgy_lower(R, xo, kxc, gb, cmax, sgm[g * GS + rloc]);
-                    sgm[g * GS + rloc] = __fadd_rd(v, sdg[g]);
+                    const uint32_t sa = smem_u32(sgm + g * GS + rloc);
+                    float raw;
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(raw) : "r"(sa) : "memory");
+                    const float v = g == g1 ? L2d : tgy_lower(R, xo, kxc, gb, cmax, raw);
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(sa), "f"(__fadd_rd(v, sdg[g])) : "memory");
                 }
                 if (cert) {
                     moved = old != j1;
@@ -1724,16 +1753,18 @@ __global__ void __launch_bounds__(320, 1)
                     lb_out = __double2float_rd(sqrt(fmax(U, 0.0)) * (1.0 - 1e-12));
                 }
             }
-            // scanned group bounds: one coalesced row segment per row (lane g
-            // writes group g)
-            __syncwarp();
-            const unsigned wm = __ballot_sync(LK_FULL_MASK, valid);
-            for (unsigned mm = wm; mm; mm &= mm - 1) {
-                const int i = __ffs(mm) - 1;
-                const int64_t row_i = __shfl_sync(LK_FULL_MASK, row, i);
-                if (lane < G && ((pm >> lane) & 1u)) S.lb[row_i * S.nlb + lane] = sgm[lane * GS + rloc0 + i];
+            // this row tile's scanned group bounds, one store per group (the
+            // row tile shares its mask: warp-uniform loop; each store writes
+            // one 4-byte entry of 32 rows' table lines)
+            if (valid) {
+                float* lbr = S.lb + row * S.nlb;
+                for (uint32_t mm = ms; mm; mm &= mm - 1) {
+                    const int g = __ffs(mm) - 1;
+                    float v;
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(sgm + g * GS + rloc)));
+                    __stcg(lbr + g, v);
+                }
             }
-            __syncwarp();
             const int64_t pos = warp_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED));
             if (moved) S.moved[pos] = make_int2((int)row, old);
             const int64_t cpos = warp_append(amb, (unsigned long long*)(stat + LK_STAT_CANDIDATE));
@@ -1751,19 +1782,19 @@ __global__ void __launch_bounds__(320, 1)
     }
 }
 
-// Union of the group masks of each 256-row pair of the sorted worklist (one
-// warp per pair).
+// Union of the group masks of each 128-row tile of the sorted worklist (one
+// warp per tile; 0 past the last tile).
 __global__ void k_pair_mask(DevState S, const int64_t* count) {
     if (*S.done) return;
     const int64_t m = *count;
-    const int64_t np = (m + 255) / 256;
+    const int64_t nt = (m + 127) / 128 + 1;
     const int lane = threadIdx.x & 31;
-    for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < np;
+    for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < nt;
          p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         uint32_t v = 0;
 #pragma unroll
-        for (int e = 0; e < 8; e++) {
-            const int64_t pos = p * 256 + e * 32 + lane;
+        for (int e = 0; e < 4; e++) {
+            const int64_t pos = p * 128 + e * 32 + lane;
             if (pos < m) v |= __ldcs(&S.tmeta[pos].mask);
         }
         v = __reduce_or_sync(LK_FULL_MASK, v);
@@ -1990,93 +2021,141 @@ __global__ void k_tile_labels(DevState S, const int64_t* count) {
 // position by a shared-memory cursor (per-block bases from k_sort_offsets)
 // and written there centered on its tile's centroid and split for 3xTF32
 // (full 128-byte lines), with its certification record (one 32-byte sector).
-// L lanes per row (float4 columns).
-template <int L>
+// Two phases per 1024-row slice of the block's chunk, so that many rows'
+// dependent loads are in flight at once:
+//   A  a thread per row (4 rows each, loads interleaved): worklist entry ->
+//      label -> sort key -> cursor (shared-memory atomic) -> tile label;
+//      (row, position, tile label, label, mask, bound) into shared memory
+//   B  8 lanes per row (one float4 column each), 4 rows per lane group in
+//      flight: the point and its tile centroid, centered split, hi/lo rows,
+//      the norms and the record.
+constexpr int kSortSlice = 1024;
+
+struct SortStage {
+    int row[kSortSlice];
+    int pos[kSortSlice];
+    int a[kSortSlice];
+    int lab[kSortSlice];
+    uint32_t mask[kSortSlice];
+    float lun[kSortSlice];
+};
+
 __global__ void __launch_bounds__(256) k_sort_gather(DevState S, const int64_t* count, const int* hist) {
     if (*S.done) return;
     extern __shared__ int sh[];
+    __shared__ SortStage st;
     const int keys = S.kcols;
     const int* h = hist + (int64_t)blockIdx.x * keys;
     for (int j = threadIdx.x; j < keys; j += blockDim.x) sh[j] = __ldg(S.lcur + j) + h[j];
     __syncthreads();
     int64_t p0, p1;
     sort_chunk(*count, gridDim.x, blockIdx.x, p0, p1);
-    const int sub = threadIdx.x & (L - 1);
+    constexpr int L = 8, RPT = kSortSlice / 256;
+    const int sub = threadIdx.x & (L - 1), grp = threadIdx.x / L;  // 32 lane groups
     const int c4n = S.ldx / 4;
     const float kap = tc_kappa_ordered(S.d);
-    const int RPB = blockDim.x / L;  // rows per block step
-    for (int64_t base = p0; base < p1; base += RPB) {
-        const int64_t p = base + threadIdx.x / L;
-        const bool ok = p < p1;
-        int row = 0, lab = 0, pos = 0, a = -1;
-        uint32_t mask = 0;
-        float lun = 0.f;
-        if (ok && sub == 0) {
-            row = __ldcs(S.work + p);
-            lab = S.labels[row];
-            mask = __ldcs(S.ymask + p);
-            lun = __ldcs(&S.ylun[p].x);
-            pos = atomicAdd(sh + sort_key(S, lab), 1);
-            a = __ldg(S.tile_lab + (pos >> 7));
-        }
-        row = __shfl_sync(LK_FULL_MASK, row, 0, L);
-        pos = __shfl_sync(LK_FULL_MASK, pos, 0, L);
-        a = __shfl_sync(LK_FULL_MASK, a, 0, L);
-        double x2 = 0.0, xo = 0.0, xx = 0.0;
-        if (ok) {
-            const float4* xp = reinterpret_cast<const float4*>(S.X32 + (int64_t)row * S.ldx);
-            const float4* op = reinterpret_cast<const float4*>(S.C32 + (int64_t)(a >= 0 ? a : 0) * S.ldc);
-            float4* hp = reinterpret_cast<float4*>(S.Xg_hi + (int64_t)pos * S.ldx);
-            float4* lp = reinterpret_cast<float4*>(S.Xg_lo + (int64_t)pos * S.ldx);
-            for (int c = sub; c < c4n; c += L) {
-                const float4 x = __ldg(xp + c);
-                const float4 o = a >= 0 ? __ldg(op + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-                const float xv[4] = {x.x, x.y, x.z, x.w};
-                const float xs[4] = {x.x - o.x, x.y - o.y, x.z - o.z, x.w - o.w};
-                const float ov[4] = {o.x, o.y, o.z, o.w};
-                float hh[4], ll[4];
+    for (int64_t base = p0; base < p1; base += kSortSlice) {
+        const int nrow = (int)(p1 - base < kSortSlice ? p1 - base : kSortSlice);
+        // ---- A: positions
+        int rw[RPT], lb[RPT];
 #pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    hh[e] = __uint_as_float(__float_as_uint(xs[e]) & 0xFFFFE000u);
-                    ll[e] = xs[e] - hh[e];
-                    x2 = fma((double)xs[e], (double)xs[e], x2);
-                    xo = fma((double)xs[e], (double)ov[e], xo);
-                    xx = fma((double)xv[e], (double)xv[e], xx);
+        for (int u = 0; u < RPT; u++) {
+            const int e = threadIdx.x + u * 256;
+            rw[u] = e < nrow ? __ldcs(S.work + base + e) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < RPT; u++) {
+            const int e = threadIdx.x + u * 256;
+            lb[u] = e < nrow ? S.labels[rw[u]] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < RPT; u++) {
+            const int e = threadIdx.x + u * 256;
+            if (e < nrow) {
+                const int pos = atomicAdd(sh + sort_key(S, lb[u]), 1);
+                st.row[e] = rw[u];
+                st.pos[e] = pos;
+                st.lab[e] = lb[u];
+                st.a[e] = __ldg(S.tile_lab + (pos >> 7));
+                st.mask[e] = __ldcs(S.ymask + base + e);
+                st.lun[e] = __ldcs(&S.ylun[base + e].x);
+            }
+        }
+        __syncthreads();
+        // ---- B: centered split rows and records, 4 rows per lane group at a time
+        // (block-uniform trip count: the 8-lane shuffles below need every
+        // lane of the warp)
+        for (int b0 = 0; b0 < nrow; b0 += 32 * 4) {
+            float4 xv[4], ov[4];
+            int er[4], ea[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = b0 + grp + u * 32;
+                er[u] = e < nrow ? e : -1;
+                ea[u] = er[u] >= 0 ? st.a[e] : -1;
+                const bool ok = er[u] >= 0 && sub < c4n;
+                xv[u] = ok ? __ldg(reinterpret_cast<const float4*>(S.X32 + (int64_t)st.row[e] * S.ldx) + sub)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                ov[u] = (ok && ea[u] >= 0) ? __ldg(reinterpret_cast<const float4*>(S.C32 + (int64_t)ea[u] * S.ldc) + sub)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = er[u];
+                double x2 = 0.0, xo = 0.0, xx = 0.0;
+                const int pos = e >= 0 ? st.pos[e] : 0;
+                if (e >= 0 && sub < c4n) {
+                    const float xa[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+                    const float oa[4] = {ov[u].x, ov[u].y, ov[u].z, ov[u].w};
+                    float hh[4], ll[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const float xs = xa[q] - oa[q];
+                        hh[q] = __uint_as_float(__float_as_uint(xs) & 0xFFFFE000u);
+                        ll[q] = xs - hh[q];
+                        x2 = fma((double)xs, (double)xs, x2);
+                        xo = fma((double)xs, (double)oa[q], xo);
+                        xx = fma((double)xa[q], (double)xa[q], xx);
+                    }
+                    __stcs(reinterpret_cast<float4*>(S.Xg_hi + (int64_t)pos * S.ldx) + sub,
+                           make_float4(hh[0], hh[1], hh[2], hh[3]));
+                    __stcs(reinterpret_cast<float4*>(S.Xg_lo + (int64_t)pos * S.ldx) + sub,
+                           make_float4(ll[0], ll[1], ll[2], ll[3]));
                 }
-                __stcs(hp + c, make_float4(hh[0], hh[1], hh[2], hh[3]));
-                __stcs(lp + c, make_float4(ll[0], ll[1], ll[2], ll[3]));
-            }
-        }
 #pragma unroll
-        for (int o = L >> 1; o > 0; o >>= 1) {
-            x2 += __shfl_xor_sync(LK_FULL_MASK, x2, o, L);
-            xo += __shfl_xor_sync(LK_FULL_MASK, xo, o, L);
-            xx += __shfl_xor_sync(LK_FULL_MASK, xx, o, L);
-        }
-        if (ok && sub == 0) {
-            TgyMeta t;
-            t.R = x2 + 2.0 * xo;
-            t.xo = __double2float_ru(sqrt(x2) * (1.0 + 1e-12));
-            t.xn2 = S.X64 ? S.xn2[row] : (float)xx;
-            float bv = INFINITY;
-            if (a >= 0 && lab == a) {
-                // upper bound on the TC value of the row's own label column (as k_gather_center)
-                const double xd = (double)t.xo, ca = (double)S.cnorm[a];
-                const double est = xd * xd - t.R;
-                const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
-                const double ea = (double)kap * xd * ca + gb * (fabs(est) + 2.0 * xd * ca) +
-                                  2.0 * 5.9604644775390625e-08 * fabs(est);
-                bv = __double2float_ru(est + 2.0 * ea + 1e-30);
+                for (int o = L >> 1; o > 0; o >>= 1) {
+                    x2 += __shfl_xor_sync(LK_FULL_MASK, x2, o, L);
+                    xo += __shfl_xor_sync(LK_FULL_MASK, xo, o, L);
+                    xx += __shfl_xor_sync(LK_FULL_MASK, xx, o, L);
+                }
+                if (e >= 0 && sub == 0) {
+                    const int a = ea[u], row = st.row[e];
+                    TgyMeta t;
+                    t.R = x2 + 2.0 * xo;
+                    t.xo = __double2float_ru(sqrt(x2) * (1.0 + 1e-12));
+                    t.xn2 = S.X64 ? S.xn2[row] : (float)xx;
+                    float bv = INFINITY;
+                    if (a >= 0 && st.lab[e] == a) {
+                        // upper bound on the TC value of the row's own label column (as k_gather_center)
+                        const double xd = (double)t.xo, ca = (double)S.cnorm[a];
+                        const double est = xd * xd - t.R;
+                        const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
+                        const double eA = (double)kap * xd * ca + gb * (fabs(est) + 2.0 * xd * ca) +
+                                          2.0 * 5.9604644775390625e-08 * fabs(est);
+                        bv = __double2float_ru(est + 2.0 * eA + 1e-30);
+                    }
+                    t.bv = bv;
+                    t.lun = st.lun[e];
+                    t.row = row;
+                    t.mask = st.mask[e];
+                    const int4* src = reinterpret_cast<const int4*>(&t);
+                    int4* dst = reinterpret_cast<int4*>(S.tmeta + pos);
+                    __stcs(dst, src[0]);
+                    __stcs(dst + 1, src[1]);
+                }
             }
-            t.bv = bv;
-            t.lun = lun;
-            t.row = row;
-            t.mask = mask;
-            const int4* src = reinterpret_cast<const int4*>(&t);
-            int4* dst = reinterpret_cast<int4*>(S.tmeta + pos);
-            __stcs(dst, src[0]);
-            __stcs(dst + 1, src[1]);
         }
+        __syncthreads();
     }
 }
 
@@ -2475,10 +2554,9 @@ lk_status launch_sort_tgy(const DevState& S, int64_t* stat, int sms, cudaStream_
     k_tile_labels<<<sms * 2, 256, 0, st>>>(S, count);
     LK_LAUNCH_CHECK();
     // (d <= 32: at most 8 float4 columns per row)
-    // four lanes per row, 8 rows of a warp in flight (the row's chain of
-    // dependent loads -- worklist, label, cursor, tile label, point -- is the
-    // limit, not the bytes); 256-thread blocks, eight per SM
-    k_sort_gather<4><<<nb, 256, hs, st>>>(S, count, S.shist);
+    // (the row's chain of dependent loads -- worklist, label, cursor, tile
+    // label, point -- is the limit, not the bytes: see k_sort_gather)
+    k_sort_gather<<<nb, 256, hs, st>>>(S, count, S.shist);
     LK_LAUNCH_CHECK();
     k_pair_mask<<<sms * 4, 256, 0, st>>>(S, count);
     LK_LAUNCH_CHECK();
