@@ -30,6 +30,25 @@ def _torch():
     return torch
 
 
+class _nvtx:
+    """NVTX range (nsys / ncu --nvtx timelines; a no-op without a profiler)."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        try:
+            _torch().cuda.nvtx.range_push(self.name)
+            self.on = True
+        except Exception:  # pragma: no cover
+            self.on = False
+        return self
+
+    def __exit__(self, *a):
+        if self.on:
+            _torch().cuda.nvtx.range_pop()
+
+
 def _world_size(comm) -> int:
     import torch.distributed as dist
     return dist.get_world_size(comm)
@@ -433,11 +452,14 @@ class DeviceLloyd:
     def step(self, t: int):
         """One iteration: assign (+recheck, +deltas), all-reduce, update."""
         st = self.stream_handle()
-        nat.check(self.lib.lk_step_assign(self.ctx, int(t), st), "lk_step_assign")
+        with _nvtx(f"lk assign t={t}"):
+            nat.check(self.lib.lk_step_assign(self.ctx, int(t), st), "lk_step_assign")
         if self.comm is not None:
             import torch.distributed as dist
-            dist.all_reduce(self.delta, group=self.comm)
-        nat.check(self.lib.lk_step_update(self.ctx, int(t), st), "lk_step_update")
+            with _nvtx(f"lk all-reduce t={t}"):
+                dist.all_reduce(self.delta, group=self.comm)
+        with _nvtx(f"lk update t={t}"):
+            nat.check(self.lib.lk_step_update(self.ctx, int(t), st), "lk_step_update")
 
     def validate(self, decayed: bool) -> dict:
         """Shadow check of the stored bounds against exact fp64 distances
@@ -563,6 +585,8 @@ class DeviceLloyd:
                     # the graph of a cached context is reused across calls
                     graphs = self.graph_ready or self.capture(2)
                 e0.record(stream)
+                nv = _nvtx(f"lk iteration {t}")
+                nv.__enter__()
                 if graphs:
                     self.replay()  # assign + update; timed as one phase
                     e1.record(stream)
@@ -582,6 +606,7 @@ class DeviceLloyd:
                         for kind, v in self.validate(True).items():
                             res["violations"].append((f"iter{t + 1}:decayed", kind, v))
                 e2.record(stream)
+                nv.__exit__()
                 chg[t - 1].copy_(self.stats[t - 1, nat.STAT["changed_global"]], non_blocking=True)
                 if t % check_every == 0 or t == T:  # (t=1 cannot converge: n rows move)
                     stream.synchronize()

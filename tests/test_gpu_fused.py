@@ -172,3 +172,30 @@ def test_history_drained_mid_run(oracle, strategy):
     ref = oracle.run_lloyd(x, k, init, t_max)
     check_trajectory(oracle, x, init, out["history"], ref["history"], f"drain {strategy}")
     assert out["converged"] == ref["converged"]
+
+
+@pytest.mark.parametrize("d,k,groups", [(40, 300, 8), (48, 500, 16), (16, 2000, 40)])
+def test_simt_multikernel_yinyang(oracle, d, k, groups):
+    """The SIMT multi-kernel Yinyang path (k_filter_yinyang -> k_yy_pairs ->
+    k_yy_merge with per-group scans), taken for d > 32 or more than 32 groups
+    on kernel="simt": the oracle's trajectory."""
+    from paper_2010_06654_b200.device import DeviceLloyd
+    rng = np.random.default_rng(d + k)
+    c = rng.uniform(-25, 25, size=(k // 4, d))
+    x = (c[rng.integers(0, k // 4, 12000)] + rng.normal(0, 1.5, size=(12000, d))).astype(np.float32)
+    m = __import__("paper_2010_06654_b200")
+    init = m.make_init(m.RunContext(seed=d), x, k, "random")
+    ref = oracle.run_lloyd(x, k, init, 8)
+    eng = DeviceLloyd(x, k, "yinyang", 8, kernel="simt", groups=groups)
+    try:
+        assert not eng.group_cap == 128  # not the group-tile path
+        out = eng.run(init)
+        hist = out["history"]
+        assert len(hist) == ref["iterations"]
+        from test_gpu_parity import check_trajectory, centroid_ok
+        check_trajectory(oracle, x, init, hist, ref["history"], f"simt yinyang d={d} t={groups}")
+        assert centroid_ok(out["centroids"], ref["centroids"], x)
+        # the group scans ran (not only full rescans)
+        assert sum(r.group_dists for r in out["records"][1:]) > 0
+    finally:
+        eng.close()
