@@ -902,7 +902,9 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             }
             ProfScope p(c, 0, st);
             // full rescans: capacity overflow, or every failing row when full_only
-            s = use_tc ? lkh::launch_assign_tc_centered(S, S.work, stat + LK_STAT_WORK, stat, n,
+            s = (use_tc && !S.center) ? lkh::launch_assign_tc_adaptive(S, S.work, stat + LK_STAT_WORK, stat,
+                                                                     n, c->sms, st)
+                : use_tc ? lkh::launch_assign_tc_centered(S, S.work, stat + LK_STAT_WORK, stat, n,
                                                         false, c->sms, st)
                        : lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
             if (s != LK_OK) return s;
@@ -915,7 +917,9 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
                 if (s != LK_OK) return s;
             }
             ProfScope p(c, 0, st);
-            s = use_tc ? lkh::launch_assign_tc_centered(S, S.work, stat + LK_STAT_WORK, stat, n,
+            s = (use_tc && !S.center) ? lkh::launch_assign_tc_adaptive(S, S.work, stat + LK_STAT_WORK, stat,
+                                                                     n, c->sms, st)
+                : use_tc ? lkh::launch_assign_tc_centered(S, S.work, stat + LK_STAT_WORK, stat, n,
                                                         false, c->sms, st)
                        : lkh::launch_assign_simt(S, S.work, stat + LK_STAT_WORK, stat, n, c->sms, st);
             if (s != LK_OK) return s;

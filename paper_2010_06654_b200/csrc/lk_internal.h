@@ -72,6 +72,10 @@ lk_status launch_filter_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaS
 lk_status launch_sort_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_assign_tgy(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
                             cudaStream_t st);
+// worklist rescan or, when the list holds most rows, one dense pass (device-chosen)
+lk_status launch_assign_tc_adaptive(const lk::DevState& S, const int32_t* rowlist,
+                                    const int64_t* rowcount, int64_t* stat, int64_t max_rows, int sms,
+                                    cudaStream_t st);
 lk_status launch_assign_tc(const lk::DevState& S, const int32_t* rowlist,
                            const int64_t* rowcount, int64_t* stat, int64_t max_rows, int sms,
                            cudaStream_t st);

@@ -343,6 +343,12 @@ struct TcArgs {
     int dbg;              // timing probe only (wrong labels): 1 = no epilogue work, 2 = no MMAs
     int kouter;           // K-outer MMA order when the centroid tiles fit the TMEM buffers
     const int64_t* rowcount;  // device row count (overrides m when non-null)
+    // device-side choice between a worklist pass and a dense pass over every
+    // row (launch_assign_tc_adaptive): gate 1 runs only if *gate_cnt > gate_thr,
+    // gate 2 only if *gate_cnt <= gate_thr, 0 always
+    const int64_t* gate_cnt;
+    int64_t gate_thr;
+    int gate;
     int n_ct;             // centroid tiles
     int n_kc;             // K chunks
     // collect mode
@@ -367,6 +373,7 @@ __global__ void __launch_bounds__(TcShape<SPLIT>::THREADS, 1)
                 const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                 DevState S, TcArgs A, int64_t* stat) {
     if (*S.done) return;
+    if (A.gate && ((*A.gate_cnt > A.gate_thr) != (A.gate == 1))) return;
     using SM = Smem<BN, ARES>;
     // ORD (d <= 32, one K chunk): one accumulator, every cross-term MMA before
     // the hi*hi MMAs -- the cross phase accumulates at 2^-10 of the final
@@ -1823,10 +1830,13 @@ __global__ void k_split_points(DevState S) {
 }
 
 // Gather worklist rows into the contiguous rescan buffers (hi = x, lo = split).
-__global__ void k_gather_rows(DevState S, const int32_t* rows, const int64_t* count) {
-    // rows: worklist of global row ids; count: device length
+__global__ void k_gather_rows(DevState S, const int32_t* rows, const int64_t* count,
+                              int64_t dense_thr = -1) {
+    // rows: worklist of global row ids; count: device length; dense_thr >= 0:
+    // nothing to gather when the list is long (the dense pass runs instead)
     if (*S.done) return;
     const int64_t m = *count;
+    if (dense_thr >= 0 && m > dense_thr) return;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     for (int64_t r = warp; r < m; r += nwarps) {
@@ -2536,6 +2546,31 @@ lk_status launch_assign_tc_centered(const DevState& S, const int32_t* rowlist,
     A.center = 1;
     A.sbeta = 1;  // (dropped by launch_mode when the double buffer does not fit)
     return launch_mode<kTop2>(S, S.Xg_hi, S.Xg_lo, A, max_rows, stat, sms, st);
+}
+
+// Rescan of the bound filter's worklist, or -- when most rows failed their
+// bounds (d = 128 Gaussian-mixture rows: every row) -- one dense pass over all
+// rows without the gather: both are launched, the device count picks (a pass
+// over rows whose bounds held re-certifies them: same labels, fresh bounds).
+// Worklist pass up to 70% of the rows (gather + 0.7 pass ~ one dense pass).
+lk_status launch_assign_tc_adaptive(const DevState& S, const int32_t* rowlist, const int64_t* rowcount,
+                                    int64_t* stat, int64_t max_rows, int sms, cudaStream_t st) {
+    const int64_t thr = (S.n * 7) / 10;
+    k_gather_rows<<<sms * 8, 256, 0, st>>>(S, rowlist, rowcount, thr);
+    LK_LAUNCH_CHECK();
+    TcArgs A = {};
+    A.rowlist = rowlist;
+    A.rowcount = rowcount;
+    A.gate_cnt = rowcount;
+    A.gate_thr = thr;
+    A.gate = 2;
+    lk_status s = launch_mode<kTop2>(S, S.Xg_hi, S.Xg_lo, A, max_rows, stat, sms, st);
+    if (s != LK_OK) return s;
+    TcArgs B = {};
+    B.gate_cnt = rowcount;
+    B.gate_thr = thr;
+    B.gate = 1;
+    return launch_mode<kTop2>(S, S.X32, S.Xlo, B, S.n, stat, sms, st);
 }
 
 // Block-sparse Yinyang pass over the filter's worklist (stat[LK_STAT_WORK]
