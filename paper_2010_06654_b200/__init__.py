@@ -12,6 +12,7 @@ from .engine import BOUND_STRATEGIES, INDEX_MODES, KnobConfig, run_engine
 from .lloyd import IterationStats, RunResult, run_lloyd
 from .pruners import STRATEGIES, run_pruner
 from .runlog import RunLog, read_runlogs, runlog_from_result, write_runlogs
+from .harness import load_dataset, make_report, run_benchmark, summarize
 
 __version__ = "0.1.0"
 
@@ -26,13 +27,17 @@ __all__ = [
     "RunLog",
     "RunResult",
     "STRATEGIES",
+    "load_dataset",
     "make_init",
+    "make_report",
     "read_runlogs",
     "run_engine",
     "run_lloyd",
+    "run_benchmark",
     "run_pruner",
     "runlog_from_result",
     "sse",
+    "summarize",
     "write_runlogs",
     "__version__",
 ]
