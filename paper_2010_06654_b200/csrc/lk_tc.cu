@@ -1104,6 +1104,7 @@ __global__ void __launch_bounds__(320, 1)
                  const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                  DevState S, TcArgs A, int64_t* stat) {
     if (*S.done) return;
+    if (A.gate && ((*A.gate_cnt > A.gate_thr) != (A.gate == 1))) return;  // (launch_assign_tc_adaptive)
     using SM = Tc2Smem;
     constexpr int BN = 128, NBUF = 2, PW = 8, MW = 9;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
