@@ -41,7 +41,7 @@ enum InternalBuf {
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
     B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB,
-    B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_VALID, B_CCH, B_RGSCR, B_RGMEANS, B_COUNT_
+    B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_VALID, B_CCH, B_RGSCR, B_RGMEANS, B_DCUMCOL, B_COUNT_
 };
 
 struct Layout {
@@ -210,6 +210,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_PMASK] = (uint64_t)(n / 128 + 4) * 4;  // per 128-row tile
         L->size[B_SHIST] = (uint64_t)1536 * kpad * 4;  // (<= 1536 sort blocks)
         L->size[B_DCUM] = (uint64_t)k * 4;
+        L->size[B_DCUMCOL] = (uint64_t)kpad * 4;
         L->size[B_DGCUM] = (uint64_t)L->groups * 4;
         L->size[B_GLB] = (uint64_t)n * 4;
     } else if (group_mode(c)) {
@@ -522,6 +523,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
         S.sgate = e ? (atoi(e) != 0) : 1;
     }
     S.dcum = buf<float>(c, B_DCUM);
+    S.dcum_col = buf<float>(c, B_DCUMCOL);
     S.dgcum = buf<float>(c, B_DGCUM);
     S.glb = buf<float>(c, B_GLB);
     S.self = buf<lk::DevState>(c, B_SELF);
@@ -775,6 +777,7 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     LK_CUDA_CHECK(cudaMemsetAsync(S.sse, 0, c->L.size[B_SSE], st));
     LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
     if (S.tgy || S.elkan) LK_CUDA_CHECK(cudaMemsetAsync(S.lb, 0, c->L.size[B_LB], st));  // bounds >= 0
+    if (S.dcum_col) LK_CUDA_CHECK(cudaMemsetAsync(S.dcum_col, 0, c->L.size[B_DCUMCOL], st));
     if (S.lazy) {
         LK_CUDA_CHECK(cudaMemsetAsync(S.dcum, 0, c->L.size[B_DCUM], st));
         LK_CUDA_CHECK(cudaMemsetAsync(S.dgcum, 0, c->L.size[B_DGCUM], st));

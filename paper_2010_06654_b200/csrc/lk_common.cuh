@@ -125,6 +125,7 @@ struct DevState {
     float* dcum;            // [k] cumulative centroid drift (rounded up)
     float* dgcum;           // [t] cumulative group drift (rounded up); scal[4] = cumulative max drift
     float* glb;             // [n] stored global lower bound (min over the groups)
+    float* dcum_col;        // [kpad] group tiles: dcum of each B column (the pass's ub store)
     // block-sparse Yinyang on the tensor cores (lk_tgy.cu, k_assign_tgy):
     // groups are 128-column tiles of the B operand (centroids in group order)
     int32_t tgy;            // 1: the group-tile path is on

@@ -820,7 +820,11 @@ __device__ __forceinline__ void update_centroid_warp(const DevState& S, int j, c
         S.qsum[j] = qs;
         const float dj = drift2 > 0.0 ? __double2float_ru(sqrt(drift2) * (1.0 + 1e-12)) : 0.f;
         S.drift[j] = dj;
-        if (S.lazy) S.dcum[j] = __fadd_ru(S.dcum[j], dj);
+        if (S.lazy) {
+            const float dc = __fadd_ru(S.dcum[j], dj);
+            S.dcum[j] = dc;
+            if (S.dcum_col) S.dcum_col[cj] = dc;
+        }
         S.cnorm[j] = __double2float_ru(sqrt(cn2) * (1.0 + 1e-12));
         sse_part[j] = cnt > 0 ? ((double)qs * qinv[S.d] - s2 / (double)cnt) : 0.0;
         // the delta payload is consumed: zero it for the next iteration

@@ -21,6 +21,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdio.h>
+#include <string.h>
 #include <stdlib.h>
 
 #include "lk_common.cuh"
@@ -349,6 +351,7 @@ struct TcArgs {
     const int64_t* gate_cnt;
     int64_t gate_thr;
     int gate;
+    unsigned long long* prof;  // k_assign_tgy phase clocks (LK_TGY_PROF debug knob), null: off
     int n_ct;             // centroid tiles
     int n_kc;             // K chunks
     // collect mode
@@ -1394,6 +1397,59 @@ __device__ __forceinline__ float tgy_lower(double R, double xo, double kx_cmax, 
     return __fsqrt_rd(__double2float_rd(fmax(L, 0.0)));
 }
 
+// The same lower bound in fp32 with directed rounding (the per-group rewrite of
+// k_assign_tgy: fp64 and its conversions dominated the pair's tail).  Every
+// step rounds toward a smaller result: R_lo <= R, the error terms are rounded
+// up, the sums / differences down, so the value never exceeds the fp64 form's
+// exact counterpart; it is a little weaker (an fp32 rounding of R + v).
+struct TgyLow {
+    float R_lo, R_hi;   // R rounded down / up
+    float xo;           // |x'| (already rounded up)
+    float kxc;          // kappa |x'| cmax, rounded up
+    float gbx;          // gb * 2 |x'| cmax, rounded up
+    float gb;           // (d + 4) u
+    float slack;        // |R| 1e-12 + 2^-126, rounded up
+};
+
+__device__ __forceinline__ TgyLow tgy_low_setup(double R, double xo, float kappa, float cmax, int d) {
+    TgyLow t;
+    t.R_lo = __double2float_rd(R);
+    t.R_hi = __double2float_ru(R);
+    t.xo = (float)xo;  // (xo holds an fp32 value)
+    t.kxc = __fmul_ru(__fmul_ru(kappa, t.xo), cmax);
+    t.gb = (float)(d + 4) * 5.9604644775390625e-08f;
+    t.gbx = __fmul_ru(t.gb, __fmul_ru(__fmul_ru(2.0f, t.xo), cmax));
+    t.slack = __fmaf_ru(fabsf(t.R_hi), 1e-12f, 1.2e-38f);
+    return t;
+}
+
+// Square roots bounded from below / above: the correctly rounded sqrtf (within
+// half an ulp) moved one ulp down / up -- cheaper than the directed-rounding
+// __fsqrt_rd / __fsqrt_ru sequences.
+__device__ __forceinline__ float sqrt_lo(float x) {
+    if (!(x > 0.f)) return 0.f;
+    const float r = sqrtf(x);
+    return isinf(r) ? r : __int_as_float(__float_as_int(r) - 1);
+}
+__device__ __forceinline__ float sqrt_hi(float x) {
+    if (!(x > 0.f)) return 0.f;
+    const float r = sqrtf(x);
+    return isinf(r) ? r : __int_as_float(__float_as_int(r) + 1);
+}
+
+__device__ __forceinline__ float tgy_lower32(const TgyLow& t, float v) {
+    if (isinf(v)) return INFINITY;
+    const float av = fabsf(v);
+    // eo = kappa |x'| cmax + gb (|v| + 2 |x'| cmax) + 2u |v|   (rounded up)
+    const float eo = __fadd_ru(__fadd_ru(t.kxc, __fmaf_ru(t.gb, av, t.gbx)), __fmul_ru(1.1920928955078125e-07f, av));
+    // ex = 2^-22 |x'| (sqrt(R + v + eo) + |x'|)                  (rounded up)
+    const float sr = sqrt_hi(__fadd_ru(__fadd_ru(t.R_hi, v), eo));
+    const float ex = __fmul_ru(__fmul_ru(2.384185791015625e-07f, t.xo), __fadd_ru(sr, t.xo));
+    // L = R + v - eo - ex - slack                               (rounded down)
+    const float L = __fsub_rd(__fsub_rd(__fsub_rd(__fadd_rd(t.R_lo, v), eo), ex), t.slack);
+    return sqrt_lo(L);
+}
+
 // Shared memory of k_assign_tgy: the k_assign_tc2 stages and resident A, a ring
 // of per-tile beta slices (the two row tiles' 128 offsets of the staged
 // centroid tile: the producer never waits for a whole pair's epilogue), the
@@ -1410,8 +1466,27 @@ struct TgySmem {
     static constexpr int DG_OFF = RING_OFF + NBB * 1024;
     static constexpr int GM_OFF = DG_OFF + 32 * 4;
     static constexpr int GS = 257;                       // per-group row stride of the minima
-    static constexpr int TOTAL = GM_OFF + 1024;          // (+ G * GS * 4 at launch)
+    static constexpr int TOTAL = GM_OFF + 1024;          // (+ G * GS * 4 + kpad * 4 at launch:
+                                                         //  the minima, the column norms)
 };
+
+// Phase clocks of k_assign_tgy (debug knob LK_TGY_PROF): cycles each role spends
+// waiting on each barrier / computing, summed over lane 0 of the role warps.
+enum TgyProf {
+    TP_P_AEMPTY, TP_P_EMPTY, TP_P_REMPTY, TP_P_TOTAL, TP_M_AFULL, TP_M_TEMPTY, TP_M_FULL, TP_M_TOTAL,
+    TP_E_TFULL, TP_E_RFULL, TP_E_TILES, TP_E_TAIL, TP_E_TOTAL, TP_PAIRS, TP_TILES,
+    TP_T_CERT, TP_T_GROUPS, TP_T_STORES, TP_T_APPEND, TP_N
+};
+#define TGY_W(idx, call)                                        \
+    do {                                                        \
+        if (prof_on) {                                          \
+            const long long t0_ = clock64();                    \
+            call;                                               \
+            pc[idx] += clock64() - t0_;                         \
+        } else {                                                \
+            call;                                               \
+        }                                                       \
+    } while (0)
 
 // A pair's centroid tiles run starting from the group of its first row tile's
 // label (then in increasing group order, wrapping): rows mostly belong to that
@@ -1448,10 +1523,16 @@ __global__ void __launch_bounds__(320, 1)
     float* ring = (float*)(smem + SM::RING_OFF);  // [NBB][2][128]
     float* sdg = (float*)(smem + SM::DG_OFF);     // [32] cumulative group drifts
     float* sgm = (float*)(smem + SM::GM_OFF);     // [G][GS]: per group, the pair's 256 rows
+    float* scn = sgm + S.t_groups * GS;           // [kpad] |c| of each B column (+inf padding)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = S.t_groups;
     const int64_t m = *A.rowcount;
+    const bool prof_on = A.prof != nullptr;
+    long long pc[TP_N];
+#pragma unroll
+    for (int e = 0; e < TP_N; e++) pc[e] = 0;
+    const long long tk0 = prof_on ? clock64() : 0;
     const int64_t n_rt = (m + BM - 1) / BM;
     const int64_t n_rp = (n_rt + 1) / 2;
     auto beta_of = [&](int64_t t_) -> const float* {
@@ -1483,6 +1564,10 @@ __global__ void __launch_bounds__(320, 1)
         prefetch_map(&map_blo);
     }
     if (threadIdx.x < 32) sdg[threadIdx.x] = threadIdx.x < G ? S.dgcum[threadIdx.x] : 0.f;
+    for (int c = threadIdx.x; c < S.kpad; c += blockDim.x) {
+        const int j = col_id(S, c);
+        scn[c] = j >= 0 ? S.cnorm[j] : S.scal[0];
+    }
     if (warp == MW) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
@@ -1504,7 +1589,7 @@ __global__ void __launch_bounds__(320, 1)
             for (int it = 0; it < n_it; it++) {
                 const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
                 const uint32_t pm = __ldg(S.pmask + 2 * rp) | __ldg(S.pmask + 2 * rp + 1);
-                mbar_wait(aempty, (it & 1) ^ 1);
+                TGY_W(TP_P_AEMPTY, mbar_wait(aempty, (it & 1) ^ 1));
                 mbar_expect_tx(afull, 4 * SM::A_BYTES);
 #pragma unroll
                 for (int s = 0; s < 2; s++) {
@@ -1517,7 +1602,7 @@ __global__ void __launch_bounds__(320, 1)
                 const int g0 = tgy_rot(S, 2 * rp);
                 for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
                     const int ct = (__ffs(mm) - 1 + g0) & 31;
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    TGY_W(TP_P_EMPTY, mbar_wait(&empty[stage], phase ^ 1));
                     uint8_t* bst = smem + stage * SM::STAGE_BYTES;
                     mbar_expect_tx(&full[stage], SM::STAGE_BYTES);
 #pragma unroll
@@ -1527,7 +1612,7 @@ __global__ void __launch_bounds__(320, 1)
                                     ct * BN + (q & 1) * (BN / 2));
                     }
                     if (++stage == SM::STAGES) { stage = 0; phase ^= 1; }
-                    mbar_wait(&rempty[rs], rphase ^ 1);
+                    TGY_W(TP_P_REMPTY, mbar_wait(&rempty[rs], rphase ^ 1));
                     mbar_expect_tx(&rfull[rs], 1024);
                     bulk_load(ring + rs * 256, bt0 + ct * BN, 512, &rfull[rs]);
                     bulk_load(ring + rs * 256 + 128, bt1 + ct * BN, 512, &rfull[rs]);
@@ -1551,13 +1636,13 @@ __global__ void __launch_bounds__(320, 1)
             const int64_t r0n = m - 2 * rp * BM < BM ? m - 2 * rp * BM : BM;
             const int64_t r1n = m - (2 * rp + 1) * BM < BM ? (m - (2 * rp + 1) * BM > 0 ? m - (2 * rp + 1) * BM : 0) : BM;
             n_dist += 128 * (r0n * __popc(m0) + r1n * __popc(m1));
-            mbar_wait(afull, it & 1);
+            TGY_W(TP_M_AFULL, mbar_wait(afull, it & 1));
             tc_fence_after();
             const int g0 = tgy_rot(S, 2 * rp);
             for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                TGY_W(TP_M_TEMPTY, mbar_wait(&tempty[acc], acc_phase ^ 1));
                 tc_fence_after();
-                mbar_wait(&full[stage], phase);
+                TGY_W(TP_M_FULL, mbar_wait(&full[stage], phase));
                 tc_fence_after();
                 uint8_t* bst = smem + stage * SM::STAGE_BYTES;
                 const uint64_t dbhi = umma_desc(bst);
@@ -1595,10 +1680,23 @@ __global__ void __launch_bounds__(320, 1)
         const float kappa = tc_kappa_ordered(S.d);
         const float dm = S.scal[4];
         const float cmax_f = S.scal[0];
+        __shared__ unsigned long long escr[9];
         int acc = 0, rs = 0;
         uint32_t acc_phase = 0, rphase = 0;
         const int rloc0 = s * BM + q * 32;   // this warp's first row in the pair
         const int rloc = rloc0 + lane;
+        // the rows' certification records (and labels) are loaded one pair ahead
+        int4 mw0 = make_int4(0, 0, 0, 0), mw1 = mw0;
+        int old_n = 0;
+        auto load_meta = [&](int it_) {
+            const int64_t r_ = (2 * (blockIdx.x + (int64_t)it_ * gridDim.x) + s) * BM + q * 32 + lane;
+            if (it_ < n_it && r_ < m) {
+                const int4* src = reinterpret_cast<const int4*>(S.tmeta + r_);
+                mw0 = __ldcs(src);
+                mw1 = __ldcs(src + 1);
+            }
+        };
+        load_meta(0);
         for (int it = 0; it < n_it; it++) {
             const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
             // the pair's tiles stream in for the union of the two row tiles'
@@ -1616,10 +1714,7 @@ __global__ void __launch_bounds__(320, 1)
             float lun = 0.f, xn2 = 0.f;
             int old = 0;
             if (valid) {
-                const int4* src = reinterpret_cast<const int4*>(S.tmeta + r);
-                int4 w[2];
-                w[0] = __ldcs(src);
-                w[1] = __ldcs(src + 1);
+                int4 w[2] = {mw0, mw1};
                 const TgyMeta& t = *reinterpret_cast<const TgyMeta*>(w);
                 row = t.row;
                 R = t.R;
@@ -1627,14 +1722,17 @@ __global__ void __launch_bounds__(320, 1)
                 lun = t.lun;
                 xn2 = t.xn2;
                 bv = t.bv;
-                old = S.labels[row];
+                old = S.labels[row];  // (used in the tail only)
             }
+            load_meta(it + 1);
             const int g0 = tgy_rot(S, 2 * rp);
             for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
                 const int ct = (__ffs(mm) - 1 + g0) & 31;
-                mbar_wait(&tfull[acc], acc_phase);
+                TGY_W(TP_E_TFULL, mbar_wait(&tfull[acc], acc_phase));
                 tc_fence_after();
-                mbar_wait(&rfull[rs], rphase);
+                TGY_W(TP_E_RFULL, mbar_wait(&rfull[rs], rphase));
+                const long long tt0 = prof_on ? clock64() : 0;
+                pc[TP_TILES]++;
                 const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 2 * BN + s * BN;
                 const uint32_t sb0 = smem_u32(ring + rs * 256 + s * 128);
                 float gmin = INFINITY;
@@ -1714,56 +1812,72 @@ __global__ void __launch_bounds__(320, 1)
                 }
                 if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
                 if (++rs == NBB) { rs = 0; rphase ^= 1; }
+                if (prof_on) pc[TP_E_TILES] += clock64() - tt0;
             }
-            const int j1 = (bj >= 0 && bv == b1) ? col_id(S, bj) : -1;
+            const long long tl0 = prof_on ? clock64() : 0;
+            pc[TP_PAIRS]++;
+            // the winning column (searched and holding the minimum), its centroid
+            // id and cumulative drift: both loads go out before the math
+            const int jc = (bj >= 0 && bv == b1) ? bj : -1;
+            const int j1 = jc >= 0 ? col_id(S, jc) : -1;
+            const float dcj = jc >= 0 ? __ldg(S.dcum_col + jc) : 0.f;
             bool moved = false, amb = false, cert = false;
             float thr_out = 0.f, lb_out = 0.f;
             if (valid) {
-                const double cmax = (double)cmax_f;
-                const double cn1 = j1 >= 0 ? (double)S.cnorm[j1] : cmax;
-                const double gb = (double)(S.d + 4) * 5.9604644775390625e-08;
-                const double ab1 = fabs((double)b1);
-                const double e1 = (double)kappa * xo * cn1 + gb * (ab1 + 2.0 * xo * cn1) +
-                                  2.0 * 5.9604644775390625e-08 * ab1;
-                const float sr1 = __fsqrt_ru(__double2float_ru(fmax(R + (double)b1 + e1, 0.0)));
-                const double ex1 = 2.384185791015625e-07 * xo * ((double)sr1 + xo);
-                const double U = (R + (double)b1 + e1 + ex1) * (1.0 + 1e-12) + 1e-300;
-                const float Ud = __fsqrt_ru(__double2float_ru(fmax(U, 0.0)));
-                const double kxc = (double)kappa * xo * cmax;
-                const float L2d = tgy_lower(R, xo, kxc, gb, cmax, b2);
+                // certification in fp32 with directed rounding (tgy_lower32's scheme:
+                // upper bounds rounded up, lower bounds down; R split into R_lo / R_hi)
+                const TgyLow tl = tgy_low_setup(R, xo, kappa, cmax_f, S.d);
+                const float cn1 = jc >= 0 ? scn[jc] : cmax_f;  // (|c| of the winner's column)
+                const float ab1 = fabsf(b1);
+                // e1 = kappa |x'| |c1| + gb (|b1| + 2 |x'| |c1|) + 2u |b1|        (up)
+                const float xc1 = __fmul_ru(tl.xo, cn1);
+                const float e1 = __fadd_ru(__fadd_ru(__fmul_ru(kappa, xc1),
+                                                     __fmul_ru(tl.gb, __fmaf_ru(2.0f, xc1, ab1))),
+                                           __fmul_ru(1.1920928955078125e-07f, ab1));
+                const float sr1 = sqrt_hi(__fadd_ru(__fadd_ru(tl.R_hi, b1), e1));
+                const float ex1 = __fmul_ru(__fmul_ru(2.384185791015625e-07f, tl.xo), __fadd_ru(sr1, tl.xo));
+                // U >= (R + b1 + e1 + ex1): the squared distance of the best column, from above
+                const float U = __fadd_ru(__fadd_ru(__fadd_ru(__fadd_ru(tl.R_hi, b1), e1), ex1), tl.slack);
+                const float Ud = sqrt_hi(U);
+                const float L2d = tgy_lower32(tl, b2);
                 // the winner beats every other scanned column and every unscanned group
-                cert = j1 >= 0 && L2d > Ud && lun > Ud && !isinf(b1);
-                const int g1 = cert ? S.group_of[j1] : -1;
+                cert = jc >= 0 && L2d > Ud && lun > Ud && !isinf(b1);
+                // (the winner's group is its tile: B columns are in group order)
+                const int g1 = cert ? (jc >> 7) : -1;
+                if (prof_on) pc[TP_T_CERT] += clock64() - tl0;
                 // every scanned group's bound (lazy encoding): its minimum bounds
                 // all its members, whichever wins; a certified row's winner group
-                // gets the second best (its other members)
+                // gets the second best (its other members).  (Rewriting only the
+                // row's own failing groups was measured: the tile's other groups
+                // then keep older, weaker bounds and fail later -- 1.3e10 ->
+                // 1.75e10 products at cfg5 iteration 20.)
                 for (uint32_t mm = ms; mm; mm &= mm - 1) {
                     const int g = __ffs(mm) - 1;
                     const uint32_t sa = smem_u32(sgm + g * GS + rloc);
                     float raw;
-                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(raw) : "r"(sa) : "memory");
-                    const float v = g == g1 ? L2d : tgy_lower(R, xo, kxc, gb, cmax, raw);
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(sa), "f"(__fadd_rd(v, sdg[g])) : "memory");
+                    asm("ld.shared.f32 %0, [%1];" : "=f"(raw) : "r"(sa));
+                    const float v = g == g1 ? L2d : tgy_lower32(tl, raw);
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(sa), "f"(__fadd_rd(v, sdg[g])));
                 }
+                if (prof_on) pc[TP_T_GROUPS] += clock64() - tl0;
                 if (cert) {
                     moved = old != j1;
                     if (moved) S.labels[row] = j1;
-                    S.ub[row] = __fsub_ru(Ud, S.dcum[j1]);
+                    S.ub[row] = __fsub_ru(Ud, dcj);
                     S.glb[row] = __fadd_rd(fminf(L2d, lun), dm);
                 } else {
                     amb = true;
-                    const double xn = (double)(sqrtf(xn2) * (1.0f + 2 * kU32));
-                    const double eunc = (double)kappa * xn * cmax + 8.0 * 5.9604644775390625e-08 *
-                                        ((double)xn2 + cmax * cmax);
-                    const double thr = (U - (double)xn2 * (1.0 - 2.384185791015625e-07) + eunc) *
-                                       (1.0 + 1e-9) + 1e-30;
-                    thr_out = __double2float_ru(thr);
-                    lb_out = __double2float_rd(sqrt(fmax(U, 0.0)) * (1.0 - 1e-12));
+                    // thresholds of the (uncentered) collect pass: every possible winner
+                    // has D'unc <= U - |x|^2 + e_unc (tc_certify's bound, rounded up)
+                    const float xn = __fmul_ru(sqrtf(xn2), 1.0f + 4 * kU32);
+                    const float eunc = __fadd_ru(__fmul_ru(__fmul_ru(kappa, xn), cmax_f),
+                                                 __fmul_ru(8.0f * kU32, __fmaf_ru(cmax_f, cmax_f, xn2)));
+                    const float thr = __fadd_ru(__fadd_ru(U, -__fmul_rd(xn2, 1.0f - 2.384185791015625e-07f)), eunc);
+                    thr_out = __fadd_ru(__fmaf_ru(fabsf(thr), 1e-9f, thr), 1e-30f);
+                    lb_out = sqrt_lo(U);
                 }
             }
-            // this row tile's scanned group bounds, one store per group (the
-            // row tile shares its mask: warp-uniform loop; each store writes
-            // one 4-byte entry of 32 rows' table lines)
+            // the rewritten group bounds, one 4-byte store per group
             if (valid) {
                 float* lbr = S.lb + row * S.nlb;
                 for (uint32_t mm = ms; mm; mm &= mm - 1) {
@@ -1773,15 +1887,30 @@ __global__ void __launch_bounds__(320, 1)
                     __stcg(lbr + g, v);
                 }
             }
-            const int64_t pos = warp_append(moved, (unsigned long long*)(stat + LK_STAT_CHANGED));
+            if (prof_on) pc[TP_T_STORES] += clock64() - tl0;
+            // one global atomic per CTA and list (all 148 CTAs append to the same two
+            // counters: per-warp atomics serialize in their L2 slice)
+            const int64_t pos = epi_append8(moved, (unsigned long long*)(stat + LK_STAT_CHANGED), escr, warp);
             if (moved) S.moved[pos] = make_int2((int)row, old);
-            const int64_t cpos = warp_append(amb, (unsigned long long*)(stat + LK_STAT_CANDIDATE));
+            const int64_t cpos = epi_append8(amb, (unsigned long long*)(stat + LK_STAT_CANDIDATE), escr, warp);
             if (amb) {
                 S.cand_rows[cpos] = (int)row;
                 S.cand_thr[cpos] = thr_out;
                 S.cand_lb[cpos] = lb_out;
             }
+            if (prof_on) {
+                pc[TP_E_TAIL] += clock64() - tl0;
+                pc[TP_T_APPEND] += clock64() - tl0;
+            }
         }
+    }
+    if (prof_on && lane == 0 && (warp == PW || warp == MW || warp == 0)) {
+        const long long tot = clock64() - tk0;
+        if (warp == PW) pc[TP_P_TOTAL] = tot;
+        if (warp == MW) pc[TP_M_TOTAL] = tot;
+        if (warp == 0) pc[TP_E_TOTAL] = tot;
+        for (int e = 0; e < TP_N; e++)
+            if (pc[e]) atomicAdd(A.prof + e, (unsigned long long)pc[e]);
     }
     __syncthreads();
     if (warp == MW) {
@@ -2318,7 +2447,7 @@ static int tc_max_dyn_smem() { return g_tc_max_dyn; }
 static int g_tgy_max_dyn = 0;
 static int tc_max_dyn_smem_tgy() { return g_tgy_max_dyn; }
 // k_assign_tgy: the k_assign_tc2 layout + the pair's per-group minima
-static int tgy_smem(const DevState& S) { return TgySmem::TOTAL + S.t_groups * TgySmem::GS * 4; }
+static int tgy_smem(const DevState& S) { return TgySmem::TOTAL + S.t_groups * TgySmem::GS * 4 + S.kpad * 4; }
 
 template <int BN, int MODE, bool SPLIT, bool ARES, int CL = 1>
 static lk_status tc_attr(int optin) {
@@ -2574,6 +2703,31 @@ lk_status launch_assign_tc_adaptive(const DevState& S, const int32_t* rowlist, c
     return launch_mode<kTop2>(S, S.X32, S.Xlo, B, S.n, stat, sms, st);
 }
 
+// LK_TGY_PROF=1 (debug knob): k_assign_tgy accumulates its phase clocks into a
+// managed buffer, printed to stderr at exit (tgy_prof_dump).
+static unsigned long long* g_tgy_prof = nullptr;
+static void tgy_prof_dump() {
+    if (!g_tgy_prof) return;
+    cudaDeviceSynchronize();
+    static const char* names[] = {"P_aempty", "P_empty", "P_rempty", "P_total", "M_afull", "M_tempty",
+                                  "M_full", "M_total", "E_tfull", "E_rfull", "E_tiles", "E_tail",
+                                  "E_total", "pairs(warp0)", "tiles(warp0)", "T_cert", "T_groups",
+                                  "T_stores", "T_append"};
+    fprintf(stderr, "k_assign_tgy phase clocks (sum over CTAs, lane 0 of producer / MMA / epilogue warp 0):");
+    for (int e = 0; e < TP_N; e++) fprintf(stderr, " %s=%llu", names[e], g_tgy_prof[e]);
+    fprintf(stderr, "\n");
+}
+static unsigned long long* tgy_prof_buffer() {
+    static const int on = env_int("LK_TGY_PROF", 0);
+    if (!on) return nullptr;
+    if (!g_tgy_prof) {
+        if (cudaMallocManaged(&g_tgy_prof, 64 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+        memset(g_tgy_prof, 0, 64 * sizeof(unsigned long long));
+        atexit(tgy_prof_dump);
+    }
+    return g_tgy_prof;
+}
+
 // Block-sparse Yinyang pass over the filter's worklist (stat[LK_STAT_WORK]
 // rows, masks in S.ymask): label sort, pair masks, centered gather, then the
 // (row-tile pair x group tile) MMAs of k_assign_tgy.
@@ -2615,6 +2769,7 @@ lk_status launch_assign_tgy(const DevState& S, int64_t* stat, int64_t max_rows, 
     A.center = 1;
     A.n_kc = 1;
     A.n_ct = S.t_groups;
+    A.prof = tgy_prof_buffer();
     const int smem = tgy_smem(S);
     if (smem > tc_max_dyn_smem_tgy()) {
         set_error("group-tile pass: %d B of shared memory needed (k = %d)", smem, S.k);
