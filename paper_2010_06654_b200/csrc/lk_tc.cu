@@ -1590,12 +1590,13 @@ __global__ void __launch_bounds__(320, 1)
                 const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
                 const uint32_t pm = __ldg(S.pmask + 2 * rp) | __ldg(S.pmask + 2 * rp + 1);
                 TGY_W(TP_P_AEMPTY, mbar_wait(aempty, (it & 1) ^ 1));
-                mbar_expect_tx(afull, 4 * SM::A_BYTES);
+                // the centered rows x' (fp32); the MMA warp splits them into the
+                // tf32 hi / lo operands in shared memory
+                mbar_expect_tx(afull, 2 * SM::A_BYTES);
 #pragma unroll
                 for (int s = 0; s < 2; s++) {
                     const int row0 = (int)((2 * rp + s) * BM);
                     tma_load_2d(&map_ahi, afull, abuf + s * 2 * SM::A_BYTES, 0, row0);
-                    tma_load_2d(&map_alo, afull, abuf + s * 2 * SM::A_BYTES + SM::A_BYTES, 0, row0);
                 }
                 const float* bt0 = beta_of(2 * rp);
                 const float* bt1 = beta_of(2 * rp + 1);
@@ -1637,6 +1638,23 @@ __global__ void __launch_bounds__(320, 1)
             const int64_t r1n = m - (2 * rp + 1) * BM < BM ? (m - (2 * rp + 1) * BM > 0 ? m - (2 * rp + 1) * BM : 0) : BM;
             n_dist += 128 * (r0n * __popc(m0) + r1n * __popc(m1));
             TGY_W(TP_M_AFULL, mbar_wait(afull, it & 1));
+            {
+                // 3xTF32 split in place: hi = trunc_tf32(x'), lo = x' - hi (exact),
+                // elementwise -- the 128B swizzle moves both buffers alike
+#pragma unroll 4
+                for (int e = lane; e < 2 * (SM::A_BYTES / 16); e += 32) {
+                    const int s_ = e / (SM::A_BYTES / 16), e4 = e % (SM::A_BYTES / 16);
+                    float4* hp = reinterpret_cast<float4*>(abuf + s_ * 2 * SM::A_BYTES) + e4;
+                    float4* lp = reinterpret_cast<float4*>(abuf + s_ * 2 * SM::A_BYTES + SM::A_BYTES) + e4;
+                    const float4 x = *hp;
+                    const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+                    *hp = h;
+                    *lp = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+                }
+                // generic-proxy writes -> visible to the tensor cores' async proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+            }
             tc_fence_after();
             const int g0 = tgy_rot(S, 2 * rp);
             for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
@@ -2159,8 +2177,9 @@ __global__ void k_tile_labels(DevState S, const int64_t* count) {
 
 // Sort and gather in one pass: each worklist row is placed at its sorted
 // position by a shared-memory cursor (per-block bases from k_sort_offsets)
-// and written there centered on its tile's centroid and split for 3xTF32
-// (full 128-byte lines), with its certification record (one 32-byte sector).
+// and written there centered on its tile's centroid (x' in fp32, one full
+// 128-byte line: the pass splits it for 3xTF32 in shared memory), with its
+// certification record (one 32-byte sector).
 // Two phases per 1024-row slice of the block's chunk, so that many rows'
 // dependent loads are in flight at once:
 //   A  a thread per row (4 rows each, loads interleaved): worklist entry ->
@@ -2247,20 +2266,17 @@ __global__ void __launch_bounds__(256) k_sort_gather(DevState S, const int64_t* 
                 if (e >= 0 && sub < c4n) {
                     const float xa[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
                     const float oa[4] = {ov[u].x, ov[u].y, ov[u].z, ov[u].w};
-                    float hh[4], ll[4];
+                    float xs[4];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const float xs = xa[q] - oa[q];
-                        hh[q] = __uint_as_float(__float_as_uint(xs) & 0xFFFFE000u);
-                        ll[q] = xs - hh[q];
-                        x2 = fma((double)xs, (double)xs, x2);
-                        xo = fma((double)xs, (double)oa[q], xo);
+                        xs[q] = xa[q] - oa[q];
+                        x2 = fma((double)xs[q], (double)xs[q], x2);
+                        xo = fma((double)xs[q], (double)oa[q], xo);
                         xx = fma((double)xa[q], (double)xa[q], xx);
                     }
+                    // x' itself (the pass splits it for 3xTF32 in shared memory)
                     __stcs(reinterpret_cast<float4*>(S.Xg_hi + (int64_t)pos * S.ldx) + sub,
-                           make_float4(hh[0], hh[1], hh[2], hh[3]));
-                    __stcs(reinterpret_cast<float4*>(S.Xg_lo + (int64_t)pos * S.ldx) + sub,
-                           make_float4(ll[0], ll[1], ll[2], ll[3]));
+                           make_float4(xs[0], xs[1], xs[2], xs[3]));
                 }
 #pragma unroll
                 for (int o = L >> 1; o > 0; o >>= 1) {
