@@ -25,6 +25,7 @@
 #include <string.h>
 #include <stdlib.h>
 
+#include "lk_async.cuh"
 #include "lk_common.cuh"
 #include "lk_internal.h"
 
@@ -55,53 +56,7 @@ struct Smem {
 
 // ---- PTX helpers -----------------------------------------------------------
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t addr = smem_u32(bar);
-    while (!mbar_try(addr, parity)) {
-    }
-}
-
-__device__ __forceinline__ bool mbar_test(uint32_t addr, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
+// (smem_u32, the mbarrier helpers and bulk_load: lk_async.cuh)
 
 // wait without suspending the thread (A/B knob for the TMEM handoff latency)
 __device__ __forceinline__ void mbar_wait_k(uint64_t* bar, uint32_t parity, int spin) {
@@ -120,14 +75,6 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-
-// 1-D bulk copy global -> shared, completing on an mbarrier (transaction bytes)
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        ::"r"(smem_u32(dst)), "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -1450,10 +1397,12 @@ __device__ __forceinline__ float tgy_lower32(const TgyLow& t, float v) {
     return sqrt_lo(L);
 }
 
-// Shared memory of k_assign_tgy: the k_assign_tc2 stages and resident A, a ring
-// of per-tile beta slices (the two row tiles' 128 offsets of the staged
-// centroid tile: the producer never waits for a whole pair's epilogue), the
-// cumulative group drifts and the pair's per-group minima.
+// Shared memory of k_assign_tgy: the k_assign_tc2 stages and resident A (the
+// tf32 hi / lo operands of the pair's two row tiles), a staging buffer for the
+// next pair's centered rows (fp32, as the sort wrote them), a ring of per-tile
+// beta slices (the two row tiles' 128 offsets of the staged centroid tile: the
+// producer never waits for a whole pair's epilogue), the cumulative group
+// drifts.
 struct TgySmem {
     static constexpr int B_BYTES = 128 * KC * 4;
     static constexpr int STAGE_BYTES = 2 * B_BYTES;
@@ -1461,13 +1410,11 @@ struct TgySmem {
     static constexpr int NBB = 4;                        // beta ring slots
     static constexpr int A_BYTES = BM * KC * 4;
     static constexpr int A_OFF = STAGES * STAGE_BYTES;
-    static constexpr int BAR_OFF = A_OFF + 4 * A_BYTES;
+    static constexpr int XS_OFF = A_OFF + 4 * A_BYTES;   // staging: [row tile][128 rows] x' (fp32)
+    static constexpr int BAR_OFF = XS_OFF + 2 * A_BYTES;
     static constexpr int RING_OFF = BAR_OFF + 256;
     static constexpr int DG_OFF = RING_OFF + NBB * 1024;
-    static constexpr int GM_OFF = DG_OFF + 32 * 4;
-    static constexpr int GS = 257;                       // per-group row stride of the minima
-    static constexpr int TOTAL = GM_OFF + 1024;          // (+ G * GS * 4 + kpad * 4 at launch:
-                                                         //  the minima, the column norms)
+    static constexpr int TOTAL = DG_OFF + 32 * 4 + 1024; // (+ kpad * 4 at launch: the column norms)
 };
 
 // Phase clocks of k_assign_tgy (debug knob LK_TGY_PROF): cycles each role spends
@@ -1501,13 +1448,39 @@ __device__ __forceinline__ uint32_t rotr32(uint32_t m, int r) {
     return r ? (m >> r) | (m << (32 - r)) : m;
 }
 
-__global__ void __launch_bounds__(320, 1)
+// One row tile of the pair's 3xTF32 split, staging -> A operands: hi =
+// trunc_tf32(x'), lo = x' - hi (exact), elementwise (the 128B swizzle moves all
+// three buffers alike).  Waits for the staged rows and for the previous pair's
+// MMAs (the A operands are free), then arrives on sdone.
+__device__ __forceinline__ void tgy_split_tile(const uint8_t* xs, uint8_t* abuf, int s_, uint64_t* sfull,
+                                               uint64_t* aempty, uint64_t* sdone, int it, int lane) {
+    constexpr int A_BYTES = TgySmem::A_BYTES;
+    mbar_wait(sfull, it & 1);
+    if (it > 0) mbar_wait(aempty, (it - 1) & 1);
+    tc_fence_after();
+    const float4* xp = reinterpret_cast<const float4*>(xs + s_ * A_BYTES);
+    float4* hp = reinterpret_cast<float4*>(abuf + s_ * 2 * A_BYTES);
+    float4* lp = reinterpret_cast<float4*>(abuf + s_ * 2 * A_BYTES + A_BYTES);
+#pragma unroll 8
+    for (int e = lane; e < A_BYTES / 16; e += 32) {
+        const float4 x = xp[e];
+        const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+        hp[e] = h;
+        lp[e] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+    }
+    // generic-proxy writes -> visible to the tensor cores' async proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(sdone);
+}
+
+__global__ void __launch_bounds__(352, 1)
     k_assign_tgy(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                  const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                  DevState S, TcArgs A, int64_t* stat) {
     if (*S.done) return;
     using SM = TgySmem;
-    constexpr int BN = 128, NBUF = 2, PW = 8, MW = 9, GS = SM::GS, NBB = SM::NBB;
+    constexpr int BN = 128, NBUF = 2, PW = 8, MW = 9, LW = 10, NBB = SM::NBB;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* abuf = smem + SM::A_OFF;
@@ -1515,15 +1488,16 @@ __global__ void __launch_bounds__(320, 1)
     uint64_t* empty = full + SM::STAGES;
     uint64_t* tfull = empty + SM::STAGES;
     uint64_t* tempty = tfull + NBUF;
-    uint64_t* afull = tempty + NBUF;
-    uint64_t* aempty = afull + 1;
-    uint64_t* rfull = aempty + 1;     // [NBB] beta slices staged
+    uint64_t* sfull = tempty + NBUF;  // the next pair's x' staged (TMA)
+    uint64_t* aempty = sfull + 1;     // the pair's MMAs are done (A operands free)
+    uint64_t* sdone = aempty + 1;     // both row tiles split (staging free, A ready)
+    uint64_t* rfull = sdone + 1;      // [NBB] beta slices staged
     uint64_t* rempty = rfull + NBB;   // [NBB] ... and released by the 8 epilogue warps
     uint32_t* tmem_slot = (uint32_t*)(rempty + NBB);
     float* ring = (float*)(smem + SM::RING_OFF);  // [NBB][2][128]
     float* sdg = (float*)(smem + SM::DG_OFF);     // [32] cumulative group drifts
-    float* sgm = (float*)(smem + SM::GM_OFF);     // [G][GS]: per group, the pair's 256 rows
-    float* scn = sgm + S.t_groups * GS;           // [kpad] |c| of each B column (+inf padding)
+    float* scn = sdg + 32;                        // [kpad] |c| of each B column (+inf padding)
+    uint8_t* xs = smem + SM::XS_OFF;              // [2][A_BYTES] staged x'
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = S.t_groups;
@@ -1555,8 +1529,9 @@ __global__ void __launch_bounds__(320, 1)
             mbar_init(&rfull[b], 1);
             mbar_init(&rempty[b], 8);
         }
-        mbar_init(afull, 1);
+        mbar_init(sfull, 1);
         mbar_init(aempty, 1);
+        mbar_init(sdone, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_map(&map_ahi);
         prefetch_map(&map_alo);
@@ -1589,15 +1564,6 @@ __global__ void __launch_bounds__(320, 1)
             for (int it = 0; it < n_it; it++) {
                 const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
                 const uint32_t pm = __ldg(S.pmask + 2 * rp) | __ldg(S.pmask + 2 * rp + 1);
-                TGY_W(TP_P_AEMPTY, mbar_wait(aempty, (it & 1) ^ 1));
-                // the centered rows x' (fp32); the MMA warp splits them into the
-                // tf32 hi / lo operands in shared memory
-                mbar_expect_tx(afull, 2 * SM::A_BYTES);
-#pragma unroll
-                for (int s = 0; s < 2; s++) {
-                    const int row0 = (int)((2 * rp + s) * BM);
-                    tma_load_2d(&map_ahi, afull, abuf + s * 2 * SM::A_BYTES, 0, row0);
-                }
                 const float* bt0 = beta_of(2 * rp);
                 const float* bt1 = beta_of(2 * rp + 1);
                 const int g0 = tgy_rot(S, 2 * rp);
@@ -1637,24 +1603,9 @@ __global__ void __launch_bounds__(320, 1)
             const int64_t r0n = m - 2 * rp * BM < BM ? m - 2 * rp * BM : BM;
             const int64_t r1n = m - (2 * rp + 1) * BM < BM ? (m - (2 * rp + 1) * BM > 0 ? m - (2 * rp + 1) * BM : 0) : BM;
             n_dist += 128 * (r0n * __popc(m0) + r1n * __popc(m1));
-            TGY_W(TP_M_AFULL, mbar_wait(afull, it & 1));
-            {
-                // 3xTF32 split in place: hi = trunc_tf32(x'), lo = x' - hi (exact),
-                // elementwise -- the 128B swizzle moves both buffers alike
-#pragma unroll 4
-                for (int e = lane; e < 2 * (SM::A_BYTES / 16); e += 32) {
-                    const int s_ = e / (SM::A_BYTES / 16), e4 = e % (SM::A_BYTES / 16);
-                    float4* hp = reinterpret_cast<float4*>(abuf + s_ * 2 * SM::A_BYTES) + e4;
-                    float4* lp = reinterpret_cast<float4*>(abuf + s_ * 2 * SM::A_BYTES + SM::A_BYTES) + e4;
-                    const float4 x = *hp;
-                    const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
-                    *hp = h;
-                    *lp = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
-                }
-                // generic-proxy writes -> visible to the tensor cores' async proxy
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-            }
+            // row tile 1's split (the loader warp splits row tile 0), then both
+            TGY_W(TP_M_AFULL, tgy_split_tile(xs, abuf, 1, sfull, aempty, sdone, it, lane));
+            TGY_W(TP_M_AFULL, mbar_wait(sdone, it & 1));
             tc_fence_after();
             const int g0 = tgy_rot(S, 2 * rp);
             for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
@@ -1692,13 +1643,32 @@ __global__ void __launch_bounds__(320, 1)
             mma_commit(aempty);
         }
         if (lane == 0 && n_dist) atomicAdd((unsigned long long*)(stat + LK_STAT_DIST), (unsigned long long)n_dist);
+    } else if (warp == LW) {
+        // ===== A loader: the next pair's centered rows x' (fp32) into the
+        // staging buffer while the current pair runs; row tile 0's split.  The
+        // split waits only for the previous pair's MMAs, not for an HBM load.
+        if (n_it > 0 && lane == 0) {
+            mbar_expect_tx(sfull, 2 * SM::A_BYTES);
+            tma_load_2d(&map_ahi, sfull, xs, 0, (int)(2 * (int64_t)blockIdx.x * BM));
+            tma_load_2d(&map_ahi, sfull, xs + SM::A_BYTES, 0, (int)((2 * (int64_t)blockIdx.x + 1) * BM));
+        }
+        for (int it = 0; it < n_it; it++) {
+            tgy_split_tile(xs, abuf, 0, sfull, aempty, sdone, it, lane);
+            mbar_wait(sdone, it & 1);  // (both halves read: the staging buffer is free)
+            if (it + 1 < n_it && lane == 0) {
+                const int64_t rp = blockIdx.x + (int64_t)(it + 1) * gridDim.x;
+                mbar_expect_tx(sfull, 2 * SM::A_BYTES);
+                tma_load_2d(&map_ahi, sfull, xs, 0, (int)(2 * rp * BM));
+                tma_load_2d(&map_ahi, sfull, xs + SM::A_BYTES, 0, (int)((2 * rp + 1) * BM));
+            }
+            __syncwarp();
+        }
     } else {
         // ===== epilogue: warp w = rows 32 (w % 4) .. of row tile w / 4 =====
         const int q = warp & 3, s = warp >> 2;
         const float kappa = tc_kappa_ordered(S.d);
         const float dm = S.scal[4];
         const float cmax_f = S.scal[0];
-        __shared__ unsigned long long escr[9];
         int acc = 0, rs = 0;
         uint32_t acc_phase = 0, rphase = 0;
         const int rloc0 = s * BM + q * 32;   // this warp's first row in the pair
@@ -1743,6 +1713,10 @@ __global__ void __launch_bounds__(320, 1)
                 old = S.labels[row];  // (used in the tail only)
             }
             load_meta(it + 1);
+            // the fp32 lower-bound setup of the row (tgy_lower32): each scanned
+            // group's bound is formed and stored as soon as its tile is done
+            const TgyLow tl = tgy_low_setup(R, xo, kappa, cmax_f, S.d);
+            float* lbr = S.lb + row * S.nlb;
             const int g0 = tgy_rot(S, 2 * rp);
             for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
                 const int ct = (__ffs(mm) - 1 + g0) & 31;
@@ -1820,14 +1794,20 @@ __global__ void __launch_bounds__(320, 1)
                         }
                     }
                 }
-                if (mine)  // the group's minimum D'~ (raw)
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(sgm + ct * GS + rloc)), "f"(gmin) : "memory");
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&tempty[acc]);
                     mbar_arrive(&rempty[rs]);
                 }
+                // the group's bound (lazy encoding) from its minimum D'~: it bounds
+                // all its members, whichever wins (the winner's group is rewritten
+                // from the second best in the tail when the row is certified).
+                // Every group of the row tile's mask is rewritten, not only the
+                // row's own failing groups (measured: the tile's other groups then
+                // keep older, weaker bounds and fail later -- 1.3e10 -> 1.75e10
+                // products at cfg5 iteration 20).
+                if (mine && valid) __stcg(lbr + ct, __fadd_rd(tgy_lower32(tl, gmin), sdg[ct]));
                 if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
                 if (++rs == NBB) { rs = 0; rphase ^= 1; }
                 if (prof_on) pc[TP_E_TILES] += clock64() - tt0;
@@ -1841,10 +1821,11 @@ __global__ void __launch_bounds__(320, 1)
             const float dcj = jc >= 0 ? __ldg(S.dcum_col + jc) : 0.f;
             bool moved = false, amb = false, cert = false;
             float thr_out = 0.f, lb_out = 0.f;
+            float L2d = 0.f, Ud = 0.f;
+            int g1 = -1;
             if (valid) {
                 // certification in fp32 with directed rounding (tgy_lower32's scheme:
                 // upper bounds rounded up, lower bounds down; R split into R_lo / R_hi)
-                const TgyLow tl = tgy_low_setup(R, xo, kappa, cmax_f, S.d);
                 const float cn1 = jc >= 0 ? scn[jc] : cmax_f;  // (|c| of the winner's column)
                 const float ab1 = fabsf(b1);
                 // e1 = kappa |x'| |c1| + gb (|b1| + 2 |x'| |c1|) + 2u |b1|        (up)
@@ -1856,33 +1837,14 @@ __global__ void __launch_bounds__(320, 1)
                 const float ex1 = __fmul_ru(__fmul_ru(2.384185791015625e-07f, tl.xo), __fadd_ru(sr1, tl.xo));
                 // U >= (R + b1 + e1 + ex1): the squared distance of the best column, from above
                 const float U = __fadd_ru(__fadd_ru(__fadd_ru(__fadd_ru(tl.R_hi, b1), e1), ex1), tl.slack);
-                const float Ud = sqrt_hi(U);
-                const float L2d = tgy_lower32(tl, b2);
+                Ud = sqrt_hi(U);
+                L2d = tgy_lower32(tl, b2);
                 // the winner beats every other scanned column and every unscanned group
                 cert = jc >= 0 && L2d > Ud && lun > Ud && !isinf(b1);
                 // (the winner's group is its tile: B columns are in group order)
-                const int g1 = cert ? (jc >> 7) : -1;
-                if (prof_on) pc[TP_T_CERT] += clock64() - tl0;
-                // every scanned group's bound (lazy encoding): its minimum bounds
-                // all its members, whichever wins; a certified row's winner group
-                // gets the second best (its other members).  (Rewriting only the
-                // row's own failing groups was measured: the tile's other groups
-                // then keep older, weaker bounds and fail later -- 1.3e10 ->
-                // 1.75e10 products at cfg5 iteration 20.)
-                for (uint32_t mm = ms; mm; mm &= mm - 1) {
-                    const int g = __ffs(mm) - 1;
-                    const uint32_t sa = smem_u32(sgm + g * GS + rloc);
-                    float raw;
-                    asm("ld.shared.f32 %0, [%1];" : "=f"(raw) : "r"(sa));
-                    const float v = g == g1 ? L2d : tgy_lower32(tl, raw);
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(sa), "f"(__fadd_rd(v, sdg[g])));
-                }
-                if (prof_on) pc[TP_T_GROUPS] += clock64() - tl0;
+                g1 = cert ? (jc >> 7) : -1;
                 if (cert) {
                     moved = old != j1;
-                    if (moved) S.labels[row] = j1;
-                    S.ub[row] = __fsub_ru(Ud, dcj);
-                    S.glb[row] = __fadd_rd(fminf(L2d, lun), dm);
                 } else {
                     amb = true;
                     // thresholds of the (uncentered) collect pass: every possible winner
@@ -1895,23 +1857,35 @@ __global__ void __launch_bounds__(320, 1)
                     lb_out = sqrt_lo(U);
                 }
             }
-            // the rewritten group bounds, one 4-byte store per group
+            if (prof_on) pc[TP_T_CERT] += clock64() - tl0;
+            // list slots: one atomic per warp and list (no barrier across the
+            // epilogue warps), issued before the group-bound work so that their
+            // round trips overlap it
+            const unsigned mmv = __ballot_sync(LK_FULL_MASK, moved);
+            const unsigned mam = __ballot_sync(LK_FULL_MASK, amb);
+            unsigned long long bmv = 0, bam = 0;
+            if (lane == 0) {
+                if (mmv) bmv = atomicAdd((unsigned long long*)(stat + LK_STAT_CHANGED), (unsigned long long)__popc(mmv));
+                if (mam) bam = atomicAdd((unsigned long long*)(stat + LK_STAT_CANDIDATE), (unsigned long long)__popc(mam));
+            }
             if (valid) {
-                float* lbr = S.lb + row * S.nlb;
-                for (uint32_t mm = ms; mm; mm &= mm - 1) {
-                    const int g = __ffs(mm) - 1;
-                    float v;
-                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(sgm + g * GS + rloc)));
-                    __stcg(lbr + g, v);
+                if (cert) {
+                    // the winner's group: the second best bounds its other members
+                    __stcg(lbr + g1, __fadd_rd(L2d, sdg[g1]));
+                    if (moved) S.labels[row] = j1;
+                    S.ub[row] = __fsub_ru(Ud, dcj);
+                    S.glb[row] = __fadd_rd(fminf(L2d, lun), dm);
                 }
             }
-            if (prof_on) pc[TP_T_STORES] += clock64() - tl0;
-            // one global atomic per CTA and list (all 148 CTAs append to the same two
-            // counters: per-warp atomics serialize in their L2 slice)
-            const int64_t pos = epi_append8(moved, (unsigned long long*)(stat + LK_STAT_CHANGED), escr, warp);
-            if (moved) S.moved[pos] = make_int2((int)row, old);
-            const int64_t cpos = epi_append8(amb, (unsigned long long*)(stat + LK_STAT_CANDIDATE), escr, warp);
+            if (prof_on) {
+                pc[TP_T_GROUPS] += clock64() - tl0;
+                pc[TP_T_STORES] += clock64() - tl0;
+            }
+            bmv = __shfl_sync(LK_FULL_MASK, bmv, 0);
+            bam = __shfl_sync(LK_FULL_MASK, bam, 0);
+            if (moved) S.moved[bmv + __popc(mmv & lanemask_lt())] = make_int2((int)row, old);
             if (amb) {
+                const int64_t cpos = (int64_t)(bam + __popc(mam & lanemask_lt()));
                 S.cand_rows[cpos] = (int)row;
                 S.cand_thr[cpos] = thr_out;
                 S.cand_lb[cpos] = lb_out;
@@ -2463,7 +2437,7 @@ static int tc_max_dyn_smem() { return g_tc_max_dyn; }
 static int g_tgy_max_dyn = 0;
 static int tc_max_dyn_smem_tgy() { return g_tgy_max_dyn; }
 // k_assign_tgy: the k_assign_tc2 layout + the pair's per-group minima
-static int tgy_smem(const DevState& S) { return TgySmem::TOTAL + S.t_groups * TgySmem::GS * 4 + S.kpad * 4; }
+static int tgy_smem(const DevState& S) { return TgySmem::TOTAL + S.kpad * 4; }
 
 template <int BN, int MODE, bool SPLIT, bool ARES, int CL = 1>
 static lk_status tc_attr(int optin) {
@@ -2786,12 +2760,18 @@ lk_status launch_assign_tgy(const DevState& S, int64_t* stat, int64_t max_rows, 
     A.n_kc = 1;
     A.n_ct = S.t_groups;
     A.prof = tgy_prof_buffer();
+    {
+        // LK_TGY_PROF_SKIP=N: the first N launches run without the clocks
+        static int launches = 0;
+        static const int skip = env_int("LK_TGY_PROF_SKIP", 0);
+        if (launches++ < skip) A.prof = nullptr;
+    }
     const int smem = tgy_smem(S);
     if (smem > tc_max_dyn_smem_tgy()) {
         set_error("group-tile pass: %d B of shared memory needed (k = %d)", smem, S.k);
         return LK_ERR_UNSUPPORTED;
     }
-    k_assign_tgy<<<sms, 320, smem, st>>>(mah, mal, mbh, mbl, S, A, stat);
+    k_assign_tgy<<<sms, 352, smem, st>>>(mah, mal, mbh, mbl, S, A, stat);
     LK_LAUNCH_CHECK();
     return LK_OK;
 }
