@@ -41,7 +41,8 @@ enum InternalBuf {
     B_XLO, B_XN2, B_CHI, B_CLO, B_CN2, B_XG_HI, B_XG_LO, B_CAND_ROWS, B_CAND_THR, B_CAND_LB, B_CAND_SLOTS, B_CAND_CNT, B_OVF,
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
     B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB,
-    B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_VALID, B_CCH, B_RGSCR, B_RGMEANS, B_DCUMCOL, B_COUNT_
+    B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_VALID, B_CCH, B_RGSCR, B_RGMEANS, B_DCUMCOL,
+    B_WORK2, B_YMASK2, B_YLUN2, B_GFREQ, B_GSEL, B_BHIST, B_BBASE, B_COUNT_
 };
 
 struct Layout {
@@ -209,6 +210,13 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_TMETA] = (uint64_t)n * sizeof(lk::TgyMeta);
         L->size[B_PMASK] = (uint64_t)(n / 128 + 4) * 4;  // per 128-row tile
         L->size[B_SHIST] = (uint64_t)1536 * kpad * 4;  // (<= 1536 sort blocks)
+        L->size[B_WORK2] = (uint64_t)n * 4;
+        L->size[B_YMASK2] = (uint64_t)n * 4;
+        L->size[B_YLUN2] = (uint64_t)n * 8;
+        L->size[B_GFREQ] = (uint64_t)k * 32 * 4;
+        L->size[B_GSEL] = (uint64_t)k * 4;
+        L->size[B_BHIST] = (uint64_t)1536 * 64 * 4;
+        L->size[B_BBASE] = 64 * 4;
         L->size[B_DCUM] = (uint64_t)k * 4;
         L->size[B_DCUMCOL] = (uint64_t)kpad * 4;
         L->size[B_DGCUM] = (uint64_t)L->groups * 4;
@@ -517,6 +525,13 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.pmask = buf<uint32_t>(c, B_PMASK);
     S.shist = buf<int32_t>(c, B_SHIST);
     S.tmeta = buf<lk::TgyMeta>(c, B_TMETA);
+    S.work2 = buf<int32_t>(c, B_WORK2);
+    S.ymask2 = buf<uint32_t>(c, B_YMASK2);
+    S.ylun2 = buf<float2>(c, B_YLUN2);
+    S.gfreq = buf<int32_t>(c, B_GFREQ);
+    S.gsel = buf<uint32_t>(c, B_GSEL);
+    S.bhist = buf<int32_t>(c, B_BHIST);
+    S.bbase = buf<int32_t>(c, B_BBASE);
     S.hlog_inline = (S.lazy && S.hlog != nullptr && S.hlog_cap > 0) ? 1 : 0;
     {
         const char* e = getenv("LK_SGATE");  // A/B knob for the centroid-separation gate
@@ -556,6 +571,10 @@ lk_status lk_ctx_destroy(lk_ctx* c) {
 }
 
 lk_status lk_buffer(const lk_ctx* c, int32_t id, uint64_t* offset, uint64_t* bytes) {
+    // (debug tools: 1000 the group-tile worklist records, 1001 the tile labels;
+    // internal layout, not part of the interface)
+    if (c && (id == 1000 || id == 1001)) id = id == 1000 ? B_TMETA : B_TILE_LAB;
+    else
     if (!c || id < 0 || id >= LK_NBUF) {
         set_error("bad buffer id %d", id);
         return LK_ERR_ARG;
@@ -778,6 +797,11 @@ lk_status lk_set_centroids(lk_ctx* c, const double* c64, void* stream) {
     LK_CUDA_CHECK(cudaMemsetAsync(S.delta, 0, c->L.size[B_DELTA], st));
     if (S.tgy || S.elkan) LK_CUDA_CHECK(cudaMemsetAsync(S.lb, 0, c->L.size[B_LB], st));  // bounds >= 0
     if (S.dcum_col) LK_CUDA_CHECK(cudaMemsetAsync(S.dcum_col, 0, c->L.size[B_DCUMCOL], st));
+    if (S.gsel) {
+        // no bucket key before the first listing
+        LK_CUDA_CHECK(cudaMemsetAsync(S.gsel, 0, c->L.size[B_GSEL], st));
+        LK_CUDA_CHECK(cudaMemsetAsync(S.gfreq, 0, c->L.size[B_GFREQ], st));
+    }
     if (S.lazy) {
         LK_CUDA_CHECK(cudaMemsetAsync(S.dcum, 0, c->L.size[B_DCUM], st));
         LK_CUDA_CHECK(cudaMemsetAsync(S.dgcum, 0, c->L.size[B_DGCUM], st));
@@ -866,7 +890,7 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             ProfScope p(c, 0, st);
             s = lkh::launch_assign_tgy(S, stat, n, c->sms, st);
             if (s != LK_OK) return s;
-            c->launches += 8;
+            c->launches += lkh::tgy_bucket_on(S) ? 12 : 8;
         } else if (group_mode(c->cfg)) {
             // tensor-core runs: every row failing the bounds is rescanned in full
             const bool full_only = use_tc;

@@ -108,7 +108,7 @@ struct DevState {
     int32_t* ginv;          // [k] position of centroid j in gperm
     int32_t* goff;          // [t + 1] group ranges in gperm
     float* Cg;              // [k, ldc] fp32 centroids in group order (gperm)
-    float2* ylun;           // [n] per worklist row: (min bound over unscanned groups, |x|)
+    float2* ylun;           // [n] per worklist row: (min bound over unscanned groups, the label's bits on the group tiles)
     int4* ywl;              // [n] worklist: (row, pair offset, pair count, bits of D~_a)
     int2* ypairs;           // [pair_cap] (row, group | label position << 16)
     float4* yres;           // [pair_cap] (bits of best j, best D~, second D~, -)
@@ -135,6 +135,15 @@ struct DevState {
     uint32_t* pmask;        // [n / 128 + 4] per 128-row tile: union of its rows' masks
     int32_t* shist;         // [tgy_sort_blocks, kcols] worklist sort: per-block key counts
     struct TgyMeta* tmeta;  // [n] per sorted position of the group-tile worklist (32 B)
+    // second sort key of the group-tile worklist (rows of one label ordered by
+    // the groups they scan, so a 128-row tile's union of masks stays small)
+    int32_t* work2;         // [n] the worklist partitioned by mask bucket: rows,
+    uint32_t* ymask2;       // [n]   masks,
+    float2* ylun2;          // [n]   (bound over the unscanned groups, label)
+    int32_t* gfreq;         // [k, 32] listed rows of a label that scan group g (this iteration)
+    uint32_t* gsel;         // [k] the groups whose mask bits form a label's bucket key
+    int32_t* bhist;         // [tgy_sort_blocks, 64] per-block bucket counts / offsets
+    int32_t* bbase;         // [64] bucket bases
     // Elkan's per-centroid bounds (lk_elkan.cu): lb is [k, n]
     int32_t elkan;
     float* cch;             // [k, k] certified lower bound of 1/2 ||c_a - c_j||

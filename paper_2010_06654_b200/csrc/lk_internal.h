@@ -70,6 +70,7 @@ lk_status launch_elkan(const lk::DevState& S, int64_t* stat, int sms, cudaStream
 lk_status launch_regroup(const lk::DevState& S, int32_t* scr, double* means, int sms, cudaStream_t st);
 lk_status launch_filter_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
 lk_status launch_sort_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaStream_t st);
+bool tgy_bucket_on(const lk::DevState& S);  // 4 more launches in launch_sort_tgy
 lk_status launch_assign_tgy(const lk::DevState& S, int64_t* stat, int64_t max_rows, int sms,
                             cudaStream_t st);
 // worklist rescan or, when the list holds most rows, one dense pass (device-chosen)

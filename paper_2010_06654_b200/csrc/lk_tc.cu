@@ -1913,21 +1913,36 @@ __global__ void __launch_bounds__(352, 1)
 
 // Union of the group masks of each 128-row tile of the sorted worklist (one
 // warp per tile; 0 past the last tile).
-__global__ void k_pair_mask(DevState S, const int64_t* count) {
+__global__ void k_pair_mask(DevState S, const int64_t* count, int freq) {
     if (*S.done) return;
     const int64_t m = *count;
     const int64_t nt = (m + 127) / 128 + 1;
     const int lane = threadIdx.x & 31;
     for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < nt;
          p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        uint32_t v = 0;
+        uint32_t v = 0, ve[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             const int64_t pos = p * 128 + e * 32 + lane;
-            if (pos < m) v |= __ldcs(&S.tmeta[pos].mask);
+            ve[e] = pos < m ? __ldcs(&S.tmeta[pos].mask) : 0u;
+            v |= ve[e];
         }
-        v = __reduce_or_sync(LK_FULL_MASK, v);
-        if (lane == 0) S.pmask[p] = v;
+        const uint32_t any = __reduce_or_sync(LK_FULL_MASK, v);
+        if (lane == 0) S.pmask[p] = any;
+        if (freq && any) {
+            // how many of the tile's rows scan each group, added to the tile
+            // label's frequencies (lane g owns group g)
+            const int lab = __ldg(S.tile_lab + p);
+            int mine = 0;
+            for (uint32_t mm = any; mm; mm &= mm - 1) {
+                const int g = __ffs(mm) - 1;
+                int c = 0;
+#pragma unroll
+                for (int e = 0; e < 4; e++) c += __popc(__ballot_sync(LK_FULL_MASK, (ve[e] >> g) & 1));
+                if (lane == g) mine = c;
+            }
+            if (lab >= 0 && mine > 0) atomicAdd(S.gfreq + (int64_t)lab * 32 + lane, mine);
+        }
     }
 }
 
@@ -2101,7 +2116,166 @@ __device__ __forceinline__ void sort_chunk(int64_t m, int nb, int b, int64_t& p0
     p1 = p0 + per < m ? p0 + per : m;
 }
 
-__global__ void __launch_bounds__(256) k_sort_hist(DevState S, const int64_t* count, int* hist) {
+// ---- second sort key: the groups a row scans --------------------------------
+// A 128-row tile runs the union of its rows' group masks, and rows of one label
+// fail different neighbour groups: in label order alone the pass evaluated
+// ~1.7x the products of the rows' own masks (cfg5).  So the worklist is first
+// partitioned by a bucket key -- the row's mask bits at up to kSelBits groups
+// chosen per label (S.gsel: the groups whose separation saves the most tile
+// scans, from the previous iteration's per-label frequencies S.gfreq) -- and
+// the label sort, which keeps the block order inside a label, then leaves a
+// label's rows ordered by bucket (an LSD radix sort with the label as the
+// last digit; a block's chunk lies in one bucket but for the ~64 boundaries).
+constexpr int kSelBits = 6;
+constexpr int kBuckets = 1 << kSelBits;
+
+__device__ __forceinline__ int bucket_key(uint32_t mask, uint32_t sel) {
+    int key = 0;
+    while (sel) {
+        const int b = __ffs(sel) - 1;
+        key = (key << 1) | ((mask >> b) & 1);
+        sel &= sel - 1;
+    }
+    return key;
+}
+
+// counts `key` over the warp's active lanes with one shared-memory atomic per
+// distinct key; returns the lane's slot (base from the atomic + rank)
+__device__ __forceinline__ int warp_key_add(int* sh, int key, bool ok) {
+    // (whole-warp call; lanes without a row share the key -1 and add nothing)
+    const unsigned peers = __match_any_sync(LK_FULL_MASK, ok ? key : -1);
+    const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+    int base = 0;
+    if (ok && lane == leader) base = atomicAdd(sh + key, __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    return base + __popc(peers & lanemask_lt());
+}
+
+__global__ void __launch_bounds__(256) k_bucket_hist(DevState S, const int64_t* count) {
+    if (*S.done) return;
+    __shared__ int sh[kBuckets];
+    if (threadIdx.x < kBuckets) sh[threadIdx.x] = 0;
+    __syncthreads();
+    int64_t p0, p1;
+    sort_chunk(*count, gridDim.x, blockIdx.x, p0, p1);
+    for (int64_t b = p0; b < p1; b += blockDim.x) {
+        const int64_t p = b + threadIdx.x;
+        const bool ok = p < p1;
+        int key = 0;
+        if (ok) {
+            const int lab = __float_as_int(__ldg(&S.ylun[p].y));
+            key = bucket_key(__ldg(S.ymask + p), __ldg(S.gsel + lab));
+        }
+        warp_key_add(sh, key, ok);
+    }
+    __syncthreads();
+    if (threadIdx.x < kBuckets) S.bhist[blockIdx.x * kBuckets + threadIdx.x] = sh[threadIdx.x];
+}
+
+// per bucket: exclusive prefix over the blocks (in place), then the bucket bases
+__global__ void __launch_bounds__(1024) k_bucket_offsets(DevState S, int nb) {
+    if (*S.done) return;
+    __shared__ int tot[kBuckets];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = warp; j < kBuckets; j += 32) {
+        int run = 0;
+        for (int b0 = 0; b0 < nb; b0 += 32) {
+            const int b = b0 + lane;
+            const int v = b < nb ? S.bhist[b * kBuckets + j] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(LK_FULL_MASK, incl, o);
+                if (lane >= o) incl += u;
+            }
+            if (b < nb) S.bhist[b * kBuckets + j] = run + incl - v;
+            run += __shfl_sync(LK_FULL_MASK, incl, 31);
+        }
+        if (lane == 0) tot[j] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int j = 0; j < kBuckets; j++) {
+            S.bbase[j] = run;
+            run += tot[j];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bucket_scatter(DevState S, const int64_t* count) {
+    if (*S.done) return;
+    __shared__ int sh[kBuckets];
+    if (threadIdx.x < kBuckets)
+        sh[threadIdx.x] = S.bbase[threadIdx.x] + S.bhist[blockIdx.x * kBuckets + threadIdx.x];
+    __syncthreads();
+    int64_t p0, p1;
+    sort_chunk(*count, gridDim.x, blockIdx.x, p0, p1);
+    for (int64_t b = p0; b < p1; b += blockDim.x) {
+        const int64_t p = b + threadIdx.x;
+        const bool ok = p < p1;
+        float2 yl = make_float2(0.f, 0.f);
+        uint32_t mask = 0;
+        int row = 0, key = 0;
+        if (ok) {
+            yl = __ldcs(S.ylun + p);
+            mask = __ldcs(S.ymask + p);
+            row = __ldcs(S.work + p);
+            key = bucket_key(mask, __ldg(S.gsel + __float_as_int(yl.y)));
+        }
+        const int pos = warp_key_add(sh, key, ok);
+        if (ok) {
+            S.work2[pos] = row;
+            S.ymask2[pos] = mask;
+            S.ylun2[pos] = yl;
+        }
+    }
+}
+
+// A label's bucket key for the next iteration, from this iteration's listing:
+// with p the share of the label's listed rows that scan group g, a tile of 128
+// of them scans g with probability 1 - (1 - p)^128 when the rows are mixed and
+// p when they are separated; the kSelBits groups with the largest difference
+// are selected.  Clears the label's frequencies.
+__global__ void k_pick_sel(DevState S) {
+    if (*S.done) return;
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= S.k) return;
+    const int G = S.t_groups, own = S.group_of[l];
+    int* f = S.gfreq + (int64_t)l * 32;
+    const float cnt = (float)f[own];
+    float sc[32];
+#pragma unroll
+    for (int g = 0; g < 32; g++) {
+        float v = -1.f;
+        if (g < G && g != own && cnt > 0.f) {
+            const float p = fminf((float)f[g] / cnt, 1.f);
+            v = 1.f - __expf(128.f * log1pf(-fminf(p, 0.999999f))) - p;
+        }
+        sc[g] = v;
+        if (g < G) f[g] = 0;
+    }
+    uint32_t sel = 0;
+    for (int r = 0; r < kSelBits; r++) {
+        float best = 0.02f;  // (a group nearly every / hardly any row scans is not worth a bit)
+        int bg = -1;
+#pragma unroll
+        for (int g = 0; g < 32; g++)
+            if (sc[g] > best) {
+                best = sc[g];
+                bg = g;
+            }
+        if (bg < 0) break;
+        sel |= 1u << bg;
+#pragma unroll
+        for (int g = 0; g < 32; g++)
+            if (g == bg) sc[g] = -1.f;
+    }
+    S.gsel[l] = sel;
+}
+
+__global__ void __launch_bounds__(256) k_sort_hist(DevState S, const int64_t* count, int* hist,
+                                                   const float2* __restrict__ wlun) {
     if (*S.done) return;
     extern __shared__ int sh[];
     const int keys = S.kcols;
@@ -2110,7 +2284,7 @@ __global__ void __launch_bounds__(256) k_sort_hist(DevState S, const int64_t* co
     int64_t p0, p1;
     sort_chunk(*count, gridDim.x, blockIdx.x, p0, p1);
     for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x)
-        atomicAdd(sh + sort_key(S, S.labels[S.work[p]]), 1);
+        atomicAdd(sh + sort_key(S, __float_as_int(__ldcs(&wlun[p].y))), 1);
     __syncthreads();
     int* h = hist + (int64_t)blockIdx.x * keys;
     for (int j = threadIdx.x; j < keys; j += blockDim.x) h[j] = sh[j];
@@ -2173,7 +2347,10 @@ struct SortStage {
     float lun[kSortSlice];
 };
 
-__global__ void __launch_bounds__(256) k_sort_gather(DevState S, const int64_t* count, const int* hist) {
+__global__ void __launch_bounds__(256) k_sort_gather(DevState S, const int64_t* count, const int* hist,
+                                                     const int32_t* __restrict__ wrow,
+                                                     const uint32_t* __restrict__ wmask,
+                                                     const float2* __restrict__ wlun) {
     if (*S.done) return;
     extern __shared__ int sh[];
     __shared__ SortStage st;
@@ -2191,15 +2368,14 @@ __global__ void __launch_bounds__(256) k_sort_gather(DevState S, const int64_t* 
         const int nrow = (int)(p1 - base < kSortSlice ? p1 - base : kSortSlice);
         // ---- A: positions
         int rw[RPT], lb[RPT];
+        float ln[RPT];
 #pragma unroll
         for (int u = 0; u < RPT; u++) {
             const int e = threadIdx.x + u * 256;
-            rw[u] = e < nrow ? __ldcs(S.work + base + e) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < RPT; u++) {
-            const int e = threadIdx.x + u * 256;
-            lb[u] = e < nrow ? S.labels[rw[u]] : 0;
+            rw[u] = e < nrow ? __ldcs(wrow + base + e) : 0;
+            const float2 yl = e < nrow ? __ldcs(wlun + base + e) : make_float2(0.f, 0.f);
+            ln[u] = yl.x;
+            lb[u] = __float_as_int(yl.y);  // the row's label (written by the filter)
         }
 #pragma unroll
         for (int u = 0; u < RPT; u++) {
@@ -2210,8 +2386,8 @@ __global__ void __launch_bounds__(256) k_sort_gather(DevState S, const int64_t* 
                 st.pos[e] = pos;
                 st.lab[e] = lb[u];
                 st.a[e] = __ldg(S.tile_lab + (pos >> 7));
-                st.mask[e] = __ldcs(S.ymask + base + e);
-                st.lun[e] = __ldcs(&S.ylun[base + e].x);
+                st.mask[e] = __ldcs(wmask + base + e);
+                st.lun[e] = ln[u];
             }
         }
         __syncthreads();
@@ -2721,11 +2897,37 @@ static unsigned long long* tgy_prof_buffer() {
 // Block-sparse Yinyang pass over the filter's worklist (stat[LK_STAT_WORK]
 // rows, masks in S.ymask): label sort, pair masks, centered gather, then the
 // (row-tile pair x group tile) MMAs of k_assign_tgy.
+// the worklist is partitioned by mask bucket before the label sort
+// (LK_TGY_BUCKET, A/B knob, default 0: sort by label alone.  Measured on cfg5:
+// the pass evaluates 13% fewer products, not the 35% the tile unions alone
+// predict -- a row also has the bounds of its tile's other groups refreshed, so
+// wider unions list fewer rows and leave fewer ambiguous -- and the partition
+// costs more than the pass saves)
+bool tgy_bucket_on(const DevState& S) {
+    static const int bucket = env_int("LK_TGY_BUCKET", 0);
+    return bucket != 0 && S.work2 != nullptr;
+}
+
 lk_status launch_sort_tgy(const DevState& S, int64_t* stat, int sms, cudaStream_t st) {
     const int64_t* count = stat + LK_STAT_WORK;
     const int nb = tgy_sort_blocks(sms);
     const size_t hs = (size_t)S.kcols * 4;
-    k_sort_hist<<<nb, 256, hs, st>>>(S, count, S.shist);
+    const bool bucket = tgy_bucket_on(S);
+    const int32_t* wrow = S.work;
+    const uint32_t* wmask = S.ymask;
+    const float2* wlun = S.ylun;
+    if (bucket) {
+        k_bucket_hist<<<nb, 256, 0, st>>>(S, count);
+        LK_LAUNCH_CHECK();
+        k_bucket_offsets<<<1, 1024, 0, st>>>(S, nb);
+        LK_LAUNCH_CHECK();
+        k_bucket_scatter<<<nb, 256, 0, st>>>(S, count);
+        LK_LAUNCH_CHECK();
+        wrow = S.work2;
+        wmask = S.ymask2;
+        wlun = S.ylun2;
+    }
+    k_sort_hist<<<nb, 256, hs, st>>>(S, count, S.shist, wlun);
     LK_LAUNCH_CHECK();
     k_sort_offsets<<<(S.kcols + 255) / 256, 256, 0, st>>>(S, S.shist, nb);
     LK_LAUNCH_CHECK();
@@ -2736,10 +2938,14 @@ lk_status launch_sort_tgy(const DevState& S, int64_t* stat, int sms, cudaStream_
     // (d <= 32: at most 8 float4 columns per row)
     // (the row's chain of dependent loads -- worklist, label, cursor, tile
     // label, point -- is the limit, not the bytes: see k_sort_gather)
-    k_sort_gather<<<nb, 256, hs, st>>>(S, count, S.shist);
+    k_sort_gather<<<nb, 256, hs, st>>>(S, count, S.shist, wrow, wmask, wlun);
     LK_LAUNCH_CHECK();
-    k_pair_mask<<<sms * 4, 256, 0, st>>>(S, count);
+    k_pair_mask<<<sms * 4, 256, 0, st>>>(S, count, bucket ? 1 : 0);
     LK_LAUNCH_CHECK();
+    if (bucket) {
+        k_pick_sel<<<(S.k + 127) / 128, 128, 0, st>>>(S);
+        LK_LAUNCH_CHECK();
+    }
     return LK_OK;
 }
 

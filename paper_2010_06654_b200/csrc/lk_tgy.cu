@@ -131,14 +131,18 @@ __global__ void __launch_bounds__(kThreads) k_filter_tgy(DevState S, int64_t* st
         bool need = false;
         uint32_t mask = 0;
         float lun = INFINITY;
-        if (i < S.n)
-            need = tgy_row<DP>(S, i, __ldcs(S.labels + i), __ldcs(S.ub + i), __ldcs(S.glb + i), dg, dm, rho,
+        int a = 0;
+        if (i < S.n) {
+            a = __ldcs(S.labels + i);
+            need = tgy_row<DP>(S, i, a, __ldcs(S.ub + i), __ldcs(S.glb + i), dg, dm, rho,
                                n_active, n_pairs, mask, lun);
+        }
         const int64_t pos = block_append(need, (unsigned long long*)(stat + LK_STAT_WORK), scr);
         if (need) {
+            // (the label rides along: the sort keys on it without a gather)
             S.work[pos] = (int)i;
             S.ymask[pos] = mask;
-            S.ylun[pos] = make_float2(lun, 0.f);
+            S.ylun[pos] = make_float2(lun, __int_as_float(a));
         }
     }
     warp_add(n_active, stat + LK_STAT_ACTIVE);
@@ -157,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tgy_wq(DevState S, int64
     __shared__ int qrow[kThreads / 32][kQ];
     __shared__ uint32_t qmask[kThreads / 32][kQ];
     __shared__ float qlun[kThreads / 32][kQ];
+    __shared__ int qlab[kThreads / 32][kQ];
     __shared__ float dg[32];
     const int G = S.t_groups;
     if (threadIdx.x < 32) dg[threadIdx.x] = threadIdx.x < G ? S.dgcum[threadIdx.x] : 0.f;
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tgy_wq(DevState S, int64
         for (int e = lane; e < qn; e += 32) {
             S.work[b + e] = qrow[w][e];
             S.ymask[b + e] = qmask[w][e];
-            S.ylun[b + e] = make_float2(qlun[w][e], 0.f);
+            S.ylun[b + e] = make_float2(qlun[w][e], __int_as_float(qlab[w][e]));
         }
         __syncwarp();
         qn = 0;
@@ -206,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tgy_wq(DevState S, int64
             qrow[w][off] = (int)i;
             qmask[w][off] = mask;
             qlun[w][off] = lun;
+            qlab[w][off] = a;
         }
         qn += __popc(bal);
         if (qn > kQ - 32) flush();
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tgy_wq(DevState S, int64
 }
 
 
-// Variant 1 (default for 16 < d <= 32): a streaming pipeline.  Each CTA walks
+// Variant 2: a streaming pipeline, 8 lanes per row.  Each CTA walks
 // 128-row tiles of the row range; one thread stages a tile's labels, stored
 // bounds, points and group tables with 1-D bulk copies (3 stages, ~34 KB each
 // at d = 32, 32 groups) -- every byte of the row range streams in whether the
@@ -239,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_filter_tgy_bulk(DevState S, int
     __shared__ int qrow[kThreads / 32][kQB];
     __shared__ uint32_t qmask[kThreads / 32][kQB];
     __shared__ float qlun[kThreads / 32][kQB];
+    __shared__ int qlab[kThreads / 32][kQB];
     __shared__ float dg[32];
     const int G = S.t_groups;
     const int ldx = S.ldx, nlb = S.nlb;
@@ -277,19 +284,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_filter_tgy_bulk(DevState S, int
         for (int e = lane; e < qn; e += 32) {
             S.work[b + e] = qrow[w][e];
             S.ymask[b + e] = qmask[w][e];
-            S.ylun[b + e] = make_float2(qlun[w][e], 0.f);
+            S.ylun[b + e] = make_float2(qlun[w][e], __int_as_float(qlab[w][e]));
         }
         __syncwarp();
         qn = 0;
     };
     // append the rows whose lane group leader (sub == 0) has need set
-    auto append = [&](bool need, int64_t i, uint32_t mask, float lun) {
+    auto append = [&](bool need, int64_t i, uint32_t mask, float lun, int lab) {
         const unsigned bal = __ballot_sync(LK_FULL_MASK, need);
         if (need) {
             const int off = qn + __popc(bal & lanemask_lt());
             qrow[w][off] = (int)i;
             qmask[w][off] = mask;
             qlun[w][off] = lun;
+            qlab[w][off] = lab;
         }
         qn += __popc(bal);
         if (qn > kQB - 32) flush();
@@ -379,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_filter_tgy_bulk(DevState S, int
                 n_active += active;
                 if (need) n_pairs += __popc(mask);
             }
-            append(need && sub == 0, i, mask, lun);
+            append(need && sub == 0, i, mask, lun, a[rr]);
         }
         __syncthreads();  // stage st_ consumed
         if (tid == 0 && j + kST < n_my) issue(j + kST, st_);
@@ -391,13 +399,190 @@ __global__ void __launch_bounds__(kThreads, 2) k_filter_tgy_bulk(DevState S, int
             bool need = false;
             uint32_t mask = 0;
             float lun = INFINITY;
+            int la = 0;
             if (i < S.n) {
                 int64_t na = 0, np = 0;
-                need = tgy_row<DP>(S, i, S.labels[i], S.ub[i], S.glb[i], dg, dm, rho, na, np, mask, lun);
+                la = S.labels[i];
+                need = tgy_row<DP>(S, i, la, S.ub[i], S.glb[i], dg, dm, rho, na, np, mask, lun);
                 n_active += na;
                 n_pairs += np;
             }
-            append(need, i, mask, lun);
+            append(need, i, mask, lun, la);
+        }
+    }
+    if (qn) flush();
+    warp_add(n_active, stat + LK_STAT_ACTIVE);
+    warp_add(n_pairs, stat + LK_STAT_PAIRS);
+}
+
+// Variant 4 (default for 16 < d <= 32): the streaming pipeline of variant 1
+// with a thread per row.  The 8-lanes-per-row form issues ~1800 thread
+// instructions per row (every lane repeats the row's scalar work and 15
+// shuffles; ncu: issue-active 51% at 16 warps per SM, DRAM 35%), so it is
+// bound by instruction issue, not by HBM.  Here a tile's 128 rows are staged
+// the same way (1-D bulk copies, 2 stages per CTA, 3 CTAs per SM) and thread r
+// walks row r's point and group table in shared memory, the float4 columns
+// rotated by r so that a quarter-warp's eight threads read eight different
+// bank groups (conflict-free at 128-byte rows); the own centroid's row comes
+// through L1/L2 in the same rotated order.
+constexpr int kSR = 128;   // rows per tile = threads per CTA
+constexpr int kSS = 2;     // stages
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kSR, 3) k_filter_tgy_srow(DevState S, int64_t* stat) {
+    if (*S.done) return;
+    extern __shared__ __align__(128) uint8_t fsm[];
+    __shared__ uint64_t fbar[kSS];
+    __shared__ int qrow[kSR / 32][kQB];
+    __shared__ uint32_t qmask[kSR / 32][kQB];
+    __shared__ float qlun[kSR / 32][kQB];
+    __shared__ int qlab[kSR / 32][kQB];
+    __shared__ __align__(16) float dg[32];
+    const int G = S.t_groups;
+    const int ldx = S.ldx, nlb = S.nlb;  // (both 32: the launcher checks)
+    const int SB = kSR * (12 + 4 * ldx + 4 * nlb);
+    const int64_t n_full = S.n / kSR;  // full tiles
+    const int64_t n_my = n_full > blockIdx.x ? (n_full - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    if (tid < 32) dg[tid] = tid < G ? S.dgcum[tid] : 0.f;
+    auto issue = [&](int64_t j, int st_) {
+        const int64_t r0 = (blockIdx.x + j * gridDim.x) * (int64_t)kSR;
+        uint8_t* b = fsm + (size_t)st_ * SB;
+        mbar_expect_tx(&fbar[st_], (uint32_t)SB);
+        bulk_load(b, S.labels + r0, kSR * 4, &fbar[st_]);
+        bulk_load(b + kSR * 4, S.ub + r0, kSR * 4, &fbar[st_]);
+        bulk_load(b + kSR * 8, S.glb + r0, kSR * 4, &fbar[st_]);
+        bulk_load(b + kSR * 12, S.X32 + r0 * ldx, (uint32_t)(kSR * ldx * 4), &fbar[st_]);
+        bulk_load(b + kSR * (12 + 4 * ldx), S.lb + r0 * nlb, (uint32_t)(kSR * nlb * 4), &fbar[st_]);
+    };
+    if (tid == 0) {
+        for (int e = 0; e < kSS; e++) mbar_init(&fbar[e], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int e = 0; e < kSS && e < n_my; e++) issue(e, e);
+    }
+    __syncthreads();
+    const float dm = S.scal[4];
+    const float rho = simt_rel_err(S.d);
+    int64_t n_active = 0, n_pairs = 0;
+    int qn = 0;  // (warp-uniform)
+    auto flush = [&]() {
+        __syncwarp();
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd((unsigned long long*)(stat + LK_STAT_WORK), (unsigned long long)qn);
+        b = __shfl_sync(LK_FULL_MASK, b, 0);
+        for (int e = lane; e < qn; e += 32) {
+            S.work[b + e] = qrow[w][e];
+            S.ymask[b + e] = qmask[w][e];
+            S.ylun[b + e] = make_float2(qlun[w][e], __int_as_float(qlab[w][e]));
+        }
+        __syncwarp();
+        qn = 0;
+    };
+    auto append = [&](bool need, int64_t i, uint32_t mask, float lun, int lab) {
+        const unsigned bal = __ballot_sync(LK_FULL_MASK, need);
+        if (need) {
+            const int off = qn + __popc(bal & lanemask_lt());
+            qrow[w][off] = (int)i;
+            qmask[w][off] = mask;
+            qlun[w][off] = lun;
+            qlab[w][off] = lab;
+        }
+        qn += __popc(bal);
+        if (qn > kQB - 32) flush();
+    };
+    // groups past G never scan and never bound: v = lb - (-inf) = +inf
+    if (tid < 32 && tid >= G) dg[tid] = -INFINITY;
+    __syncthreads();
+    const float rho1 = 1.0f + rho + 4.76837158203125e-07f;  // (+ 2^-21: the approximate square roots)
+    for (int64_t j = 0; j < n_my; j++) {
+        const int st_ = (int)(j % kSS);
+        const int64_t i = (blockIdx.x + j * gridDim.x) * (int64_t)kSR + tid;
+        mbar_wait(&fbar[st_], (uint32_t)((j / kSS) & 1));
+        const uint8_t* b = fsm + (size_t)st_ * SB;
+        const int a = reinterpret_cast<const int*>(b)[tid];
+        const float ub_s = reinterpret_cast<const float*>(b + kSR * 4)[tid];
+        const float glb_s = reinterpret_cast<const float*>(b + kSR * 8)[tid];
+        const float4* spt = reinterpret_cast<const float4*>(b + kSR * 12) + tid * 8;
+        const float4* slb = reinterpret_cast<const float4*>(b + kSR * (12 + 4 * 32)) + tid * 8;
+        // everything indexed by the label is requested at once (one L2 round
+        // trip); rows that pass the global gate (16% at cfg5) load it in vain
+        const float4* cp = reinterpret_cast<const float4*>(S.C32 + (int64_t)a * S.ldc);
+        float4 cv[8];
+#pragma unroll
+        for (int c = 0; c < 8; c++) cv[c] = __ldg(cp + ((c + tid) & 7));
+        const float dca = __ldg(S.dcum + a);
+        const float sa = __ldg(S.s_half + a);
+        const float cna = __ldg(S.cnorm + a);
+        const int ga = __ldg(S.group_of + a);
+        // tighten (fp32 difference form, certified)
+        float acc = 0.f, xn2 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const float4 x = spt[(c + tid) & 7];
+            const float t0 = x.x - cv[c].x, t1 = x.y - cv[c].y, t2 = x.z - cv[c].z, t3 = x.w - cv[c].w;
+            acc = fmaf(t3, t3, fmaf(t2, t2, fmaf(t1, t1, fmaf(t0, t0, acc))));
+            xn2 = fmaf(x.w, x.w, fmaf(x.z, x.z, fmaf(x.y, x.y, fmaf(x.x, x.x, xn2))));
+        }
+        const float u0 = __fadd_ru(ub_s, dca);
+        const float gate = fmaxf(__fsub_rd(glb_s, dm), sa);
+        const bool active = !(gate > u0);
+        // (sqrt.approx: relative error <= 2^-23, covered by rho1)
+        const float U = (sqrt_approx(acc) + kU32 * (sqrt_approx(xn2) + cna)) * rho1;
+        const bool tight = U < u0;
+        const float u = fminf(u0, U);
+        const bool fail = active && !(gate > u);
+        // the group gate, branch-free: the mask of the groups to scan (the
+        // label's own group included) and the bound over the others
+        float gmin = INFINITY, lun = INFINITY;
+        uint32_t mask = 0;
+        const unsigned gac = (unsigned)ga >> 2, gab = 1u << (ga & 3);
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const int cc = (c + tid) & 7;
+            const float4 q = slb[cc];
+            const float4 dq = reinterpret_cast<const float4*>(dg)[cc];
+            const unsigned ob = (unsigned)cc == gac ? gab : 0u;
+            const float v0 = __fsub_rd(q.x, dq.x), v1 = __fsub_rd(q.y, dq.y);  // (a negative lower bound is still valid)
+            const float v2 = __fsub_rd(q.z, dq.z), v3 = __fsub_rd(q.w, dq.w);
+            gmin = fminf(gmin, fminf(fminf(v0, v1), fminf(v2, v3)));
+            const bool s0 = !(v0 > u) || (ob & 1u), s1 = !(v1 > u) || (ob & 2u);
+            const bool s2 = !(v2 > u) || (ob & 4u), s3 = !(v3 > u) || (ob & 8u);
+            const unsigned nib = (s0 ? 1u : 0u) | (s1 ? 2u : 0u) | (s2 ? 4u : 0u) | (s3 ? 8u : 0u);
+            mask |= nib << (4 * cc);
+            lun = fminf(lun, fminf(fminf(s0 ? INFINITY : v0, s1 ? INFINITY : v1),
+                                   fminf(s2 ? INFINITY : v2, s3 ? INFINITY : v3)));
+        }
+        const bool need = fail && !(fmaxf(gmin, sa) > u);
+        if (fail && !need) S.glb[i] = __fadd_rd(gmin, dm);  // every group prunes: their minimum is the global bound
+        if (active && tight && !need) S.ub[i] = __fsub_ru(u, dca);
+        n_active += active;
+        if (need) n_pairs += __popc(mask);
+        append(need, i, mask, lun, a);
+        __syncthreads();  // stage st_ consumed
+        if (tid == 0 && j + kSS < n_my) issue(j + kSS, st_);
+    }
+    // rows past the last full tile: one thread per row from global memory
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int64_t i0 = n_full * kSR; i0 < S.n; i0 += kSR) {
+            const int64_t i = i0 + tid;
+            bool need = false;
+            uint32_t mask = 0;
+            float lun = INFINITY;
+            int la = 0;
+            if (i < S.n) {
+                int64_t na = 0, np = 0;
+                la = S.labels[i];
+                need = tgy_row<DP>(S, i, la, S.ub[i], S.glb[i], dg, dm, rho, na, np, mask, lun);
+                n_active += na;
+                n_pairs += np;
+            }
+            append(need, i, mask, lun, la);
         }
     }
     if (qn) flush();
@@ -414,15 +599,27 @@ lk_status launch_filter_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaS
     int64_t blocks = (S.n + lk::tgy::kThreads - 1) / lk::tgy::kThreads;
     if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
     if (blocks < 1) blocks = 1;
-    // LK_TGY_FILTER (A/B knob): 1 (default) the streaming pipeline where it
-    // applies (16 < d <= 32), else 0; 0 a thread per row with block-aggregated
-    // appends; 2 the streaming pipeline forced; 3 a thread per row with warp queues
+    // LK_TGY_FILTER (A/B knob): 1 (default) the streaming pipeline with a
+    // thread per row where it applies (128-byte points and group tables:
+    // 28 < d <= 32, 29..32 groups), else 0; 0 a thread per row from global
+    // memory with block-aggregated appends; 2 the streaming pipeline with 8
+    // lanes per row; 3 a thread per row with warp queues
     static const int variant = [] {
         const char* e = getenv("LK_TGY_FILTER");
         return e ? atoi(e) : 1;
     }();
     const bool bulk_ok = S.nlb % 4 == 0 && S.ldx % 4 == 0;
-    if (bulk_ok && (variant == 2 || (variant == 1 && S.d > 16))) {
+    if (bulk_ok && S.nlb == 32 && S.ldx == 32 && (variant == 4 || variant == 1)) {
+        // the streaming pipeline, a thread per row: three CTAs per SM
+        const int smem = lk::tgy::kSS * lk::tgy::kSR * (12 + 4 * S.ldx + 4 * S.nlb);
+        static bool attr4 = false;
+        if (!attr4) {
+            LK_CUDA_CHECK(cudaFuncSetAttribute(lk::tgy::k_filter_tgy_srow<32>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024));
+            attr4 = true;
+        }
+        lk::tgy::k_filter_tgy_srow<32><<<(unsigned)(sms * 3), lk::tgy::kSR, smem, st>>>(S, stat);
+    } else if (bulk_ok && (variant == 2 || variant == 5)) {
         // the streaming pipeline: one wave of two CTAs per SM
         constexpr int kMaxSmem = 110 * 1024;
         const int smem = lk::tgy::kST * lk::tgy::tgy_bulk_stage_bytes(S.ldx, S.nlb);

@@ -76,6 +76,22 @@ def test_group_tiles_4096_centroids(oracle):
     assert centroid_ok(res.centroids, ref["centroids"], x)
 
 
+def test_streaming_filter_partial_groups_ragged_rows(oracle):
+    """The thread-per-row streaming filter (128-byte points and group tables)
+    with 29 of 32 group slots in use and a row count that is not a multiple of
+    the 128-row tile."""
+    from paper_2010_06654_b200 import datasets
+    x = datasets.generate("cfg5", 33333)
+    k = 3700
+    m = lk()
+    init = m.make_init(m.RunContext(seed=77), x, k, "random")
+    ref = oracle.run_lloyd(x, k, init, 6)
+    res = m.run_pruner(x, k, "yinyang", init=init, t_max=6)
+    check_trajectory(oracle, x, init, res.assign_history, ref["history"], "k=3700 ragged")
+    assert centroid_ok(res.centroids, ref["centroids"], x)
+    assert len(res.iterations) == ref["iterations"]
+
+
 OFF_CASE = r"""
 import sys, numpy as np
 sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})

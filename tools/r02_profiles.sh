@@ -16,5 +16,5 @@ done
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cfg5.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > $O/ncu_launches.log 2>&1; echo "launches=$?"
 timeout 1500 ncu --set full --import-source on --clock-control none \
-    -k regex:"k_assign_tgy|k_filter_tgy|k_sort_gather|k_assign_tc" --launch-skip 12 --launch-count 4 \
+    -k regex:"k_assign_tgy|k_filter_tgy|k_sort_gather|k_assign_tc|k_recheck_cand|k_sort_hist" --launch-skip 18 --launch-count 6 \
     -o $O/ncu_full_cfg5 python bench.py --steps 2 --warmup 3 --no-cpu > $O/ncu_full.log 2>&1; echo "ncu_full=$?"
