@@ -42,7 +42,7 @@ enum InternalBuf {
     B_GPERM, B_GOFF, B_YWL, B_YPAIRS, B_YRES, B_GINV, B_CG, B_YLUN, B_YAUX, B_YPAIRS4, B_YBUCKET,
     B_SELF, B_DCUM, B_DGCUM, B_GLB, B_PTAB, B_PERM, B_LCUR, B_TILE_LAB, B_ROWR, B_ROWXO, B_ROWBV, B_ROWXN2, B_ROWLAB,
     B_YMASK, B_PMASK, B_SHIST, B_TMETA, B_VALID, B_CCH, B_RGSCR, B_RGMEANS, B_DCUMCOL,
-    B_WORK2, B_YMASK2, B_YLUN2, B_GFREQ, B_GSEL, B_BHIST, B_BBASE, B_COUNT_
+    B_WORK2, B_YMASK2, B_YLUN2, B_GFREQ, B_GSEL, B_BHIST, B_BBASE, B_PINFO, B_COUNT_
 };
 
 struct Layout {
@@ -217,6 +217,7 @@ static bool make_layout(const lk_config& c, Layout* L) {
         L->size[B_GSEL] = (uint64_t)k * 4;
         L->size[B_BHIST] = (uint64_t)1536 * 64 * 4;
         L->size[B_BBASE] = 64 * 4;
+        L->size[B_PINFO] = (uint64_t)(n / 256 + 2) * 16;
         L->size[B_DCUM] = (uint64_t)k * 4;
         L->size[B_DCUMCOL] = (uint64_t)kpad * 4;
         L->size[B_DGCUM] = (uint64_t)L->groups * 4;
@@ -532,6 +533,7 @@ lk_status lk_ctx_create(lk_ctx** out, const lk_config* cfg, void* workspace, uin
     S.gsel = buf<uint32_t>(c, B_GSEL);
     S.bhist = buf<int32_t>(c, B_BHIST);
     S.bbase = buf<int32_t>(c, B_BBASE);
+    S.pinfo = buf<int4>(c, B_PINFO);
     S.hlog_inline = (S.lazy && S.hlog != nullptr && S.hlog_cap > 0) ? 1 : 0;
     {
         const char* e = getenv("LK_SGATE");  // A/B knob for the centroid-separation gate
@@ -890,7 +892,7 @@ lk_status lk_step_assign(lk_ctx* c, int32_t t, void* stream) {
             ProfScope p(c, 0, st);
             s = lkh::launch_assign_tgy(S, stat, n, c->sms, st);
             if (s != LK_OK) return s;
-            c->launches += lkh::tgy_bucket_on(S) ? 12 : 8;
+            c->launches += lkh::tgy_bucket_on(S) ? 13 : 9;
         } else if (group_mode(c->cfg)) {
             // tensor-core runs: every row failing the bounds is rescanned in full
             const bool full_only = use_tc;

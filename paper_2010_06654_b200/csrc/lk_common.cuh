@@ -144,6 +144,7 @@ struct DevState {
     uint32_t* gsel;         // [k] the groups whose mask bits form a label's bucket key
     int32_t* bhist;         // [tgy_sort_blocks, 64] per-block bucket counts / offsets
     int32_t* bbase;         // [64] bucket bases
+    int4* pinfo;            // [n / 256 + 2] per row-tile pair of the sorted worklist (k_pair_info)
     // Elkan's per-centroid bounds (lk_elkan.cu): lb is [k, n]
     int32_t elkan;
     float* cch;             // [k, k] certified lower bound of 1/2 ||c_a - c_j||

@@ -1370,18 +1370,22 @@ __device__ __forceinline__ TgyLow tgy_low_setup(double R, double xo, float kappa
     return t;
 }
 
-// Square roots bounded from below / above: the correctly rounded sqrtf (within
-// half an ulp) moved one ulp down / up -- cheaper than the directed-rounding
-// __fsqrt_rd / __fsqrt_ru sequences.
+// Square roots bounded from below / above, cheaper than the directed-rounding
+// __fsqrt_rd / __fsqrt_ru sequences (and than sqrtf's Newton step and slow path).
+// (sqrt.approx.f32: one MUFU op, relative error <= 2^-23 over the positive
+// finite range, subnormals included; the bounds take 2^-21 of margin)
+__device__ __forceinline__ float sqrt_mufu(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float sqrt_lo(float x) {
     if (!(x > 0.f)) return 0.f;
-    const float r = sqrtf(x);
-    return isinf(r) ? r : __int_as_float(__float_as_int(r) - 1);
+    return __fmul_rd(sqrt_mufu(x), 1.0f - 4.76837158203125e-07f);  // (+inf stays +inf)
 }
 __device__ __forceinline__ float sqrt_hi(float x) {
     if (!(x > 0.f)) return 0.f;
-    const float r = sqrtf(x);
-    return isinf(r) ? r : __int_as_float(__float_as_int(r) + 1);
+    return __fmul_ru(sqrt_mufu(x), 1.0f + 4.76837158203125e-07f);
 }
 
 __device__ __forceinline__ float tgy_lower32(const TgyLow& t, float v) {
@@ -1422,7 +1426,11 @@ struct TgySmem {
 enum TgyProf {
     TP_P_AEMPTY, TP_P_EMPTY, TP_P_REMPTY, TP_P_TOTAL, TP_M_AFULL, TP_M_TEMPTY, TP_M_FULL, TP_M_TOTAL,
     TP_E_TFULL, TP_E_RFULL, TP_E_TILES, TP_E_TAIL, TP_E_TOTAL, TP_PAIRS, TP_TILES,
-    TP_T_CERT, TP_T_GROUPS, TP_T_STORES, TP_T_APPEND, TP_N
+    TP_T_CERT, TP_T_GROUPS, TP_T_STORES, TP_T_APPEND,
+#ifdef LK_TGY_PROF_CHUNKS
+    TP_C_LOAD, TP_C_FAST, TP_C_SLOW, TP_C_MINE, TP_C_SLOWN,
+#endif
+    TP_N
 };
 #define TGY_W(idx, call)                                        \
     do {                                                        \
@@ -1504,6 +1512,9 @@ __global__ void __launch_bounds__(352, 1)
     const int64_t m = *A.rowcount;
     const bool prof_on = A.prof != nullptr;
     long long pc[TP_N];
+#ifdef LK_TGY_PROF_CHUNKS
+    uint32_t pcc[5] = {0, 0, 0, 0, 0};  // chunk-level clocks of epilogue warp 0 (build-time probe)
+#endif
 #pragma unroll
     for (int e = 0; e < TP_N; e++) pc[e] = 0;
     const long long tk0 = prof_on ? clock64() : 0;
@@ -1561,12 +1572,16 @@ __global__ void __launch_bounds__(352, 1)
         if (lane == 0) {
             int stage = 0, rs = 0;
             uint32_t phase = 0, rphase = 0;
+            int4 pi_n = n_it > 0 ? __ldg(S.pinfo + blockIdx.x) : make_int4(0, 0, 0, 0);  // (one pair ahead)
             for (int it = 0; it < n_it; it++) {
                 const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
-                const uint32_t pm = __ldg(S.pmask + 2 * rp) | __ldg(S.pmask + 2 * rp + 1);
-                const float* bt0 = beta_of(2 * rp);
-                const float* bt1 = beta_of(2 * rp + 1);
-                const int g0 = tgy_rot(S, 2 * rp);
+                const int4 pi = pi_n;
+                if (it + 1 < n_it) pi_n = __ldg(S.pinfo + rp + gridDim.x);
+                const uint32_t pm = (uint32_t)pi.x | (uint32_t)pi.y;
+                const int l0 = (pi.w & 0xffff) - 1, l1 = ((unsigned)pi.w >> 16) - 1;
+                const float* bt0 = l0 >= 0 ? S.ptab + (int64_t)l0 * S.kpad : S.cn2;
+                const float* bt1 = l1 >= 0 ? S.ptab + (int64_t)l1 * S.kpad : S.cn2;
+                const int g0 = pi.z & 31;
                 for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
                     const int ct = (__ffs(mm) - 1 + g0) & 31;
                     TGY_W(TP_P_EMPTY, mbar_wait(&empty[stage], phase ^ 1));
@@ -1595,10 +1610,13 @@ __global__ void __launch_bounds__(352, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         int64_t n_dist = 0;
+        int4 pi_n = n_it > 0 ? __ldg(S.pinfo + blockIdx.x) : make_int4(0, 0, 0, 0);  // (one pair ahead)
         for (int it = 0; it < n_it; it++) {
             const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
+            const int4 pi = pi_n;
+            if (it + 1 < n_it) pi_n = __ldg(S.pinfo + rp + gridDim.x);
             // each row tile runs only the centroid tiles of its own mask
-            const uint32_t m0 = __ldg(S.pmask + 2 * rp), m1 = __ldg(S.pmask + 2 * rp + 1);
+            const uint32_t m0 = (uint32_t)pi.x, m1 = (uint32_t)pi.y;
             const uint32_t pm = m0 | m1;
             const int64_t r0n = m - 2 * rp * BM < BM ? m - 2 * rp * BM : BM;
             const int64_t r1n = m - (2 * rp + 1) * BM < BM ? (m - (2 * rp + 1) * BM > 0 ? m - (2 * rp + 1) * BM : 0) : BM;
@@ -1607,7 +1625,7 @@ __global__ void __launch_bounds__(352, 1)
             TGY_W(TP_M_AFULL, tgy_split_tile(xs, abuf, 1, sfull, aempty, sdone, it, lane));
             TGY_W(TP_M_AFULL, mbar_wait(sdone, it & 1));
             tc_fence_after();
-            const int g0 = tgy_rot(S, 2 * rp);
+            const int g0 = pi.z & 31;
             for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
                 TGY_W(TP_M_TEMPTY, mbar_wait(&tempty[acc], acc_phase ^ 1));
                 tc_fence_after();
@@ -1685,12 +1703,15 @@ __global__ void __launch_bounds__(352, 1)
             }
         };
         load_meta(0);
+        int4 pi_n = n_it > 0 ? __ldg(S.pinfo + blockIdx.x) : make_int4(0, 0, 0, 0);  // (one pair ahead)
         for (int it = 0; it < n_it; it++) {
             const int64_t rp = blockIdx.x + (int64_t)it * gridDim.x;
+            const int4 pi = pi_n;
+            if (it + 1 < n_it) pi_n = __ldg(S.pinfo + rp + gridDim.x);
             // the pair's tiles stream in for the union of the two row tiles'
             // masks; this row tile evaluates only its own (ms)
-            const uint32_t ms = __ldg(S.pmask + 2 * rp + s);
-            const uint32_t pm = __ldg(S.pmask + 2 * rp) | __ldg(S.pmask + 2 * rp + 1);
+            const uint32_t ms = (uint32_t)(s ? pi.y : pi.x);
+            const uint32_t pm = (uint32_t)pi.x | (uint32_t)pi.y;
             const int64_t rt = 2 * rp + s;
             const int64_t r = rt * BM + q * 32 + lane;
             const bool valid = r < m;
@@ -1717,7 +1738,11 @@ __global__ void __launch_bounds__(352, 1)
             // group's bound is formed and stored as soon as its tile is done
             const TgyLow tl = tgy_low_setup(R, xo, kappa, cmax_f, S.d);
             float* lbr = S.lb + row * S.nlb;
-            const int g0 = tgy_rot(S, 2 * rp);
+            const int g0 = pi.z & 31;
+            // the B column of this row tile's label: its 64-column chunk runs
+            // first (it sets the rows' best, so the tile's other chunk seldom
+            // needs the exact top-2)
+            const int acol = (int)(((unsigned)pi.z >> (s ? 18 : 5)) & 0x1fffu) - 1;
             for (uint32_t mm = rotr32(pm, g0); mm; mm &= mm - 1) {
                 const int ct = (__ffs(mm) - 1 + g0) & 31;
                 TGY_W(TP_E_TFULL, mbar_wait(&tfull[acc], acc_phase));
@@ -1729,9 +1754,14 @@ __global__ void __launch_bounds__(352, 1)
                 const uint32_t sb0 = smem_u32(ring + rs * 256 + s * 128);
                 float gmin = INFINITY;
                 const bool mine = (ms >> ct) & 1u;  // (warp-uniform)
+                const int cf = (acol >= 0 && (acol >> 7) == ct) ? (acol & 64) : 0;
 #pragma unroll 1
-                for (int c0 = 0; c0 < (mine ? BN : 0); c0 += 64) {
+                for (int ci = 0; ci < ((mine && A.dbg != 4) ? 2 : 0); ci++) {
+                    const int c0 = ci == 0 ? cf : 64 - cf;
                     uint32_t r0[32], r1[32];
+#ifdef LK_TGY_PROF_CHUNKS
+                    const long long tc0 = prof_on ? clock64() : 0;
+#endif
                     tmem_ld32_async(taddr + c0, r0);
                     tmem_ld32_async(taddr + c0 + 32, r1);
                     const int jb = ct * BN + c0;
@@ -1743,6 +1773,9 @@ __global__ void __launch_bounds__(352, 1)
                                      : "=f"(cv[c4].x), "=f"(cv[c4].y), "=f"(cv[c4].z), "=f"(cv[c4].w)
                                      : "r"(sb + 16 * c4));
                     tmem_wait_ld();
+#ifdef LK_TGY_PROF_CHUNKS
+                    const long long tc1 = prof_on ? clock64() : 0;
+#endif
                     float dv[64];
 #pragma unroll
                     for (int c4 = 0; c4 < 16; c4++) {
@@ -1772,9 +1805,20 @@ __global__ void __launch_bounds__(352, 1)
                     // (the first tile of a row, and rows about to move), so the
                     // exact top-2 of the chunk -- a merge tree, no serial chain
                     // -- runs only when some row of the warp has one.
-                    if (!__any_sync(LK_FULL_MASK, mc < b1)) {
+#ifdef LK_TGY_PROF_CHUNKS
+                    const long long tc2 = prof_on ? clock64() : 0;
+                    if (prof_on) {
+                        pcc[0] += (uint32_t)(tc1 - tc0);
+                        pcc[1] += (uint32_t)(tc2 - tc1);
+                        pcc[3]++;
+                    }
+#endif
+                    if (A.dbg == 1 || !__any_sync(LK_FULL_MASK, mc < b1)) {
                         b2 = fminf(b2, mc);
                     } else {
+#ifdef LK_TGY_PROF_CHUNKS
+                        pcc[4]++;
+#endif
                         float g1v[8], g2v[8];
 #pragma unroll
                         for (int g8 = 0; g8 < 8; g8++) {
@@ -1816,6 +1860,9 @@ __global__ void __launch_bounds__(352, 1)
                             }
                         }
                     }
+#ifdef LK_TGY_PROF_CHUNKS
+                    if (prof_on) pcc[2] += (uint32_t)(clock64() - tc2);
+#endif
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -1830,13 +1877,14 @@ __global__ void __launch_bounds__(352, 1)
                 // row's own failing groups (measured: the tile's other groups then
                 // keep older, weaker bounds and fail later -- 1.3e10 -> 1.75e10
                 // products at cfg5 iteration 20).
-                if (mine && valid) __stcg(lbr + ct, __fadd_rd(tgy_lower32(tl, gmin), sdg[ct]));
+                if (mine && valid && A.dbg != 2) __stcg(lbr + ct, __fadd_rd(tgy_lower32(tl, gmin), sdg[ct]));
                 if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
                 if (++rs == NBB) { rs = 0; rphase ^= 1; }
                 if (prof_on) pc[TP_E_TILES] += clock64() - tt0;
             }
             const long long tl0 = prof_on ? clock64() : 0;
             pc[TP_PAIRS]++;
+            if (A.dbg == 3) continue;  // (timing probe: no pair tail)
             // the winning column (searched and holding the minimum), its centroid
             // id and cumulative drift: both loads go out before the math
             const int jc = (bj >= 0 && bv == b1) ? bj : -1;
@@ -1924,6 +1972,10 @@ __global__ void __launch_bounds__(352, 1)
         if (warp == PW) pc[TP_P_TOTAL] = tot;
         if (warp == MW) pc[TP_M_TOTAL] = tot;
         if (warp == 0) pc[TP_E_TOTAL] = tot;
+#ifdef LK_TGY_PROF_CHUNKS
+        if (warp == 0)
+            for (int e = 0; e < 5; e++) pc[TP_C_LOAD + e] = pcc[e];
+#endif
         for (int e = 0; e < TP_N; e++)
             if (pc[e]) atomicAdd(A.prof + e, (unsigned long long)pc[e]);
     }
@@ -1966,6 +2018,32 @@ __global__ void k_pair_mask(DevState S, const int64_t* count, int freq) {
             }
             if (lab >= 0 && mine > 0) atomicAdd(S.gfreq + (int64_t)lab * 32 + lane, mine);
         }
+    }
+}
+
+// Per row-tile pair of the sorted worklist, everything the pass's three roles
+// derive from the pair's tile labels and masks, in one 16-byte record (no
+// dependent loads at the start of a pair): x / y the two row tiles' masks,
+// z = group of the first tile's label | (B column of tile 0's label + 1) << 5
+// | (of tile 1's + 1) << 18, w = (label 0 + 1) | (label 1 + 1) << 16.
+__global__ void k_pair_info(DevState S, const int64_t* count) {
+    if (*S.done) return;
+    const int64_t m = *count;
+    const int64_t nt = (m + 127) / 128, np = (nt + 1) / 2;
+    for (int64_t rp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rp <= np;
+         rp += (int64_t)gridDim.x * blockDim.x) {
+        int4 v = make_int4(0, 0, 0, 0);
+        if (rp < np) {
+            const int l0 = 2 * rp < nt ? S.tile_lab[2 * rp] : -1;
+            const int l1 = 2 * rp + 1 < nt ? S.tile_lab[2 * rp + 1] : -1;
+            v.x = (int)S.pmask[2 * rp];
+            v.y = 2 * rp + 1 < nt ? (int)S.pmask[2 * rp + 1] : 0;
+            const int g0 = l0 >= 0 ? S.group_of[l0] : 0;
+            const int a0 = l0 >= 0 ? S.ginv[l0] : -1, a1 = l1 >= 0 ? S.ginv[l1] : -1;
+            v.z = g0 | ((a0 + 1) << 5) | ((a1 + 1) << 18);
+            v.w = (l0 + 1) | ((l1 + 1) << 16);
+        }
+        S.pinfo[rp] = v;
     }
 }
 
@@ -2901,7 +2979,11 @@ static void tgy_prof_dump() {
     static const char* names[] = {"P_aempty", "P_empty", "P_rempty", "P_total", "M_afull", "M_tempty",
                                   "M_full", "M_total", "E_tfull", "E_rfull", "E_tiles", "E_tail",
                                   "E_total", "pairs(warp0)", "tiles(warp0)", "T_cert", "T_groups",
-                                  "T_stores", "T_append"};
+                                  "T_stores", "T_append",
+#ifdef LK_TGY_PROF_CHUNKS
+                                  "C_load", "C_fast", "C_slow", "chunks(warp0)", "slow_chunks(warp0)"
+#endif
+    };
     fprintf(stderr, "k_assign_tgy phase clocks (sum over CTAs, lane 0 of producer / MMA / epilogue warp 0):");
     for (int e = 0; e < TP_N; e++) fprintf(stderr, " %s=%llu", names[e], g_tgy_prof[e]);
     fprintf(stderr, "\n");
@@ -2965,6 +3047,8 @@ lk_status launch_sort_tgy(const DevState& S, int64_t* stat, int sms, cudaStream_
     LK_LAUNCH_CHECK();
     k_pair_mask<<<sms * 4, 256, 0, st>>>(S, count, bucket ? 1 : 0);
     LK_LAUNCH_CHECK();
+    k_pair_info<<<sms, 256, 0, st>>>(S, count);
+    LK_LAUNCH_CHECK();
     if (bucket) {
         k_pick_sel<<<(S.k + 127) / 128, 128, 0, st>>>(S);
         LK_LAUNCH_CHECK();
@@ -2989,6 +3073,15 @@ lk_status launch_assign_tgy(const DevState& S, int64_t* stat, int64_t max_rows, 
     A.n_kc = 1;
     A.n_ct = S.t_groups;
     A.prof = tgy_prof_buffer();
+    {
+        // LK_TGY_DBG=v LK_TGY_DBG_AT=N (timing probes, wrong results): launch N
+        // (1-based; 0: every launch) runs without 1 the chunks' exact top-2,
+        // 2 the per-tile group bounds, 3 the pair tail, 4 the chunk math
+        static int dbg_launch = 0;
+        static const int dbg = env_int("LK_TGY_DBG", 0), dbg_at = env_int("LK_TGY_DBG_AT", 0);
+        dbg_launch++;
+        A.dbg = (dbg && (dbg_at == 0 || dbg_at == dbg_launch)) ? dbg : 0;
+    }
     {
         // LK_TGY_PROF_SKIP=N: the first N launches run without the clocks
         static int launches = 0;
