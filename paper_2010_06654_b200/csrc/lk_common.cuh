@@ -162,7 +162,11 @@ __device__ __forceinline__ float store_ub(const DevState& S, float U, int label)
 }
 
 // Blocks of the group-tile worklist sort (lk_tc.cu k_sort_*): three per SM (one wave at 72 registers).
-inline int tgy_sort_blocks(int sms) { return 3 * (sms > 0 ? sms : 148) > 1536 ? 1536 : 3 * (sms > 0 ? sms : 148); }
+inline int tgy_sort_blocks(int sms) {
+    // four resident blocks per SM (k_sort_gather: 64 registers, 40 KB of shared memory)
+    const int nb = 4 * (sms > 0 ? sms : 148);
+    return nb > 1536 ? 1536 : nb;
+}
 
 // numpy pairwise-sum association program passed by value (k-means++ D^2
 // updates): (0, start, len) = leaf, (1, 0, 0) = add the two top values.

@@ -2448,7 +2448,7 @@ struct SortStage {
     float lun[kSortSlice];
 };
 
-__global__ void __launch_bounds__(256) k_sort_gather(DevState S, const int64_t* count, const int* hist,
+__global__ void __launch_bounds__(256, 4) k_sort_gather(DevState S, const int64_t* count, const int* hist,
                                                      const int32_t* __restrict__ wrow,
                                                      const uint32_t* __restrict__ wmask,
                                                      const float2* __restrict__ wlun) {
