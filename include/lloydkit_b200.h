@@ -159,7 +159,9 @@ typedef struct lk_ctx lk_ctx;
 lk_status lk_ctx_create(lk_ctx **out, const lk_config *cfg, void *workspace, uint64_t bytes);
 lk_status lk_ctx_destroy(lk_ctx *ctx);
 
-/* Byte offset and size of a named buffer inside the workspace. */
+/* Byte offset and size of a named buffer inside the workspace.  (ids 1000 / 1001 report two
+ * internal buffers of the group-tile worklist to tools/tile_stats.py: a debug aid, not part of
+ * the interface.) */
 lk_status lk_buffer(const lk_ctx *ctx, int32_t id, uint64_t *offset, uint64_t *bytes);
 /* Row stride (floats) of LK_BUF_X32 and the length of LK_BUF_DELTA (int64s). */
 lk_status lk_layout(const lk_ctx *ctx, int64_t *ldx, int64_t *delta_len, int32_t *nlb);

@@ -420,13 +420,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_filter_tgy_bulk(DevState S, int
 // instructions per row (every lane repeats the row's scalar work and 15
 // shuffles; ncu: issue-active 51% at 16 warps per SM, DRAM 35%), so it is
 // bound by instruction issue, not by HBM.  Here a tile's 128 rows are staged
-// the same way (1-D bulk copies, 2 stages per CTA, 3 CTAs per SM) and thread r
+// the same way (1-D bulk copies; stages and CTAs per SM: see NST below) and thread r
 // walks row r's point and group table in shared memory, the float4 columns
 // rotated by r so that a quarter-warp's eight threads read eight different
 // bank groups (conflict-free at 128-byte rows); the own centroid's row comes
 // through L1/L2 in the same rotated order.
 constexpr int kSR = 128;   // rows per tile = threads per CTA
-constexpr int kSS = 2;     // stages
 
 __device__ __forceinline__ float sqrt_approx(float x) {
     float r;
@@ -434,9 +433,15 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     return r;
 }
 
-template <int DP>
-__global__ void __launch_bounds__(kSR, 3) k_filter_tgy_srow(DevState S, int64_t* stat) {
+// NST = 2: two stages per CTA, three CTAs per SM, a tile's label-indexed loads
+// requested at its start.  NST = 3: three stages, two CTAs per SM, and the
+// next tile's label-indexed loads (its stage has landed while the previous
+// tile ran) requested before this tile's math, so no tile starts with an L2
+// round trip.
+template <int DP, int NST>
+__global__ void __launch_bounds__(kSR, NST == 2 ? 3 : 2) k_filter_tgy_srow(DevState S, int64_t* stat) {
     if (*S.done) return;
+    constexpr int kSS = NST;
     extern __shared__ __align__(128) uint8_t fsm[];
     __shared__ uint64_t fbar[kSS];
     __shared__ int qrow[kSR / 32][kQB];
@@ -500,26 +505,50 @@ __global__ void __launch_bounds__(kSR, 3) k_filter_tgy_srow(DevState S, int64_t*
     if (tid < 32 && tid >= G) dg[tid] = -INFINITY;
     __syncthreads();
     const float rho1 = 1.0f + rho + 4.76837158203125e-07f;  // (+ 2^-21: the approximate square roots)
+    // everything indexed by a row's label, requested at once (one L2 round
+    // trip); rows that pass the global gate (16% at cfg5) load it in vain
+    struct ByLabel {
+        float4 cv[8];
+        float dca, sa, cna;
+        int ga, a;
+    };
+    auto by_label = [&](int a_, ByLabel& L) {
+        const float4* cp = reinterpret_cast<const float4*>(S.C32 + (int64_t)a_ * S.ldc);
+#pragma unroll
+        for (int c = 0; c < 8; c++) L.cv[c] = __ldg(cp + ((c + tid) & 7));
+        L.dca = __ldg(S.dcum + a_);
+        L.sa = __ldg(S.s_half + a_);
+        L.cna = __ldg(S.cnorm + a_);
+        L.ga = __ldg(S.group_of + a_);
+        L.a = a_;
+    };
+    ByLabel cur, nxt;
+    if (NST >= 3 && n_my > 0) {
+        mbar_wait(&fbar[0], 0);
+        by_label(reinterpret_cast<const int*>(fsm)[tid], cur);
+    }
     for (int64_t j = 0; j < n_my; j++) {
         const int st_ = (int)(j % kSS);
         const int64_t i = (blockIdx.x + j * gridDim.x) * (int64_t)kSR + tid;
-        mbar_wait(&fbar[st_], (uint32_t)((j / kSS) & 1));
+        if (NST >= 3) {
+            if (j + 1 < n_my) {
+                const int s1 = (int)((j + 1) % kSS);
+                mbar_wait(&fbar[s1], (uint32_t)(((j + 1) / kSS) & 1));
+                by_label(reinterpret_cast<const int*>(fsm + (size_t)s1 * SB)[tid], nxt);
+            }
+        } else {
+            mbar_wait(&fbar[st_], (uint32_t)((j / kSS) & 1));
+        }
         const uint8_t* b = fsm + (size_t)st_ * SB;
-        const int a = reinterpret_cast<const int*>(b)[tid];
+        if (NST < 3) by_label(reinterpret_cast<const int*>(b)[tid], cur);
+        const int a = cur.a;
         const float ub_s = reinterpret_cast<const float*>(b + kSR * 4)[tid];
         const float glb_s = reinterpret_cast<const float*>(b + kSR * 8)[tid];
         const float4* spt = reinterpret_cast<const float4*>(b + kSR * 12) + tid * 8;
         const float4* slb = reinterpret_cast<const float4*>(b + kSR * (12 + 4 * 32)) + tid * 8;
-        // everything indexed by the label is requested at once (one L2 round
-        // trip); rows that pass the global gate (16% at cfg5) load it in vain
-        const float4* cp = reinterpret_cast<const float4*>(S.C32 + (int64_t)a * S.ldc);
-        float4 cv[8];
-#pragma unroll
-        for (int c = 0; c < 8; c++) cv[c] = __ldg(cp + ((c + tid) & 7));
-        const float dca = __ldg(S.dcum + a);
-        const float sa = __ldg(S.s_half + a);
-        const float cna = __ldg(S.cnorm + a);
-        const int ga = __ldg(S.group_of + a);
+        const float4 (&cv)[8] = cur.cv;
+        const float dca = cur.dca, sa = cur.sa, cna = cur.cna;
+        const int ga = cur.ga;
         // tighten (fp32 difference form, certified)
         float acc = 0.f, xn2 = 0.f;
 #pragma unroll
@@ -566,6 +595,7 @@ __global__ void __launch_bounds__(kSR, 3) k_filter_tgy_srow(DevState S, int64_t*
         append(need, i, mask, lun, a);
         __syncthreads();  // stage st_ consumed
         if (tid == 0 && j + kSS < n_my) issue(j + kSS, st_);
+        if (NST >= 3) cur = nxt;
     }
     // rows past the last full tile: one thread per row from global memory
     if (blockIdx.x == gridDim.x - 1) {
@@ -610,15 +640,25 @@ lk_status launch_filter_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaS
     }();
     const bool bulk_ok = S.nlb % 4 == 0 && S.ldx % 4 == 0;
     if (bulk_ok && S.nlb == 32 && S.ldx == 32 && (variant == 4 || variant == 1)) {
-        // the streaming pipeline, a thread per row: three CTAs per SM
-        const int smem = lk::tgy::kSS * lk::tgy::kSR * (12 + 4 * S.ldx + 4 * S.nlb);
+        // the streaming pipeline, a thread per row (LK_TGY_STAGES, A/B knob: 3
+        // stages and two CTAs per SM, or 2 stages and three CTAs per SM)
+        static const int nst = [] {
+            const char* e = getenv("LK_TGY_STAGES");
+            return (e && atoi(e) == 2) ? 2 : 3;
+        }();
+        const int smem = nst * lk::tgy::kSR * (12 + 4 * S.ldx + 4 * S.nlb);
         static bool attr4 = false;
         if (!attr4) {
-            LK_CUDA_CHECK(cudaFuncSetAttribute(lk::tgy::k_filter_tgy_srow<32>,
+            LK_CUDA_CHECK(cudaFuncSetAttribute(lk::tgy::k_filter_tgy_srow<32, 2>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024));
+            LK_CUDA_CHECK(cudaFuncSetAttribute(lk::tgy::k_filter_tgy_srow<32, 3>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 108 * 1024));
             attr4 = true;
         }
-        lk::tgy::k_filter_tgy_srow<32><<<(unsigned)(sms * 3), lk::tgy::kSR, smem, st>>>(S, stat);
+        if (nst == 2)
+            lk::tgy::k_filter_tgy_srow<32, 2><<<(unsigned)(sms * 3), lk::tgy::kSR, smem, st>>>(S, stat);
+        else
+            lk::tgy::k_filter_tgy_srow<32, 3><<<(unsigned)(sms * 2), lk::tgy::kSR, smem, st>>>(S, stat);
     } else if (bulk_ok && (variant == 2 || variant == 5)) {
         // the streaming pipeline: one wave of two CTAs per SM
         constexpr int kMaxSmem = 110 * 1024;
