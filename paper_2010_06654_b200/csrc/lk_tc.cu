@@ -1254,21 +1254,40 @@ __global__ void __launch_bounds__(320, 1)
                     m8[7] = m21[21];
                     const float mc = fmin3(fmin3(m8[0], m8[1], m8[2]), fmin3(m8[3], m8[4], m8[5]),
                                            fminf(m8[6], m8[7]));
-                    if (__any_sync(LK_FULL_MASK, mc < b2)) {
-                        float a1 = b1, a2 = b2, e1 = INFINITY, e2 = INFINITY;
+                    // (as in k_assign_tgy: a chunk that does not beat the row's best
+                    // only offers its minimum as a second best; the chunk's exact
+                    // top-2, a merge tree, runs only under a new best)
+                    if (!__any_sync(LK_FULL_MASK, mc < b1)) {
+                        b2 = fminf(b2, mc);
+                    } else {
+                        float g1v[8], g2v[8];
 #pragma unroll
-                        for (int pp = 0; pp < 32; pp += 2) {
-                            const float lo0 = fminf(dv[2 * pp], dv[2 * pp + 1]);
-                            const float hi0 = fmaxf(dv[2 * pp], dv[2 * pp + 1]);
-                            a2 = fmin3(fmaxf(a1, lo0), a2, hi0);
-                            a1 = fminf(a1, lo0);
-                            const float lo1 = fminf(dv[2 * pp + 2], dv[2 * pp + 3]);
-                            const float hi1 = fmaxf(dv[2 * pp + 2], dv[2 * pp + 3]);
-                            e2 = fmin3(fmaxf(e1, lo1), e2, hi1);
-                            e1 = fminf(e1, lo1);
+                        for (int g8 = 0; g8 < 8; g8++) {
+                            float lo[4], hi[4];
+#pragma unroll
+                            for (int pp = 0; pp < 4; pp++) {
+                                lo[pp] = fminf(dv[8 * g8 + 2 * pp], dv[8 * g8 + 2 * pp + 1]);
+                                hi[pp] = fmaxf(dv[8 * g8 + 2 * pp], dv[8 * g8 + 2 * pp + 1]);
+                            }
+                            const float l01 = fminf(lo[0], lo[1]), h01 = fmin3(fmaxf(lo[0], lo[1]), hi[0], hi[1]);
+                            const float l23 = fminf(lo[2], lo[3]), h23 = fmin3(fmaxf(lo[2], lo[3]), hi[2], hi[3]);
+                            g1v[g8] = fminf(l01, l23);
+                            g2v[g8] = fmin3(fmaxf(l01, l23), h01, h23);
                         }
-                        b2 = fmin3(fmaxf(a1, e1), a2, e2);
-                        b1 = fminf(a1, e1);
+#pragma unroll
+                        for (int w2 = 4; w2 >= 1; w2 >>= 1)
+#pragma unroll
+                            for (int pp = 0; pp < w2; pp++) {
+                                const float l = fminf(g1v[pp], g1v[pp + w2]);
+                                g2v[pp] = fmin3(fmaxf(g1v[pp], g1v[pp + w2]), g2v[pp], g2v[pp + w2]);
+                                g1v[pp] = l;
+                            }
+                        if (g1v[0] < b1) {
+                            b2 = fminf(b1, g2v[0]);
+                            b1 = g1v[0];
+                        } else {
+                            b2 = fminf(b2, g1v[0]);
+                        }
                         const bool imp = b1 < bv;
                         if (__any_sync(LK_FULL_MASK, imp)) {
                             int found = -1;

@@ -640,11 +640,13 @@ lk_status launch_filter_tgy(const lk::DevState& S, int64_t* stat, int sms, cudaS
     }();
     const bool bulk_ok = S.nlb % 4 == 0 && S.ldx % 4 == 0;
     if (bulk_ok && S.nlb == 32 && S.ldx == 32 && (variant == 4 || variant == 1)) {
-        // the streaming pipeline, a thread per row (LK_TGY_STAGES, A/B knob: 3
-        // stages and two CTAs per SM, or 2 stages and three CTAs per SM)
+        // the streaming pipeline, a thread per row (LK_TGY_STAGES, A/B knob: 2
+        // stages and three CTAs per SM -- the default: 3.7 ms on cfg5 -- or 3
+        // stages and two CTAs per SM with the next tile's label-indexed loads
+        // prefetched: 4.2 ms, eight warps per SM hide less than the prefetch saves)
         static const int nst = [] {
             const char* e = getenv("LK_TGY_STAGES");
-            return (e && atoi(e) == 2) ? 2 : 3;
+            return (e && atoi(e) == 3) ? 3 : 2;
         }();
         const int smem = nst * lk::tgy::kSR * (12 + 4 * S.ldx + 4 * S.nlb);
         static bool attr4 = false;
