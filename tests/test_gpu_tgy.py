@@ -119,6 +119,41 @@ def test_group_tiles_off_knob():
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
 
 
+TGY_CASE = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
+from oracle import oracle
+import paper_2010_06654_b200 as m
+from paper_2010_06654_b200 import datasets
+from test_gpu_parity import check_trajectory, centroid_ok
+x = datasets.generate("cfg5", 40000)
+k = 4096
+init = m.make_init(m.RunContext(seed=31), x, k, "random")
+ref = oracle.run_lloyd(x, k, init, 6)
+res = m.run_pruner(x, k, "yinyang", init=init, t_max=6)
+check_trajectory(oracle, x, init, res.assign_history, ref["history"], "group-tile variant")
+assert centroid_ok(res.centroids, ref["centroids"], x)
+assert len(res.iterations) == ref["iterations"]
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env_set", [{"LK_TGY_FILTER": "0"}, {"LK_TGY_FILTER": "2"}, {"LK_TGY_FILTER": "3"},
+                                     {"LK_TGY_STAGES": "3"}, {"LK_TGY_BUCKET": "1"}])
+def test_group_tile_variants(env_set):
+    """The group-tile path's A/B knobs -- the filter from global memory
+    (LK_TGY_FILTER=0 / 3), the 8-lanes-per-row streaming filter (2), the
+    three-stage streaming filter (LK_TGY_STAGES=3), the mask-bucket partition
+    of the worklist before the label sort (LK_TGY_BUCKET=1) -- all land on the
+    oracle's trajectory at the cfg5 shape (d = 32, k = 4096)."""
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tests = os.path.join(repo, "tests")
+    env = dict(os.environ, **env_set)
+    r = subprocess.run([sys.executable, "-c", TGY_CASE.format(repo=repo, tests=tests)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
 @pytest.mark.parametrize("d,kernel", [(2, "simt"), (16, "simt"), (32, "simt"), (40, "auto")])
 def test_regroup_rebuilds_groups_and_matches_oracle(oracle, d, kernel):
     """Regroup (pruners.py:500-504): the device rebuilds the group map after
