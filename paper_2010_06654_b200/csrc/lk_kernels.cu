@@ -890,23 +890,28 @@ __global__ void __launch_bounds__(kThreads) k_update_centroids(DevState S, const
 // 64 x 64 (j, j') tiles per block, 4 x 4 pairs per thread, d streamed in
 // chunks of 32 through shared memory; per-j minima combined with atomicMin
 // on the (nonnegative) float bits.  s_half must be +inf-filled beforehand.
-constexpr int kHsT = 64;
 constexpr int kHsDC = 32;
 
+// P x P pairs per thread: tiles of T = 16 P centroids (P = 4: 64 x 64 tiles; small k
+// takes smaller tiles so that the grid still fills the GPU -- k = 256 is 16
+// blocks of 64 x 64 but 256 of 16 x 16).  The sum over d of a pair runs in the
+// same order whatever P, so s_half does not depend on it.
+template <int P>
 __device__ __forceinline__ void half_sep_tile(const DevState& S, int tj, int tjp) {
-    __shared__ float ta[kHsDC][kHsT + 4];
-    __shared__ float tb[kHsDC][kHsT + 4];
-    const int j0 = tj * kHsT, jp0 = tjp * kHsT;
+    constexpr int T = 16 * P;
+    __shared__ float ta[kHsDC][T + 4];
+    __shared__ float tb[kHsDC][T + 4];
+    const int j0 = tj * T, jp0 = tjp * T;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads
-    float acc[4][4];
+    float acc[P][P];
 #pragma unroll
-    for (int a = 0; a < 4; a++)
+    for (int a = 0; a < P; a++)
 #pragma unroll
-        for (int b = 0; b < 4; b++) acc[a][b] = 0.f;
+        for (int b = 0; b < P; b++) acc[a][b] = 0.f;
     for (int z0 = 0; z0 < S.d; z0 += kHsDC) {
         const int zn = min(kHsDC, S.d - z0);  // (short rows: only the real dimensions)
         __syncthreads();
-        for (int e = threadIdx.x; e < kHsT * zn; e += kThreads) {
+        for (int e = threadIdx.x; e < T * zn; e += kThreads) {
             int r = e / zn, z = e % zn;
             int zz = z0 + z;
             ta[z][r] = (j0 + r < S.k) ? S.C32[(int64_t)(j0 + r) * S.ldc + zz] : 0.f;
@@ -915,15 +920,15 @@ __device__ __forceinline__ void half_sep_tile(const DevState& S, int tj, int tjp
         __syncthreads();
 #pragma unroll 8
         for (int z = 0; z < zn; z++) {
-            float av[4], bv[4];
+            float av[P], bv[P];
 #pragma unroll
-            for (int a = 0; a < 4; a++) av[a] = ta[z][ty + 16 * a];
+            for (int a = 0; a < P; a++) av[a] = ta[z][ty + 16 * a];
 #pragma unroll
-            for (int b = 0; b < 4; b++) bv[b] = tb[z][tx + 16 * b];
+            for (int b = 0; b < P; b++) bv[b] = tb[z][tx + 16 * b];
 #pragma unroll
-            for (int a = 0; a < 4; a++)
+            for (int a = 0; a < P; a++)
 #pragma unroll
-                for (int b = 0; b < 4; b++) {
+                for (int b = 0; b < P; b++) {
                     float t = av[a] - bv[b];
                     acc[a][b] = fmaf(t, t, acc[a][b]);
                 }
@@ -931,13 +936,13 @@ __device__ __forceinline__ void half_sep_tile(const DevState& S, int tj, int tjp
     }
     const float rho = simt_rel_err(S.d);
 #pragma unroll
-    for (int a = 0; a < 4; a++) {
+    for (int a = 0; a < P; a++) {
         const int j = j0 + ty + 16 * a;
         float best = INFINITY;
         if (j < S.k) {
             const float cj = S.cnorm[j];
 #pragma unroll
-            for (int b = 0; b < 4; b++) {
+            for (int b = 0; b < P; b++) {
                 const int jp = jp0 + tx + 16 * b;
                 if (jp < S.k && jp != j) {
                     float lbd = (sqrtf(acc[a][b]) - kU32 * (cj + S.cnorm[jp])) * (1.0f - rho);
@@ -952,11 +957,12 @@ __device__ __forceinline__ void half_sep_tile(const DevState& S, int tj, int tjp
     }
 }
 
+template <int P>
 __global__ void __launch_bounds__(kThreads) k_half_sep(DevState S) {
     pdl_wait();
     pdl_trigger();
     if (*S.done) return;
-    half_sep_tile(S, blockIdx.y, blockIdx.x);
+    half_sep_tile<P>(S, blockIdx.y, blockIdx.x);
 }
 
 // Label history as a log: the moved rows of iteration t with their new label
@@ -1250,8 +1256,18 @@ lk_status launch_update(const DevState& S, const double* qscale, const double* q
     LK_CUDA_CHECK(lk::launch_pdl(k_update_centroids, dim3(grid), dim3(kThreads), 0, st, S, qscale, qinv, sse_part));
     LK_LAUNCH_CHECK();
     if (need_half) {
-        dim3 g((S.k + kHsT - 1) / kHsT, (S.k + kHsT - 1) / kHsT);
-        LK_CUDA_CHECK(lk::launch_pdl(k_half_sep, g, dim3(kThreads), 0, st, S));
+        // the largest tile whose grid still has >= 128 blocks (else 16 x 16 tiles)
+        auto blocks = [&](int T) { const int g = (S.k + T - 1) / T; return g * g; };
+        if (blocks(64) >= 128) {
+            dim3 g((S.k + 63) / 64, (S.k + 63) / 64);
+            LK_CUDA_CHECK(lk::launch_pdl(k_half_sep<4>, g, dim3(kThreads), 0, st, S));
+        } else if (blocks(32) >= 128) {
+            dim3 g((S.k + 31) / 32, (S.k + 31) / 32);
+            LK_CUDA_CHECK(lk::launch_pdl(k_half_sep<2>, g, dim3(kThreads), 0, st, S));
+        } else {
+            dim3 g((S.k + 15) / 16, (S.k + 15) / 16);
+            LK_CUDA_CHECK(lk::launch_pdl(k_half_sep<1>, g, dim3(kThreads), 0, st, S));
+        }
         LK_LAUNCH_CHECK();
     }
     return LK_OK;
